@@ -1,0 +1,192 @@
+/*
+ * tor_capi.h -- C ABI of the B200 Torontonian engine (libtor_b200.so).
+ *
+ * Drop-in boundary for the reference's hot path (torfp, /root/reference/proj):
+ *
+ *   reference C++ entry point                                      replaced by
+ *   ---------------------------------------------------------------------------------
+ *   TorontonianResult torontonian(const InputMatrix&,              tor_torontonian
+ *       PrecisionChoice = Auto, int workers = 0)
+ *       (include/torfp/torontonian.hpp:50-51, src/torontonian.cpp:151-177)
+ *   double torontonian_reference(const InputMatrix&)               tor_torontonian_reference
+ *       (torontonian.hpp:55, torontonian.cpp:179-200)
+ *   PrecisionConfig select_precision(const InputMatrix&, int N,    tor_select_precision
+ *       int sig = 3, double alpha = 0.5)
+ *       (precision.hpp:66-67, precision.cpp:80-121)
+ *   PrecisionConfig force_width(const InputMatrix&, int width)     tor_force_width
+ *       (precision.hpp:71, precision.cpp:123-148)
+ *   Wide<W> torontonian_partial<W>(a, WorkAssignment, cfg, ops)    tor_torontonian_slice
+ *       (torontonian.hpp:43-45, torontonian.cpp:72-103)             (prefix-class shards)
+ *   double det_i_minus_a_float(const InputMatrix&)                 tor_det_i_minus_a
+ *       (precision.hpp:61, precision.cpp:34-36)
+ *   SymmetryReport check_symmetries(dense, 2N)                     tor_check_symmetries
+ *       (matrix_io.hpp:64, matrix_io.cpp:285-305)
+ *   double probability(a_full, ClickPattern, workers)              tor_probability
+ *       (torontonian.hpp:60, torontonian.cpp:202-209)
+ *   (new) many-instance throughput path, BASELINE config 3         tor_torontonian_batch
+ *   (new) fixed-order fold of shard partials (multi-GPU)           tor_fold_partials
+ *
+ * Conventions
+ *   - Input: InputMatrix (matrix_io.hpp:18-26): two upper triangles of n(n+1)/2
+ *     complex entries, row-major, index i*n - i(i+1)/2 + j, interleaved (re, im)
+ *     doubles.  Caller-owned, read-only for the call.
+ *   - Subset masks follow the reference (subsets.hpp:11-13): bit N-1-j = mode j.
+ *     Prefix classes are the top `class_bits` bits of that mask.
+ *   - No exceptions cross the ABI.  Every entry point returns a status (TOR_OK or
+ *     one of TOR_E_*), mapped 1:1 onto the reference's error classes
+ *     (errors.hpp:13-78), and fills *err (may be NULL) with the same stable
+ *     "module/kind" code strings the reference throws.
+ *   - Reentrant.  No hidden global state besides a per-device context cache
+ *     guarded by a mutex.  `devices` replaces the reference's `workers`.
+ */
+#ifndef TOR_CAPI_H
+#define TOR_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TOR_ABI_VERSION 1
+
+/* status codes (errors.hpp class -> code) */
+#define TOR_OK 0
+#define TOR_E_INVALID 1   /* InvalidArgument */
+#define TOR_E_BREAKDOWN 2 /* BreakdownError (non-positive pivot) */
+#define TOR_E_PRECISION 3 /* PrecisionError */
+#define TOR_E_PARSE 4     /* ParseError */
+#define TOR_E_RESOURCE 5  /* ResourceError */
+#define TOR_E_DEVICE 6    /* CUDA / NCCL failure (no reference counterpart) */
+#define TOR_E_ERROR 7     /* plain Error, e.g. "torontonian/symmetry" */
+
+/* precision selector: PrecisionChoice {Auto, Bits128, Bits256} (torontonian.hpp:31)
+ * plus the fp64 oracle path.  128-bit -> double-double, 256-bit -> quad-double. */
+typedef enum {
+    TOR_PREC_AUTO = 0,
+    TOR_PREC_W128_DD = 1,
+    TOR_PREC_W256_QD = 2,
+    TOR_PREC_FP64 = 3
+} tor_precision;
+
+typedef struct {
+    int n;                   /* modes N (InputMatrix::n_modes) */
+    const double* a00_upper; /* n(n+1)/2 complex, interleaved (re, im): A00, Hermitian */
+    const double* a01_upper; /* n(n+1)/2 complex, interleaved (re, im): A01, symmetric */
+} tor_input;
+
+/* PrecisionConfig (precision.hpp:17-29) */
+typedef struct {
+    int width_bits;
+    unsigned frac_bits;
+    int b_lower;
+    int b_upper;
+    int b_sgn;
+    int b_accum;
+    double a_repr;
+    double k_corr;
+    double alpha;
+} tor_precision_config;
+
+typedef struct {
+    char code[48];      /* "module/kind", as the reference's Error::code() */
+    char message[200];
+    int64_t pivot_row;  /* BreakdownError::pivot_row (pair order 2k: x_k, 2k+1: p_k), -1 n/a */
+    uint64_t subset_mask; /* BreakdownError::subset_mask (reference convention), 0 n/a */
+} tor_error;
+
+/* TorontonianResult (torontonian.hpp:21-29) extended with the multi-word value and
+ * the posterior cancellation check of the adaptive driver. */
+typedef struct {
+    double value;             /* nearest double of the multi-word sum */
+    int mode;                 /* tor_precision actually used (never AUTO) */
+    int width_bits;           /* 64 (fp64), 128 (DD) or 256 (QD) */
+    int nwords;               /* significant words in `words` (1, 2 or 4) */
+    double words[4];          /* unevaluated-sum value, leading word first */
+    tor_precision_config config; /* select_precision / force_width outcome */
+    uint64_t term_count;      /* 2^N (or the slice's share) */
+    /* OpCounters (linalg.hpp:44-57) as closed-form equivalents of the reference's
+     * per-subset elimination: mults + adds = Eq. 8, recips = sum C(n,z)(2z-1),
+     * rsqrts = 2^n - 1 */
+    uint64_t mults, adds, recips, rsqrts;
+    double wall_seconds;      /* host-to-result wall time of the call */
+    double device_ms;         /* device time of the engine pipeline (CUDA events) */
+    double kernel_ms;         /* device time of the subtree kernel */
+    int devices;              /* GPUs used */
+    int escalated;            /* 1 when the adaptive driver re-ran DD as QD */
+    double sum_abs_terms;     /* sum over subsets of |term| (fp64) */
+    double cancellation_bits; /* log2(sum|t| / |Tor|) */
+    double bits_left;         /* mantissa - cancellation - growth allowance */
+    uint64_t kernel_launches; /* device kernels launched by the call */
+} tor_result;
+
+/* Shard partial for multi-GPU / multi-process folds: a contiguous, power-of-two
+ * aligned range of prefix classes reduced along the engine's fixed binary tree. */
+typedef struct {
+    int mode;
+    int class_bits;
+    uint64_t class_lo, class_hi;
+    double words[4];
+    double sum_abs;
+    uint64_t term_count;
+} tor_partial;
+
+/* ------------------------------------------------------------------ API -- */
+int tor_abi_version(void);
+
+/* check_symmetries with the reference's 1e-12 gate; devs = {hermitian, a01_sym,
+ * block_conj}. */
+int tor_check_symmetries(const tor_input* in, double devs[3], int* pass, tor_error* err);
+
+/* Same gate on a dense 2N x 2N complex matrix (interleaved), as from_dense. */
+int tor_check_dense(int two_n, const double* dense, double devs[3], int* pass, tor_error* err);
+
+/* det(I - A) in floating point, reference elimination order (precision.cpp:34). */
+int tor_det_i_minus_a(const tor_input* in, double* det, tor_error* err);
+
+int tor_select_precision(const tor_input* in, int N, int sig_decimal_digits, double alpha,
+                         tor_precision_config* out, tor_error* err);
+int tor_force_width(const tor_input* in, int width_bits, tor_precision_config* out, tor_error* err);
+
+/* Full evaluation (validation N in [1,40], symmetry gate, precision selection,
+ * adaptive escalation, device evaluation).  devices == NULL / ndev <= 0: device 0. */
+int tor_torontonian(const tor_input* in, tor_precision prec, const int* devices, int ndev,
+                    tor_result* out, tor_error* err);
+
+/* fp64 oracle semantics (N <= 20, PrecisionError "torontonian/nonfinite"), computed
+ * on the device by the same engine in fp64. */
+int tor_torontonian_reference(const tor_input* in, double* value, tor_error* err);
+
+/* `count` instances of equal N in one device pass (BASELINE config 3). */
+int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, int device,
+                          tor_result* outs, tor_error* err);
+
+/* Partial sum over prefix classes [class_lo, class_hi) of the top class_bits mask
+ * bits on one device (the subset of torontonian_partial's masks with those
+ * prefixes).  prec must not be AUTO. */
+int tor_torontonian_slice(const tor_input* in, tor_precision prec, int class_bits, uint64_t class_lo,
+                          uint64_t class_hi, int device, tor_partial* out, tor_error* err);
+
+/* Rank `rank` of `world` (power of two) evaluates its aligned share of the 2^k
+ * top-level classes. */
+int tor_torontonian_shard(const tor_input* in, tor_precision prec, int rank, int world, int device,
+                          tor_partial* out, tor_error* err);
+
+/* Fold shard partials (sorted by class_lo, contiguous, power-of-two aligned) along
+ * the engine's fixed tree; bit-identical to a single-device run. */
+int tor_fold_partials(const tor_partial* parts, int count, const tor_input* in, tor_result* out,
+                      tor_error* err);
+
+/* p(S) = Tor(A_S) sqrt(det(I - A)) (torontonian.cpp:202-209); pattern bit k = mode k. */
+int tor_probability(const tor_input* full, uint64_t pattern_bits, tor_precision prec, int device,
+                    double* p, tor_error* err);
+
+/* Number of CUDA devices visible (0 without a GPU). */
+int tor_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TOR_CAPI_H */

@@ -1,0 +1,288 @@
+"""Python mirror of the reference's ``torfp`` API for the hot path, over the C ABI.
+
+Same names, argument meaning, result-dict keys and error behaviour as the
+reference's pybind module (python/bindings.cpp:104-205, python/torfp/__init__.py),
+but every evaluation runs on the GPU through ``libtor_b200.so``
+(include/tor_capi.h).  There is no CPU fallback: a missing library or a missing
+GPU raises (DeviceError / OSError), it never silently computes elsewhere.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+
+from . import errors as E
+from .matrix import InputMatrix
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libtor_b200.so")
+
+PREC_AUTO, PREC_DD, PREC_QD, PREC_FP64 = 0, 1, 2, 3
+_PREC = {"auto": PREC_AUTO, "128": PREC_DD, "dd": PREC_DD, "256": PREC_QD, "qd": PREC_QD,
+         "fp64": PREC_FP64, "64": PREC_FP64}
+_MODE_NAME = {PREC_DD: "dd", PREC_QD: "qd", PREC_FP64: "fp64"}
+
+
+class TorInput(C.Structure):
+    _fields_ = [("n", C.c_int), ("a00_upper", C.POINTER(C.c_double)), ("a01_upper", C.POINTER(C.c_double))]
+
+
+class TorPrecisionConfig(C.Structure):
+    _fields_ = [("width_bits", C.c_int), ("frac_bits", C.c_uint), ("b_lower", C.c_int), ("b_upper", C.c_int),
+                ("b_sgn", C.c_int), ("b_accum", C.c_int), ("a_repr", C.c_double), ("k_corr", C.c_double),
+                ("alpha", C.c_double)]
+
+
+class TorError(C.Structure):
+    _fields_ = [("code", C.c_char * 48), ("message", C.c_char * 200), ("pivot_row", C.c_int64),
+                ("subset_mask", C.c_uint64)]
+
+
+class TorResult(C.Structure):
+    _fields_ = [("value", C.c_double), ("mode", C.c_int), ("width_bits", C.c_int), ("nwords", C.c_int),
+                ("words", C.c_double * 4), ("config", TorPrecisionConfig), ("term_count", C.c_uint64),
+                ("mults", C.c_uint64), ("adds", C.c_uint64), ("recips", C.c_uint64), ("rsqrts", C.c_uint64),
+                ("wall_seconds", C.c_double), ("device_ms", C.c_double), ("kernel_ms", C.c_double),
+                ("devices", C.c_int), ("escalated", C.c_int), ("sum_abs_terms", C.c_double),
+                ("cancellation_bits", C.c_double), ("bits_left", C.c_double), ("kernel_launches", C.c_uint64)]
+
+
+class TorPartial(C.Structure):
+    _fields_ = [("mode", C.c_int), ("class_bits", C.c_int), ("class_lo", C.c_uint64), ("class_hi", C.c_uint64),
+                ("words", C.c_double * 4), ("sum_abs", C.c_double), ("term_count", C.c_uint64)]
+
+
+# every symbol include/tor_capi.h declares (checked by tests/test_capi.py)
+EXPORTS = ("tor_abi_version", "tor_check_symmetries", "tor_check_dense", "tor_det_i_minus_a",
+           "tor_select_precision", "tor_force_width", "tor_torontonian", "tor_torontonian_reference",
+           "tor_torontonian_batch", "tor_torontonian_slice", "tor_torontonian_shard", "tor_fold_partials",
+           "tor_probability", "tor_device_count")
+
+_lib = None
+
+
+def lib():
+    """Load libtor_b200.so (fails loudly when it is missing)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise OSError(f"{LIB_PATH} is not built; run __graft_entry__.build() "
+                          "(python -m paper_2009_01177_b200._build)")
+        L = C.CDLL(LIB_PATH)
+        P = C.POINTER
+        L.tor_torontonian.argtypes = [P(TorInput), C.c_int, P(C.c_int), C.c_int, P(TorResult), P(TorError)]
+        L.tor_torontonian_reference.argtypes = [P(TorInput), P(C.c_double), P(TorError)]
+        L.tor_torontonian_batch.argtypes = [P(TorInput), C.c_int, C.c_int, C.c_int, P(TorResult), P(TorError)]
+        L.tor_torontonian_slice.argtypes = [P(TorInput), C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int,
+                                            P(TorPartial), P(TorError)]
+        L.tor_torontonian_shard.argtypes = [P(TorInput), C.c_int, C.c_int, C.c_int, C.c_int, P(TorPartial),
+                                            P(TorError)]
+        L.tor_fold_partials.argtypes = [P(TorPartial), C.c_int, P(TorInput), P(TorResult), P(TorError)]
+        L.tor_select_precision.argtypes = [P(TorInput), C.c_int, C.c_int, C.c_double, P(TorPrecisionConfig),
+                                           P(TorError)]
+        L.tor_force_width.argtypes = [P(TorInput), C.c_int, P(TorPrecisionConfig), P(TorError)]
+        L.tor_check_symmetries.argtypes = [P(TorInput), P(C.c_double), P(C.c_int), P(TorError)]
+        L.tor_check_dense.argtypes = [C.c_int, P(C.c_double), P(C.c_double), P(C.c_int), P(TorError)]
+        L.tor_det_i_minus_a.argtypes = [P(TorInput), P(C.c_double), P(TorError)]
+        L.tor_probability.argtypes = [P(TorInput), C.c_uint64, C.c_int, C.c_int, P(C.c_double), P(TorError)]
+        _lib = L
+    return _lib
+
+
+class _In:
+    """Keeps the interleaved arrays alive while the C side reads them."""
+
+    def __init__(self, m: InputMatrix):
+        self.a00, self.a01 = m.interleaved()
+        self.s = TorInput(m.n_modes, self.a00.ctypes.data_as(C.POINTER(C.c_double)),
+                          self.a01.ctypes.data_as(C.POINTER(C.c_double)))
+
+
+def _check(status: int, err: TorError) -> None:
+    if status:
+        E.raise_for_status(status, err.code.decode(), err.message.decode(), int(err.pivot_row),
+                           int(err.subset_mask))
+
+
+def _prec(p) -> int:
+    key = str(p).lower()
+    if key not in _PREC:
+        raise E.InvalidArgument("precision/range", "precision must be auto, 128, 256 or fp64")
+    return _PREC[key]
+
+
+def _cfg_dict(c: TorPrecisionConfig) -> dict:
+    return dict(width_bits=c.width_bits, frac_bits=c.frac_bits, b_lower=c.b_lower, b_upper=c.b_upper,
+                b_sgn=c.b_sgn, b_accum=c.b_accum, a_repr=c.a_repr, k_corr=c.k_corr)
+
+
+def words_fraction(words) -> Fraction:
+    return sum((Fraction(float(w)) for w in words), Fraction(0))
+
+
+def raw_limbs(words, width_bits: int, frac_bits: int) -> tuple:
+    """The multi-word value re-quantised at the reference's scaling 2^-frac_bits as
+    two's-complement 64-bit limbs (low first, 4 entries like FixedValue::limbs)."""
+    if width_bits not in (128, 256):
+        return (0, 0, 0, 0)
+    v = words_fraction(words) * (1 << frac_bits)
+    q = math.floor(v + Fraction(1, 2))
+    q %= 1 << width_bits
+    return tuple((q >> (64 * i)) & ((1 << 64) - 1) if i < width_bits // 64 else 0 for i in range(4))
+
+
+def _result_dict(r: TorResult, workers: int) -> dict:
+    words = tuple(r.words[i] for i in range(4))
+    cfg = _cfg_dict(r.config)
+    return {
+        # reference keys (bindings.cpp:69-85)
+        "value": r.value,
+        "raw_limbs": raw_limbs(words, r.width_bits, cfg["frac_bits"]),
+        "width_bits": r.width_bits,
+        "config": cfg,
+        "term_count": r.term_count,
+        "counters": dict(mults=r.mults, adds=r.adds, recips=r.recips, rsqrts=r.rsqrts),
+        "wall_seconds": r.wall_seconds,
+        "workers": workers,
+        # engine extensions
+        "mode": _MODE_NAME.get(r.mode, "?"),
+        "words": words[: r.nwords] if r.nwords else words,
+        "device_ms": r.device_ms,
+        "kernel_ms": r.kernel_ms,
+        "devices": r.devices,
+        "escalated": bool(r.escalated),
+        "sum_abs_terms": r.sum_abs_terms,
+        "cancellation_bits": r.cancellation_bits,
+        "bits_left": r.bits_left,
+        "kernel_launches": r.kernel_launches,
+    }
+
+
+def torontonian(matrix: InputMatrix, precision="auto", workers: int = 0, devices=None) -> dict:
+    """Tor(A) (torontonian.cpp:151-177) on the GPU.  ``precision``: "auto" | "128" | "256"
+    (reference) or "fp64"; ``workers`` is accepted for drop-in compatibility (the
+    engine's parallelism is the GPU); ``devices`` lists CUDA device ids."""
+    inp = _In(matrix)
+    devs = list(devices) if devices else [0]
+    arr = (C.c_int * len(devs))(*devs)
+    r = TorResult()
+    err = TorError()
+    _check(lib().tor_torontonian(C.byref(inp.s), _prec(precision), arr, len(devs), C.byref(r), C.byref(err)), err)
+    return _result_dict(r, workers if workers > 0 else len(devs))
+
+
+def torontonian_reference(matrix: InputMatrix) -> float:
+    """fp64 oracle semantics (N <= 20) (torontonian.cpp:179-200), evaluated on the GPU."""
+    inp = _In(matrix)
+    v = C.c_double()
+    err = TorError()
+    _check(lib().tor_torontonian_reference(C.byref(inp.s), C.byref(v), C.byref(err)), err)
+    return v.value
+
+
+def torontonian_batch(matrices, precision="fp64", device: int = 0) -> list[dict]:
+    ins = [_In(m) for m in matrices]
+    arr = (TorInput * len(ins))(*[i.s for i in ins])
+    res = (TorResult * len(ins))()
+    err = TorError()
+    _check(lib().tor_torontonian_batch(arr, len(ins), _prec(precision), device, res, C.byref(err)), err)
+    return [_result_dict(res[i], 1) for i in range(len(ins))]
+
+
+def torontonian_slice(matrix: InputMatrix, precision, class_bits: int, class_lo: int, class_hi: int,
+                      device: int = 0) -> dict:
+    inp = _In(matrix)
+    p = TorPartial()
+    err = TorError()
+    _check(lib().tor_torontonian_slice(C.byref(inp.s), _prec(precision), class_bits, class_lo, class_hi, device,
+                                       C.byref(p), C.byref(err)), err)
+    return _partial_dict(p)
+
+
+def torontonian_shard(matrix: InputMatrix, precision, rank: int, world: int, device: int = 0) -> dict:
+    inp = _In(matrix)
+    p = TorPartial()
+    err = TorError()
+    _check(lib().tor_torontonian_shard(C.byref(inp.s), _prec(precision), rank, world, device, C.byref(p),
+                                       C.byref(err)), err)
+    return _partial_dict(p)
+
+
+def _partial_dict(p: TorPartial) -> dict:
+    return dict(mode=p.mode, class_bits=p.class_bits, class_lo=p.class_lo, class_hi=p.class_hi,
+                words=tuple(p.words[i] for i in range(4)), sum_abs=p.sum_abs, term_count=p.term_count)
+
+
+def partial_to_array(p: dict) -> np.ndarray:
+    """Shard partial as 10 float64 (for torch.distributed all_gather)."""
+    return np.array([p["mode"], p["class_bits"], p["class_lo"], p["class_hi"], *p["words"], p["sum_abs"],
+                     p["term_count"]], dtype=np.float64)
+
+
+def array_to_partial(a) -> dict:
+    a = [float(x) for x in a]
+    return dict(mode=int(a[0]), class_bits=int(a[1]), class_lo=int(a[2]), class_hi=int(a[3]),
+                words=tuple(a[4:8]), sum_abs=a[8], term_count=int(a[9]))
+
+
+def fold_partials(parts: list[dict], matrix: InputMatrix) -> dict:
+    parts = sorted(parts, key=lambda p: p["class_lo"])
+    arr = (TorPartial * len(parts))()
+    for i, p in enumerate(parts):
+        arr[i] = TorPartial(p["mode"], p["class_bits"], p["class_lo"], p["class_hi"], (C.c_double * 4)(*p["words"]),
+                            p["sum_abs"], p["term_count"])
+    inp = _In(matrix)
+    r = TorResult()
+    err = TorError()
+    _check(lib().tor_fold_partials(arr, len(parts), C.byref(inp.s), C.byref(r), C.byref(err)), err)
+    return _result_dict(r, len(parts))
+
+
+def select_precision(matrix: InputMatrix, n_modes: int | None = None, sig_decimal_digits: int = 3,
+                     alpha: float = 0.5) -> dict:
+    """select_precision (precision.cpp:80-121), host port with identical decisions."""
+    inp = _In(matrix)
+    c = TorPrecisionConfig()
+    err = TorError()
+    N = matrix.n_modes if n_modes is None else n_modes
+    _check(lib().tor_select_precision(C.byref(inp.s), N, sig_decimal_digits, alpha, C.byref(c), C.byref(err)), err)
+    return _cfg_dict(c)
+
+
+def force_width(matrix: InputMatrix, width_bits: int) -> dict:
+    inp = _In(matrix)
+    c = TorPrecisionConfig()
+    err = TorError()
+    _check(lib().tor_force_width(C.byref(inp.s), width_bits, C.byref(c), C.byref(err)), err)
+    return _cfg_dict(c)
+
+
+def det_i_minus_a(matrix: InputMatrix) -> float:
+    inp = _In(matrix)
+    v = C.c_double()
+    err = TorError()
+    _check(lib().tor_det_i_minus_a(C.byref(inp.s), C.byref(v), C.byref(err)), err)
+    return v.value
+
+
+def probability(matrix: InputMatrix, pattern_bits: int, workers: int = 0, precision="auto",
+                device: int = 0) -> float:
+    """p(S) = Tor(A_S) sqrt(det(I - A)) (torontonian.cpp:202-209); bit k = mode k."""
+    inp = _In(matrix)
+    v = C.c_double()
+    err = TorError()
+    _check(lib().tor_probability(C.byref(inp.s), pattern_bits, _prec(precision), device, C.byref(v),
+                                 C.byref(err)), err)
+    return v.value
+
+
+def probability_reference(matrix: InputMatrix, pattern_bits: int) -> float:
+    return probability(matrix, pattern_bits, precision="fp64")
+
+
+def device_count() -> int:
+    return lib().tor_device_count()

@@ -1,0 +1,402 @@
+// Multi-word floating-point arithmetic on FP64 FMA for the Torontonian engine.
+//
+// Replaces the reference's fixed-point Wide<W> limbs (fixed_point.hpp:27-160,
+// fixed_point.cpp:52-162): the 128-bit mode becomes double-double (DD, 2 x f64,
+// ~106-bit significand) and the 256-bit mode quad-double (QD, 4 x f64, ~212-bit),
+// both unevaluated sums built from error-free transformations (TwoSum, TwoProd
+// via DFMA).  Floating words keep RELATIVE precision, so the reference's
+// global-scaling failure modes (fixed-point BreakdownError on tiny pivots,
+// test_torontonian.cpp:218-244) do not occur; only a truly non-positive pivot
+// breaks down.
+//
+// Build contract: compiled with --fmad=false (device) / -ffp-contract=off (host),
+// so every `a*b + c` below is two roundings unless written as fma() explicitly.
+// The ops and their FP64 instruction counts are pinned in profiles/sass_counts.json.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+
+#if defined(__CUDACC__)
+#define TOR_HD __host__ __device__ __forceinline__
+#else
+#define TOR_HD inline
+#endif
+
+namespace tor {
+
+// ---------------------------------------------------------------- helpers --
+TOR_HD double fma_(double a, double b, double c) { return fma(a, b, c); }
+
+// Error-free transformations.
+TOR_HD void two_sum(double a, double b, double& s, double& e) {
+    s = a + b;
+    const double bb = s - a;
+    e = (a - (s - bb)) + (b - bb);
+}
+// Requires exponent(a) >= exponent(b) (or a == 0).
+TOR_HD void fast_two_sum(double a, double b, double& s, double& e) {
+    s = a + b;
+    e = b - (s - a);
+}
+TOR_HD void two_prod(double a, double b, double& p, double& e) {
+    p = a * b;
+    e = fma_(a, b, -p);
+}
+
+// Non-positive (or -0/+0) test on the high word: integer pipe, no FP64 issue slot.
+TOR_HD bool nonpositive(double x) {
+#if defined(__CUDA_ARCH__)
+    return __double2hiint(x) <= 0;
+#else
+    return !(x > 0.0);
+#endif
+}
+
+// Full-precision fp64 reciprocal square root for x > 0.
+TOR_HD double rsqrt_d(double x) {
+#if defined(__CUDA_ARCH__)
+    // MUFU.RSQ64H seed (~2^-23) then two Newton steps in fp64 -> ~1 ulp.
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double h = x * y;
+    double r = fma_(-h, y, 1.0);
+    y = fma_(0.5 * y, r, y);
+    h = x * y;
+    r = fma_(-h, y, 1.0);
+    y = fma_(0.5 * y, r, y);
+    return y;
+#else
+    return 1.0 / std::sqrt(x);
+#endif
+}
+
+// ===================================================================== DD ==
+struct dd {
+    double hi, lo;
+};
+
+TOR_HD dd dd_make(double x) { return dd{x, 0.0}; }
+
+// Renormalise an arbitrary (h, l) pair exactly (TwoSum: no ordering assumption).
+TOR_HD dd dd_norm(dd a) {
+    dd r;
+    two_sum(a.hi, a.lo, r.hi, r.lo);
+    return r;
+}
+
+TOR_HD dd dd_neg(dd a) { return dd{-a.hi, -a.lo}; }
+
+// Product of two DD values, normalised.  a may be unnormalised (h, l) with small l.
+TOR_HD dd dd_mul(dd a, dd b) {
+    double p, e;
+    two_prod(a.hi, b.hi, p, e);
+    e = fma_(a.hi, b.lo, e);
+    e = fma_(a.lo, b.hi, e);
+    dd r;
+    fast_two_sum(p, e, r.hi, r.lo);
+    return r;
+}
+
+// Accurate sum (both TwoSums, IEEE-style DD add): relative error ~2^-104 of the result.
+TOR_HD dd dd_add(dd a, dd b) {
+    double s, e, t, f;
+    two_sum(a.hi, b.hi, s, e);
+    two_sum(a.lo, b.lo, t, f);
+    e += t;
+    fast_two_sum(s, e, s, e);
+    e += f;
+    dd r;
+    fast_two_sum(s, e, r.hi, r.lo);
+    return r;
+}
+TOR_HD dd dd_sub(dd a, dd b) { return dd_add(a, dd_neg(b)); }
+
+// Lazy symmetric rank-2 update entry  s - a*b - c*d.  s may be unnormalised; the
+// result is the exact hi part of the TwoSum chain plus an un-renormalised lo.
+// Backward-stable at the DD level: |err| <= O(2^-105) (|s| + |ab| + |cd|).
+TOR_HD dd dd_rank2(dd s, dd a, dd b, dd c, dd d) {
+    double p1, e1, p2, e2, s1, f1, s2, f2;
+    two_prod(a.hi, b.hi, p1, e1);
+    two_prod(c.hi, d.hi, p2, e2);
+    two_sum(s.hi, -p1, s1, f1);
+    two_sum(s1, -p2, s2, f2);
+    double lo = s.lo + f1;
+    lo = lo + f2;
+    lo = lo - e1;
+    lo = lo - e2;
+    lo = fma_(-a.hi, b.lo, lo);
+    lo = fma_(-a.lo, b.hi, lo);
+    lo = fma_(-c.hi, d.lo, lo);
+    lo = fma_(-c.lo, d.hi, lo);
+    return dd{s2, lo};
+}
+// s - a*b (lazy, as above).
+TOR_HD dd dd_rank1(dd s, dd a, dd b) {
+    double p1, e1, s1, f1;
+    two_prod(a.hi, b.hi, p1, e1);
+    two_sum(s.hi, -p1, s1, f1);
+    double lo = s.lo + f1;
+    lo = lo - e1;
+    lo = fma_(-a.hi, b.lo, lo);
+    lo = fma_(-a.lo, b.hi, lo);
+    return dd{s1, lo};
+}
+
+// 1/sqrt(x) for normalised x > 0: fp64 seed + one DD Newton step on the exact
+// residual r = 1 - x*y^2 (y^2 exact by TwoProd).  Result is (y, y*r/2), |lo| <= ulp.
+TOR_HD dd dd_rsqrt(dd x) {
+    const double y = rsqrt_d(x.hi);
+    double p, pe;
+    two_prod(y, y, p, pe);
+    double r = fma_(-x.hi, p, 1.0);
+    r = fma_(-x.hi, pe, r);
+    r = fma_(-x.lo, p, r);
+    const double c = (0.5 * y) * r;
+    return dd{y, c};
+}
+
+// ===================================================================== QD ==
+// Four non-overlapping doubles x0 > x1 > x2 > x3 (Hida-Li-Bailey style algorithms,
+// restated from their published error-free-transformation formulation).
+struct qd {
+    double x[4];
+};
+
+TOR_HD qd qd_make(double a) { return qd{{a, 0.0, 0.0, 0.0}}; }
+TOR_HD qd qd_neg(qd a) { return qd{{-a.x[0], -a.x[1], -a.x[2], -a.x[3]}}; }
+
+// Branch-free renormalisation: two cascaded passes of TwoSum (exact for any
+// ordering), result non-overlapping up to a few ulps -- adequate for the engine's
+// 2^-180 budget and SIMT friendly (no data-dependent branches).
+TOR_HD qd qd_renorm5_bf(double c0, double c1, double c2, double c3, double c4) {
+    // pass 1: bottom-up accumulation
+    double e3, e2, e1, e0;
+    two_sum(c3, c4, c3, e3);
+    two_sum(c2, c3, c2, e2);
+    two_sum(c1, c2, c1, e1);
+    two_sum(c0, c1, c0, e0);
+    // now c0 holds the leading value; e0..e3 the errors in decreasing magnitude
+    double t0, t1, t2;
+    two_sum(e0, e1, t0, t1);
+    two_sum(t1, e2, t1, t2);
+    t2 += e3;
+    double r0, r1, r2, r3;
+    two_sum(c0, t0, r0, t0);
+    two_sum(t0, t1, r1, t1);
+    two_sum(t1, t2, r2, r3);
+    return qd{{r0, r1, r2, r3}};
+}
+
+TOR_HD void three_sum(double& a, double& b, double& c) {
+    double t1, t2, t3;
+    two_sum(a, b, t1, t2);
+    two_sum(c, t1, a, t3);
+    two_sum(t2, t3, b, c);
+}
+TOR_HD void three_sum2(double& a, double& b, double c) {
+    double t1, t2, t3;
+    two_sum(a, b, t1, t2);
+    two_sum(c, t1, a, t3);
+    b = t2 + t3;
+}
+
+// Accurate-enough QD addition ("sloppy" add: pairwise TwoSums then renormalise).
+TOR_HD qd qd_add(const qd& a, const qd& b) {
+    double s0, s1, s2, s3, t0, t1, t2, t3;
+    two_sum(a.x[0], b.x[0], s0, t0);
+    two_sum(a.x[1], b.x[1], s1, t1);
+    two_sum(a.x[2], b.x[2], s2, t2);
+    two_sum(a.x[3], b.x[3], s3, t3);
+    two_sum(s1, t0, s1, t0);
+    three_sum(s2, t0, t1);
+    three_sum2(s3, t0, t2);
+    t0 = t0 + t1 + t3;
+    return qd_renorm5_bf(s0, s1, s2, s3, t0);
+}
+TOR_HD qd qd_sub(const qd& a, const qd& b) { return qd_add(a, qd_neg(b)); }
+
+// QD product (sloppy: terms of order >= 4 in the component index dropped).
+TOR_HD qd qd_mul(const qd& a, const qd& b) {
+    double p0, p1, p2, p3, p4, p5, q0, q1, q2, q3, q4, q5;
+    double t0, t1, s0, s1, s2;
+    two_prod(a.x[0], b.x[0], p0, q0);
+    two_prod(a.x[0], b.x[1], p1, q1);
+    two_prod(a.x[1], b.x[0], p2, q2);
+    two_prod(a.x[0], b.x[2], p3, q3);
+    two_prod(a.x[1], b.x[1], p4, q4);
+    two_prod(a.x[2], b.x[0], p5, q5);
+    // order 1
+    three_sum(p1, p2, q0);
+    // order 2: p2, q1, q2, p3, p4, p5
+    three_sum(p2, q1, q2);
+    three_sum(p3, p4, p5);
+    two_sum(p2, p3, s0, t0);
+    two_sum(q1, p4, s1, t1);
+    s2 = q2 + p5;
+    two_sum(s1, t0, s1, t0);
+    s2 += (t0 + t1);
+    // order 3
+    s1 += a.x[0] * b.x[3] + a.x[1] * b.x[2] + a.x[2] * b.x[1] + a.x[3] * b.x[0] + q0 + q3 + q4 +
+          q5;
+    return qd_renorm5_bf(p0, p1, s0, s1, s2);
+}
+
+// QD x double.
+TOR_HD qd qd_mul_d(const qd& a, double b) {
+    double p0, p1, p2, p3, q0, q1, q2, s0, s1, s2, s3, s4;
+    two_prod(a.x[0], b, p0, q0);
+    two_prod(a.x[1], b, p1, q1);
+    two_prod(a.x[2], b, p2, q2);
+    p3 = a.x[3] * b;
+    s0 = p0;
+    two_sum(q0, p1, s1, s2);
+    three_sum(s2, q1, p2);
+    three_sum2(q1, q2, p3);
+    s3 = q1;
+    s4 = q2 + p2;
+    return qd_renorm5_bf(s0, s1, s2, s3, s4);
+}
+
+// s - a*b - c*d.
+TOR_HD qd qd_rank2(const qd& s, const qd& a, const qd& b, const qd& c, const qd& d) {
+    return qd_sub(qd_sub(s, qd_mul(a, b)), qd_mul(c, d));
+}
+TOR_HD qd qd_rank1(const qd& s, const qd& a, const qd& b) { return qd_sub(s, qd_mul(a, b)); }
+
+// 1/sqrt(x), x > 0: DD seed then one QD Newton step y + y(1 - x y^2)/2.
+TOR_HD qd qd_rsqrt(const qd& x) {
+    const dd ys = dd_rsqrt(dd_norm(dd{x.x[0], x.x[1]}));
+    const qd y = qd{{ys.hi, ys.lo, 0.0, 0.0}};
+    const qd y2 = qd_mul(y, y);
+    const qd xy2 = qd_mul(x, y2);
+    const qd r = qd_sub(qd_make(1.0), xy2);  // ~2^-104
+    const qd corr = qd_mul(y, qd_mul_d(r, 0.5));
+    return qd_add(y, corr);
+}
+
+// ================================================================ traits ==
+// Uniform interface used by the kernels.  Word type W, number of doubles K.
+template <class T> struct Arith;
+
+template <> struct Arith<double> {
+    static constexpr int K = 1;
+    TOR_HD static double zero() { return 0.0; }
+    TOR_HD static double one() { return 1.0; }
+    TOR_HD static double from(double x) { return x; }
+    TOR_HD static double hi(double a) { return a; }
+    TOR_HD static double norm(double a) { return a; }
+    TOR_HD static double mul(double a, double b) { return a * b; }
+    TOR_HD static double rank2(double s, double a, double b, double c, double d) {
+        return fma_(-c, d, fma_(-a, b, s));
+    }
+    TOR_HD static double rank1(double s, double a, double b) { return fma_(-a, b, s); }
+    TOR_HD static double rsqrt(double a) { return rsqrt_d(a); }
+    TOR_HD static double neg(double a) { return -a; }
+    TOR_HD static void words(double a, double* w) { w[0] = a; }
+};
+
+template <> struct Arith<dd> {
+    static constexpr int K = 2;
+    TOR_HD static dd zero() { return dd{0.0, 0.0}; }
+    TOR_HD static dd one() { return dd{1.0, 0.0}; }
+    TOR_HD static dd from(double x) { return dd{x, 0.0}; }
+    TOR_HD static double hi(const dd& a) { return a.hi; }
+    TOR_HD static dd norm(const dd& a) { return dd_norm(a); }
+    TOR_HD static dd mul(const dd& a, const dd& b) { return dd_mul(a, b); }
+    TOR_HD static dd rank2(const dd& s, const dd& a, const dd& b, const dd& c, const dd& d) {
+        return dd_rank2(s, a, b, c, d);
+    }
+    TOR_HD static dd rank1(const dd& s, const dd& a, const dd& b) { return dd_rank1(s, a, b); }
+    TOR_HD static dd rsqrt(const dd& a) { return dd_rsqrt(a); }
+    TOR_HD static dd neg(const dd& a) { return dd_neg(a); }
+    TOR_HD static void words(const dd& a, double* w) {
+        w[0] = a.hi;
+        w[1] = a.lo;
+    }
+};
+
+template <> struct Arith<qd> {
+    static constexpr int K = 4;
+    TOR_HD static qd zero() { return qd{{0.0, 0.0, 0.0, 0.0}}; }
+    TOR_HD static qd one() { return qd{{1.0, 0.0, 0.0, 0.0}}; }
+    TOR_HD static qd from(double x) { return qd{{x, 0.0, 0.0, 0.0}}; }
+    TOR_HD static double hi(const qd& a) { return a.x[0]; }
+    TOR_HD static qd norm(const qd& a) { return qd_renorm5_bf(a.x[0], a.x[1], a.x[2], a.x[3], 0.0); }
+    TOR_HD static qd mul(const qd& a, const qd& b) { return qd_mul(a, b); }
+    TOR_HD static qd rank2(const qd& s, const qd& a, const qd& b, const qd& c, const qd& d) {
+        return qd_rank2(s, a, b, c, d);
+    }
+    TOR_HD static qd rank1(const qd& s, const qd& a, const qd& b) { return qd_rank1(s, a, b); }
+    TOR_HD static qd rsqrt(const qd& a) { return qd_rsqrt(a); }
+    TOR_HD static qd neg(const qd& a) { return qd_neg(a); }
+    TOR_HD static void words(const qd& a, double* w) {
+        for (int i = 0; i < 4; ++i) w[i] = a.x[i];
+    }
+};
+
+// ========================================================== accumulators ==
+// Signed term accumulation.  fp64 and DD terms accumulate in an accurate DD sum,
+// QD terms in QD.  Sum |t| is carried in fp64 for the posterior cancellation check.
+template <class T> struct Acc;
+
+template <> struct Acc<double> {
+    dd s{0.0, 0.0};
+    double abs_sum = 0.0;
+    TOR_HD void add(double t, bool negative) {
+        const double v = negative ? -t : t;
+        double h, e;
+        two_sum(s.hi, v, h, e);
+        s.hi = h;
+        s.lo += e;
+        abs_sum += fabs(t);
+    }
+    TOR_HD void merge(const Acc& o) {
+        s = dd_add(s, o.s);
+        abs_sum += o.abs_sum;
+    }
+    TOR_HD void words(double* w) const {
+        const dd n = dd_norm(s);
+        w[0] = n.hi;
+        w[1] = n.lo;
+        w[2] = 0.0;
+        w[3] = 0.0;
+    }
+};
+
+template <> struct Acc<dd> {
+    dd s{0.0, 0.0};
+    double abs_sum = 0.0;
+    TOR_HD void add(const dd& t, bool negative) {
+        s = dd_add(s, negative ? dd_neg(t) : t);
+        abs_sum += fabs(t.hi);
+    }
+    TOR_HD void merge(const Acc& o) {
+        s = dd_add(s, o.s);
+        abs_sum += o.abs_sum;
+    }
+    TOR_HD void words(double* w) const {
+        w[0] = s.hi;
+        w[1] = s.lo;
+        w[2] = 0.0;
+        w[3] = 0.0;
+    }
+};
+
+template <> struct Acc<qd> {
+    qd s{{0.0, 0.0, 0.0, 0.0}};
+    double abs_sum = 0.0;
+    TOR_HD void add(const qd& t, bool negative) {
+        s = qd_add(s, negative ? qd_neg(t) : t);
+        abs_sum += fabs(t.x[0]);
+    }
+    TOR_HD void merge(const Acc& o) {
+        s = qd_add(s, o.s);
+        abs_sum += o.abs_sum;
+    }
+    TOR_HD void words(double* w) const {
+        for (int i = 0; i < 4; ++i) w[i] = s.x[i];
+    }
+};
+
+}  // namespace tor

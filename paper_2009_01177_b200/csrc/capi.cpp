@@ -1,0 +1,422 @@
+// C ABI of the B200 Torontonian engine (include/tor_capi.h).  Validation, precision
+// selection and the adaptive driver run on the host; every evaluation runs on the
+// GPU through engine_run().  There is no CPU fallback: without a CUDA device the
+// evaluation entry points fail with TOR_E_DEVICE.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "../../include/tor_capi.h"
+#include "arith.cuh"
+#include "engine.cuh"
+#include "host.hpp"
+
+using namespace tor;
+
+namespace {
+
+void set_err(tor_error* e, const char* code, const std::string& msg, int64_t row = -1, uint64_t mask = 0) {
+    if (!e) return;
+    std::memset(e, 0, sizeof(*e));
+    std::strncpy(e->code, code, sizeof(e->code) - 1);
+    std::strncpy(e->message, msg.c_str(), sizeof(e->message) - 1);
+    e->pivot_row = row;
+    e->subset_mask = mask;
+}
+
+int fail(tor_error* e, const HostError& h) {
+    set_err(e, h.code.c_str(), h.what(), h.pivot_row, h.subset_mask);
+    return h.status;
+}
+
+void clear_err(tor_error* e) {
+    if (e) set_err(e, "", "");
+}
+
+Input checked_input(const tor_input* in, int nmax) {
+    if (!in || in->n < 1 || in->n > nmax || !in->a00_upper || !in->a01_upper)
+        throw HostError(TOR_E_INVALID, "torontonian/range",
+                        nmax == 20 ? "reference path supports 1 <= N <= 20" : "engine supports 1 <= N <= 40");
+    Input a = make_input(in->n, in->a00_upper, in->a01_upper);
+    for (auto* v : {&a.a00, &a.a01})
+        for (const auto& x : *v)
+            if (!std::isfinite(x.real()) || !std::isfinite(x.imag()))
+                throw HostError(TOR_E_INVALID, "torontonian/domain", "input entries must be finite");
+    const SymReport s = check_symmetries(to_dense(a), 2 * a.n);  // torontonian.cpp:155-157
+    if (!s.pass) throw HostError(TOR_E_ERROR, "torontonian/symmetry", "input violates the block symmetries");
+    return a;
+}
+
+void put_cfg(const PrecCfg& c, tor_precision_config* o) {
+    o->width_bits = c.width_bits;
+    o->frac_bits = c.frac_bits;
+    o->b_lower = c.b_lower;
+    o->b_upper = c.b_upper;
+    o->b_sgn = c.b_sgn;
+    o->b_accum = c.b_accum;
+    o->a_repr = c.a_repr;
+    o->k_corr = c.k_corr;
+    o->alpha = c.alpha;
+}
+
+int mode_of(tor_precision p) {
+    return p == TOR_PREC_FP64 ? MODE_FP64 : (p == TOR_PREC_W256_QD ? MODE_QD : MODE_DD);
+}
+int width_of(int mode) { return mode == MODE_FP64 ? 64 : (mode == MODE_DD ? 128 : 256); }
+double mantissa_bits(int mode) { return mode == MODE_FP64 ? 52.0 : (mode == MODE_DD ? 104.0 : 208.0); }
+
+double words_value(const double* w) { return ((w[3] + w[2]) + w[1]) + w[0]; }
+
+void device_check(int device) {
+    int cnt = 0;
+    const cudaError_t e = cudaGetDeviceCount(&cnt);
+    if (e != cudaSuccess || cnt == 0)
+        throw HostError(TOR_E_DEVICE, "device/unavailable",
+                        std::string("no CUDA device: ") + (e == cudaSuccess ? "count 0" : cudaGetErrorString(e)));
+    if (device < 0 || device >= cnt) throw HostError(TOR_E_INVALID, "device/range", "device index out of range");
+}
+
+// Runs the engine and maps its failures onto the error taxonomy.
+std::vector<EngineOut> run(int device, int mode, const std::vector<Input>& ins, const WorkRange& range,
+                           EngineStats* stats) {
+    device_check(device);
+    std::vector<PreparedInput> prep(ins.size());
+    for (size_t i = 0; i < ins.size(); ++i) {
+        prep[i].n = ins[i].n;
+        prep[i].R = build_R(ins[i], mode_words(mode));
+    }
+    std::vector<EngineOut> out;
+    std::string err;
+    const int st = engine_run(device, mode, prep, range, out, stats, err);
+    if (st != 0) throw HostError(TOR_E_DEVICE, "device/cuda", err);
+    for (const auto& o : out)
+        if (o.breakdown) {
+            HostError h(TOR_E_BREAKDOWN, "linalg/breakdown", "non-positive pivot in elimination");
+            h.pivot_row = o.bad_row;
+            h.subset_mask = o.bad_mask;
+            throw h;
+        }
+    return out;
+}
+
+void fill_result(const Input& a, int mode, const PrecCfg& cfg, const EngineOut& o, const EngineStats& st,
+                 double wall, int ndev, tor_result* r) {
+    std::memset(r, 0, sizeof(*r));
+    r->mode = mode == MODE_FP64 ? TOR_PREC_FP64 : (mode == MODE_DD ? TOR_PREC_W128_DD : TOR_PREC_W256_QD);
+    r->width_bits = width_of(mode);
+    r->nwords = mode_words(mode);
+    for (int i = 0; i < 4; ++i) r->words[i] = o.words[i];
+    r->value = words_value(o.words);
+    put_cfg(cfg, &r->config);
+    r->term_count = o.terms;
+    op_counts(a.n, r->mults, r->adds, r->recips, r->rsqrts);
+    r->wall_seconds = wall;
+    r->device_ms = st.total_ms;
+    r->kernel_ms = st.kernel_ms;
+    r->devices = ndev;
+    r->sum_abs_terms = o.sum_abs;
+    const double av = std::fabs(r->value);
+    r->cancellation_bits = av > 0 ? std::log2(o.sum_abs / av) : std::numeric_limits<double>::infinity();
+    // error growth allowance: log2(n) + 4 bits over the working precision
+    r->bits_left = mantissa_bits(mode) - r->cancellation_bits - (std::log2(static_cast<double>(a.n)) + 4.0);
+    r->kernel_launches = st.launches;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tor_abi_version(void) { return TOR_ABI_VERSION; }
+
+int tor_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+    return c;
+}
+
+int tor_check_symmetries(const tor_input* in, double devs[3], int* pass, tor_error* err) {
+    try {
+        clear_err(err);
+        if (!in || in->n < 1) throw HostError(TOR_E_INVALID, "matrixio/dim", "matrix has no modes");
+        const Input a = make_input(in->n, in->a00_upper, in->a01_upper);
+        const SymReport s = check_symmetries(to_dense(a), 2 * a.n);
+        devs[0] = s.hermitian_dev;
+        devs[1] = s.a01_sym_dev;
+        devs[2] = s.block_conj_dev;
+        *pass = s.pass ? 1 : 0;
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+int tor_check_dense(int two_n, const double* dense, double devs[3], int* pass, tor_error* err) {
+    try {
+        clear_err(err);
+        if (two_n < 2 || !dense) throw HostError(TOR_E_INVALID, "matrixio/dim", "dense matrix must be 2N x 2N");
+        std::vector<std::complex<double>> d(static_cast<size_t>(two_n) * two_n);
+        for (size_t i = 0; i < d.size(); ++i) d[i] = {dense[2 * i], dense[2 * i + 1]};
+        const SymReport s = check_symmetries(d, two_n);
+        devs[0] = s.hermitian_dev;
+        devs[1] = s.a01_sym_dev;
+        devs[2] = s.block_conj_dev;
+        *pass = s.pass ? 1 : 0;
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+int tor_det_i_minus_a(const tor_input* in, double* det, tor_error* err) {
+    try {
+        clear_err(err);
+        if (!in || in->n < 1) throw HostError(TOR_E_INVALID, "matrixio/dim", "matrix has no modes");
+        *det = det_i_minus_a_float(make_input(in->n, in->a00_upper, in->a01_upper));
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+int tor_select_precision(const tor_input* in, int N, int sig, double alpha, tor_precision_config* out,
+                         tor_error* err) {
+    try {
+        clear_err(err);
+        if (!in || in->n < 1) throw HostError(TOR_E_INVALID, "precision/range", "N must be >= 1");
+        put_cfg(select_precision(make_input(in->n, in->a00_upper, in->a01_upper), N, sig, alpha), out);
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+int tor_force_width(const tor_input* in, int width_bits, tor_precision_config* out, tor_error* err) {
+    try {
+        clear_err(err);
+        if (!in || in->n < 1) throw HostError(TOR_E_INVALID, "precision/range", "N must be >= 1");
+        put_cfg(force_width(make_input(in->n, in->a00_upper, in->a01_upper), width_bits), out);
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+int tor_torontonian(const tor_input* in, tor_precision prec, const int* devices, int ndev, tor_result* out,
+                    tor_error* err) {
+    try {
+        clear_err(err);
+        const auto t0 = std::chrono::steady_clock::now();
+        const Input a = checked_input(in, 40);
+        if (prec < TOR_PREC_AUTO || prec > TOR_PREC_FP64)
+            throw HostError(TOR_E_INVALID, "precision/range", "unknown precision mode");
+        const int dev = (devices && ndev > 0) ? devices[0] : 0;
+        PrecCfg cfg;
+        int mode;
+        if (prec == TOR_PREC_AUTO) {
+            cfg = select_precision(a, a.n, 3, 0.5);
+            mode = cfg.width_bits == 128 ? MODE_DD : MODE_QD;
+        } else if (prec == TOR_PREC_FP64) {
+            cfg = force_width(a, 128);
+            cfg.width_bits = 64;
+            mode = MODE_FP64;
+        } else {
+            cfg = force_width(a, prec == TOR_PREC_W128_DD ? 128 : 256);
+            mode = mode_of(prec);
+        }
+        EngineStats st;
+        auto res = run(dev, mode, {a}, WorkRange{}, &st);
+        int escalated = 0;
+        if (prec == TOR_PREC_AUTO) {
+            // posterior check: keep >= b_sgn significant bits after cancellation
+            tor_result tmp;
+            fill_result(a, mode, cfg, res[0], st, 0.0, 1, &tmp);
+            if (tmp.value != 0.0 && tmp.bits_left < cfg.b_sgn) {
+                if (mode == MODE_DD) {
+                    mode = MODE_QD;
+                    escalated = 1;
+                    res = run(dev, mode, {a}, WorkRange{}, &st);
+                    fill_result(a, mode, cfg, res[0], st, 0.0, 1, &tmp);
+                }
+                if (tmp.bits_left < cfg.b_sgn)
+                    throw HostError(TOR_E_PRECISION, "precision/insufficient",
+                                    "cancellation leaves fewer than b_sgn significant bits");
+            }
+        }
+        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        fill_result(a, mode, cfg, res[0], st, wall, 1, out);
+        out->escalated = escalated;
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+int tor_torontonian_reference(const tor_input* in, double* value, tor_error* err) {
+    try {
+        clear_err(err);
+        const Input a = checked_input(in, 20);
+        EngineStats st;
+        const auto res = run(0, MODE_FP64, {a}, WorkRange{}, &st);
+        const double v = words_value(res[0].words);
+        if (!std::isfinite(v))
+            throw HostError(TOR_E_PRECISION, "torontonian/nonfinite", "non-finite term in reference summation");
+        *value = v;
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, int device, tor_result* outs,
+                          tor_error* err) {
+    try {
+        clear_err(err);
+        if (count < 1 || !ins) throw HostError(TOR_E_INVALID, "torontonian/range", "empty batch");
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<Input> as;
+        as.reserve(count);
+        for (int i = 0; i < count; ++i) {
+            as.push_back(checked_input(&ins[i], 40));
+            if (as.back().n != as.front().n)
+                throw HostError(TOR_E_INVALID, "torontonian/range", "batch instances must share N");
+        }
+        const int mode = prec == TOR_PREC_AUTO ? MODE_DD : mode_of(prec);
+        std::vector<PrecCfg> cfgs(count);
+        for (int i = 0; i < count; ++i) {
+            if (prec == TOR_PREC_AUTO) {
+                cfgs[i] = select_precision(as[i], as[i].n, 3, 0.5);
+                if (cfgs[i].width_bits != 128)
+                    throw HostError(TOR_E_PRECISION, "precision/batch-width",
+                                    "batch AUTO requires every instance to select 128 bits");
+            } else if (prec == TOR_PREC_FP64) {
+                cfgs[i] = PrecCfg{};
+                cfgs[i].width_bits = 64;
+            } else {
+                cfgs[i] = force_width(as[i], prec == TOR_PREC_W128_DD ? 128 : 256);
+            }
+        }
+        EngineStats st;
+        const auto res = run(device, mode, as, WorkRange{}, &st);
+        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        for (int i = 0; i < count; ++i) fill_result(as[i], mode, cfgs[i], res[i], st, wall, 1, &outs[i]);
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+int tor_torontonian_slice(const tor_input* in, tor_precision prec, int class_bits, uint64_t class_lo,
+                          uint64_t class_hi, int device, tor_partial* out, tor_error* err) {
+    try {
+        clear_err(err);
+        const Input a = checked_input(in, 40);
+        if (prec == TOR_PREC_AUTO) throw HostError(TOR_E_INVALID, "precision/range", "slice needs an explicit mode");
+        if (class_bits < 0 || class_bits > a.n || class_hi <= class_lo || class_hi > (1ull << class_bits))
+            throw HostError(TOR_E_INVALID, "torontonian/slice", "bad class range");
+        const int mode = mode_of(prec);
+        WorkRange wr;
+        wr.class_bits = class_bits;
+        wr.class_lo = class_lo;
+        wr.class_hi = class_hi;
+        EngineStats st;
+        const auto res = run(device, mode, {a}, wr, &st);
+        std::memset(out, 0, sizeof(*out));
+        out->mode = prec;
+        out->class_bits = class_bits;
+        out->class_lo = class_lo;
+        out->class_hi = class_hi;
+        for (int i = 0; i < 4; ++i) out->words[i] = res[0].words[i];
+        out->sum_abs = res[0].sum_abs;
+        out->term_count = res[0].terms;
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+int tor_torontonian_shard(const tor_input* in, tor_precision prec, int rank, int world, int device,
+                          tor_partial* out, tor_error* err) {
+    if (world < 1 || (world & (world - 1)) || rank < 0 || rank >= world) {
+        set_err(err, "torontonian/shard", "world must be a power of two and 0 <= rank < world");
+        return TOR_E_INVALID;
+    }
+    int k = 0;
+    while ((1 << k) < world) ++k;
+    if (prec == TOR_PREC_AUTO) {
+        tor_precision_config c;
+        const int st = tor_select_precision(in, in ? in->n : 0, 3, 0.5, &c, err);
+        if (st) return st;
+        prec = c.width_bits == 128 ? TOR_PREC_W128_DD : TOR_PREC_W256_QD;
+    }
+    return tor_torontonian_slice(in, prec, k, static_cast<uint64_t>(rank), static_cast<uint64_t>(rank) + 1, device,
+                                 out, err);
+}
+
+int tor_fold_partials(const tor_partial* parts, int count, const tor_input* in, tor_result* out, tor_error* err) {
+    try {
+        clear_err(err);
+        if (count < 1 || !parts) throw HostError(TOR_E_INVALID, "torontonian/shard", "no partials");
+        const Input a = checked_input(in, 40);
+        const int mode = mode_of(static_cast<tor_precision>(parts[0].mode));
+        std::vector<double> buf(static_cast<size_t>(count) * 5);
+        uint64_t terms = 0;
+        for (int i = 0; i < count; ++i) {
+            if (i > 0 && (parts[i].class_bits != parts[0].class_bits || parts[i].class_lo != parts[i - 1].class_hi))
+                throw HostError(TOR_E_INVALID, "torontonian/shard", "partials must be contiguous and sorted");
+            for (int x = 0; x < 4; ++x) buf[i * 5 + x] = parts[i].words[x];
+            buf[i * 5 + 4] = parts[i].sum_abs;
+            terms += parts[i].term_count;
+        }
+        double w5[5];
+        fold_words(mode, buf.data(), count, w5);
+        EngineOut o;
+        for (int x = 0; x < 4; ++x) o.words[x] = w5[x];
+        o.sum_abs = w5[4];
+        o.terms = terms;
+        PrecCfg cfg = (mode == MODE_FP64) ? PrecCfg{} : force_width(a, mode == MODE_DD ? 128 : 256);
+        if (mode == MODE_FP64) cfg.width_bits = 64;
+        EngineStats st;
+        fill_result(a, mode, cfg, o, st, 0.0, count, out);
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+int tor_probability(const tor_input* full, uint64_t pattern_bits, tor_precision prec, int device, double* p,
+                    tor_error* err) {
+    try {
+        clear_err(err);
+        if (!full || full->n < 1) throw HostError(TOR_E_INVALID, "matrixio/dim", "matrix has no modes");
+        const Input a = make_input(full->n, full->a00_upper, full->a01_upper);
+        const double det = det_i_minus_a_float(a);  // torontonian.cpp:203
+        if (!(det > 0.0)) throw HostError(TOR_E_ERROR, "torontonian/invalid-state", "det(I - A) must be positive");
+        if (pattern_bits == 0) {
+            *p = std::sqrt(det);
+            return TOR_OK;
+        }
+        const Input sub = extract_submatrix(a, pattern_bits);
+        std::vector<double> w00(sub.a00.size() * 2), w01(sub.a01.size() * 2);
+        for (size_t i = 0; i < sub.a00.size(); ++i) {
+            w00[2 * i] = sub.a00[i].real();
+            w00[2 * i + 1] = sub.a00[i].imag();
+            w01[2 * i] = sub.a01[i].real();
+            w01[2 * i + 1] = sub.a01[i].imag();
+        }
+        const tor_input si{sub.n, w00.data(), w01.data()};
+        tor_result r;
+        const int st = tor_torontonian(&si, prec, &device, 1, &r, err);
+        if (st) return st;
+        *p = r.value * std::sqrt(det);
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+}  // extern "C"

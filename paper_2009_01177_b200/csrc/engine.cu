@@ -1,0 +1,1008 @@
+// sm_100a kernels of the Torontonian engine (see engine.cuh and DESIGN.md).
+//
+// Work decomposition of the 2^n subsets (binary decision tree over modes 0..n-1,
+// decision "include mode m" = Cholesky elimination of the mode's 2x2 pair block
+// from the current Schur complement; "exclude" = drop the pair, a view):
+//
+//   depth 0 .. c           prefix levels, level-synchronous in global memory
+//                          (prefix_level_kernel, one warp per include node)
+//   depth c                jobs: 2^c prefix classes (top c reference-mask bits),
+//                          one warp per job (subtree_kernel)
+//   depth c .. n-q0        warp DFS, warp-cooperative eliminations, per-warp
+//                          global scratch stack (L1/L2 resident)
+//   depth n-q0 .. n-L      5-level breadth-first fan-out in shared memory, one
+//                          node per lane at the end (32 lanes)
+//   depth n-L .. n         per-lane register-resident subtree (fully unrolled)
+//
+// Every include node emits one signed term t = 1/sqrt(det R_Z) = prod of pivot
+// rsqrts; terms accumulate per lane (compensated), lanes fold by a fixed xor
+// butterfly, jobs by a fixed binary tree: the result is bit-identical for any
+// grid size, SM count or power-of-two shard count.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "arith.cuh"
+#include "engine.cuh"
+
+namespace tor {
+
+namespace {
+
+constexpr int FAN = 5;  // breadth-first fan-out levels -> 32 lane nodes
+constexpr int MAX_LEVELS = 48;
+
+__host__ __device__ constexpr int tri_sz(int d) { return d * (d + 1) / 2; }
+__host__ __device__ __forceinline__ int tri_ix(int d, int i, int j) {
+    return i * d - ((i * (i + 1)) >> 1) + j;
+}
+
+// Lane-level register depth per word type (register budget: the L-mode state is
+// read from shared memory, states of < L modes live in registers).
+template <class T> struct Cfg;
+template <> struct Cfg<double> { static constexpr int L = 4; static constexpr int WPB = 4; };
+template <> struct Cfg<dd> { static constexpr int L = 4; static constexpr int WPB = 2; };
+template <> struct Cfg<qd> { static constexpr int L = 3; static constexpr int WPB = 1; };
+
+template <class T> constexpr int root_modes() { return Cfg<T>::L + FAN; }
+
+// ----------------------------------------------------------------- jobs ----
+template <class T> struct Job {
+    const T* base;  // buffer holding the node's state (packed triangle, `dim` rows)
+    int dim;        // rows of the buffer
+    int skip;       // leading modes of the buffer dropped (excluded) for this node
+    int inst;       // instance index
+    int nsel;       // |Z| so far
+    uint64_t mask;  // reference-convention mask bits of the node's subset
+    T t;            // 1/sqrt(det R_Z)
+};
+
+struct PrefixGeom {
+    int n;                             // modes
+    int c;                             // prefix depth
+    size_t off[MAX_LEVELS + 1];        // entry offset of level e buffers (per instance)
+    size_t toff[MAX_LEVELS + 1];       // offset of level e t values (per instance)
+    size_t inst_entries;               // entries per instance
+    size_t inst_ts;                    // t values per instance
+};
+
+__device__ __forceinline__ void report_breakdown(unsigned long long* err, uint64_t mask, int row) {
+    // smallest failing mask wins (deterministic); row in the low byte
+    atomicMin(err, (static_cast<unsigned long long>(mask) << 8) | static_cast<unsigned long long>(row & 0xff));
+}
+
+template <class T> __device__ __forceinline__ T shfl_xor_t(const T& v, int m);
+template <> __device__ __forceinline__ double shfl_xor_t<double>(const double& v, int m) {
+    return __shfl_xor_sync(0xffffffffu, v, m);
+}
+template <> __device__ __forceinline__ dd shfl_xor_t<dd>(const dd& v, int m) {
+    return dd{__shfl_xor_sync(0xffffffffu, v.hi, m), __shfl_xor_sync(0xffffffffu, v.lo, m)};
+}
+template <> __device__ __forceinline__ qd shfl_xor_t<qd>(const qd& v, int m) {
+    qd r;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r.x[i] = __shfl_xor_sync(0xffffffffu, v.x[i], m);
+    return r;
+}
+template <class T> __device__ __forceinline__ T shfl_t(const T& v, int src);
+template <> __device__ __forceinline__ double shfl_t<double>(const double& v, int s) {
+    return __shfl_sync(0xffffffffu, v, s);
+}
+template <> __device__ __forceinline__ dd shfl_t<dd>(const dd& v, int s) {
+    return dd{__shfl_sync(0xffffffffu, v.hi, s), __shfl_sync(0xffffffffu, v.lo, s)};
+}
+template <> __device__ __forceinline__ qd shfl_t<qd>(const qd& v, int s) {
+    qd r;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r.x[i] = __shfl_sync(0xffffffffu, v.x[i], s);
+    return r;
+}
+
+template <class T> __device__ __forceinline__ void warp_fold(Acc<T>& a) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+        Acc<T> o;
+        o.s = shfl_xor_t(a.s, m);
+        o.abs_sum = __shfl_xor_sync(0xffffffffu, a.abs_sum, m);
+        a.merge(o);
+    }
+}
+// fp64 mode accumulates in DD
+template <> __device__ __forceinline__ void warp_fold<double>(Acc<double>& a) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+        Acc<double> o;
+        o.s = shfl_xor_t(a.s, m);
+        o.abs_sum = __shfl_xor_sync(0xffffffffu, a.abs_sum, m);
+        a.merge(o);
+    }
+}
+
+// ------------------------------------------------ warp-cooperative elimination --
+// Eliminates the first mode (rows 0,1) of the q-mode view (S, d, sr) into the
+// packed (2q-2)-row triangle dst; t_out = t * rho1 * rho2.  uw: shared scratch of
+// 4q entries.  All lanes compute the pivot chain redundantly (warp-uniform).
+template <class T>
+__device__ void warp_elim(const T* S, int d, int sr, int q, T* dst, const T& t_in, T* t_out, T* uw,
+                          uint64_t mask, int nsel, unsigned long long* err) {
+    using A = Arith<T>;
+    const int lane = threadIdx.x & 31;
+    const T a = A::norm(S[tri_ix(d, sr, sr)]);
+    const bool bad0 = nonpositive(A::hi(a));
+    const T r1 = A::rsqrt(a);
+    const T u1 = A::mul(S[tri_ix(d, sr, sr + 1)], r1);
+    const T b = A::norm(A::rank1(S[tri_ix(d, sr + 1, sr + 1)], u1, u1));
+    const bool bad1 = nonpositive(A::hi(b));
+    const T r2 = A::rsqrt(b);
+    if (lane == 0) {
+        if (bad0 || bad1) report_breakdown(err, mask, 2 * nsel + (bad0 ? 0 : 1));
+        *t_out = A::mul(A::mul(t_in, r1), r2);
+    }
+    const int m = 2 * q;
+    for (int j = 2 + lane; j < m; j += 32) {
+        const T uj = A::mul(S[tri_ix(d, sr, sr + j)], r1);
+        const T wj = A::mul(A::rank1(S[tri_ix(d, sr + 1, sr + j)], u1, uj), r2);
+        uw[j] = uj;
+        uw[m + j] = wj;
+    }
+    __syncwarp();
+    const int dn = m - 2;
+    const int total = tri_sz(dn);
+    int i = 0, k0 = lane;
+    while (i < dn && k0 >= dn - i) {
+        k0 -= dn - i;
+        ++i;
+    }
+    int j = i + k0;
+    for (int k = lane; k < total; k += 32) {
+        dst[k] = A::rank2(S[tri_ix(d, sr + 2 + i, sr + 2 + j)], uw[2 + i], uw[2 + j], uw[m + 2 + i],
+                          uw[m + 2 + j]);
+        j += 32;
+        while (i < dn && j >= dn) {
+            j -= dn - (i + 1);
+            ++i;
+        }
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------------- prefix levels ----
+template <class T>
+__device__ __forceinline__ void node_view(const PrefixGeom& g, const T* pool, const T* tpool, int inst, int e,
+                                          uint64_t c, const T*& base, int& dim, int& skip, T& t) {
+    const T* ib = pool + inst * g.inst_entries;
+    if (c == 0) {
+        base = ib + g.off[0];
+        dim = 2 * g.n;
+        skip = e;
+        t = Arith<T>::one();
+        return;
+    }
+    const int tz = __ffsll(static_cast<long long>(c)) - 1;
+    const int lvl = e - tz;
+    const uint64_t p = (c >> tz) >> 1;
+    dim = 2 * (g.n - lvl);
+    base = ib + g.off[lvl] + p * static_cast<uint64_t>(tri_sz(dim));
+    skip = tz;
+    t = tpool[inst * g.inst_ts + g.toff[lvl] + p];
+}
+
+// Level e: every include node (inst, p), p < 2^(e-1), eliminates the first mode of
+// its parent view (e-1, p) into level-e buffer p.
+template <class T>
+__global__ void prefix_level_kernel(PrefixGeom g, T* pool, T* tpool, int e, int ninst,
+                                    unsigned long long* err) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* uw_all = reinterpret_cast<T*>(smem_raw);
+    const int wib = threadIdx.x >> 5;
+    T* uw = uw_all + wib * (4 * g.n);
+    const uint64_t per = 1ull << (e - 1);
+    const uint64_t total = per * ninst;
+    const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t it = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; it < total; it += nw) {
+        const int inst = static_cast<int>(it / per);
+        const uint64_t p = it % per;
+        const T* base;
+        int dim, skip;
+        T t;
+        node_view<T>(g, pool, tpool, inst, e - 1, p, base, dim, skip, t);
+        const int q = g.n - (e - 1);
+        T* dst = pool + inst * g.inst_entries + g.off[e] + p * static_cast<uint64_t>(tri_sz(2 * (g.n - e)));
+        T* tdst = tpool + inst * g.inst_ts + g.toff[e] + p;
+        const uint64_t mask = ((p << 1) | 1ull) << (g.n - e);
+        warp_elim<T>(base, dim, 2 * skip, q, dst, t, tdst, uw, mask, __popcll(mask) - 1, err);
+    }
+}
+
+template <class T>
+__global__ void make_jobs_kernel(PrefixGeom g, const T* pool, const T* tpool, int ninst, uint64_t lo,
+                                 uint64_t hi, Job<T>* jobs) {
+    const uint64_t per = hi - lo;
+    const uint64_t total = per * ninst;
+    for (uint64_t it = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; it < total;
+         it += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const int inst = static_cast<int>(it / per);
+        const uint64_t c = lo + it % per;
+        Job<T> J;
+        node_view<T>(g, pool, tpool, inst, g.c, c, J.base, J.dim, J.skip, J.t);
+        J.inst = inst;
+        J.mask = g.c ? (c << (g.n - g.c)) : 0;
+        J.nsel = __popcll(c);
+        jobs[it] = J;
+    }
+}
+
+// Direct prefix for slices with class bits beyond the materialised prefix depth:
+// one warp per class walks modes 0..k-1 (include -> eliminate into the class's own
+// ping-pong buffers, exclude -> skip).
+template <class T>
+__global__ void direct_prefix_kernel(int n, int k, const T* R, int ninst, size_t inst_entries, uint64_t lo,
+                                     uint64_t hi, T* work, size_t work_stride, Job<T>* jobs,
+                                     unsigned long long* err) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* uw_all = reinterpret_cast<T*>(smem_raw);
+    T* tslot = uw_all + (blockDim.x >> 5) * (4 * n);
+    const int wib = threadIdx.x >> 5;
+    T* uw = uw_all + wib * (4 * n);
+    T* tt = tslot + wib;
+    const int lane = threadIdx.x & 31;
+    const uint64_t per = hi - lo;
+    const uint64_t total = per * ninst;
+    const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t it = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; it < total; it += nw) {
+        const int inst = static_cast<int>(it / per);
+        const uint64_t cls = lo + it % per;
+        const T* base = R + inst * inst_entries;
+        int dim = 2 * n, skip = 0, nsel = 0;
+        T t = Arith<T>::one();
+        T* bufs[2] = {work + it * work_stride, work + it * work_stride + tri_sz(2 * n)};
+        int cur = 0;
+        uint64_t mask = 0;
+        for (int m = 0; m < k; ++m) {
+            const bool inc = (cls >> (k - 1 - m)) & 1;
+            if (!inc) {
+                ++skip;
+                continue;
+            }
+            mask |= 1ull << (n - 1 - m);
+            const int q = dim / 2 - skip;
+            T* dst = bufs[cur];
+            warp_elim<T>(base, dim, 2 * skip, q, dst, t, tt, uw, mask, nsel, err);
+            __syncwarp();
+            t = *tt;
+            __syncwarp();
+            base = dst;
+            dim = 2 * (q - 1);
+            skip = 0;
+            cur ^= 1;
+            ++nsel;
+        }
+        if (lane == 0) {
+            Job<T> J;
+            J.base = base;
+            J.dim = dim;
+            J.skip = skip;
+            J.inst = inst;
+            J.nsel = nsel;
+            J.mask = mask;
+            J.t = t;
+            jobs[it] = J;
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------ register-level subtrees ----
+// State of Q modes in registers: packed upper triangle of 2Q rows.
+template <class T, int Q> struct St {
+    T e[tri_sz(2 * Q)];
+};
+
+template <int D> __device__ __forceinline__ constexpr int cix(int i, int j) { return i * D - (i * (i + 1)) / 2 + j; }
+
+// Eliminate mode 0 of a Q-mode register state into a (Q-1)-mode state.
+template <class T, int Q>
+__device__ __forceinline__ void elim_reg(const St<T, Q>& S, St<T, Q - 1>& out, const T& t, T& tout, uint64_t mask,
+                                         int nsel, unsigned long long* err) {
+    using A = Arith<T>;
+    constexpr int M = 2 * Q;
+    const T a = A::norm(S.e[cix<M>(0, 0)]);
+    const bool bad0 = nonpositive(A::hi(a));
+    const T r1 = A::rsqrt(a);
+    const T u1 = A::mul(S.e[cix<M>(0, 1)], r1);
+    const T b = A::norm(A::rank1(S.e[cix<M>(1, 1)], u1, u1));
+    const bool bad1 = nonpositive(A::hi(b));
+    const T r2 = A::rsqrt(b);
+    if (bad0 || bad1) report_breakdown(err, mask, 2 * nsel + (bad0 ? 0 : 1));
+    tout = A::mul(A::mul(t, r1), r2);
+    T u[M], w[M];
+#pragma unroll
+    for (int j = 2; j < M; ++j) {
+        u[j] = A::mul(S.e[cix<M>(0, j)], r1);
+        w[j] = A::mul(A::rank1(S.e[cix<M>(1, j)], u1, u[j]), r2);
+    }
+#pragma unroll
+    for (int i = 2; i < M; ++i)
+#pragma unroll
+        for (int j = i; j < M; ++j)
+            out.e[cix<M - 2>(i - 2, j - 2)] = A::rank2(S.e[cix<M>(i, j)], u[i], u[j], w[i], w[j]);
+}
+
+// All nonempty subsets of the Q register modes (the node's own term excluded).
+// neg: sign of the current node's term; bits: reference mask of the node.
+template <class T, int Q> struct SubReg {
+    __device__ __forceinline__ static void run(const St<T, Q>& S, const T& t, bool neg, uint64_t mask, int nsel,
+                                               Acc<T>& acc, unsigned long long* err) {
+        using A = Arith<T>;
+        const uint64_t bit = 1ull << (Q - 1);
+        {
+            St<T, Q - 1> Sn;
+            T tn;
+            elim_reg<T, Q>(S, Sn, t, tn, mask | bit, nsel, err);
+            acc.add(tn, !neg);
+            SubReg<T, Q - 1>::run(Sn, tn, !neg, mask | bit, nsel + 1, acc, err);
+        }
+        {
+            St<T, Q - 1> Sx;
+            constexpr int M = 2 * Q;
+#pragma unroll
+            for (int i = 2; i < M; ++i)
+#pragma unroll
+                for (int j = i; j < M; ++j) Sx.e[cix<M - 2>(i - 2, j - 2)] = S.e[cix<M>(i, j)];
+            SubReg<T, Q - 1>::run(Sx, t, neg, mask, nsel, acc, err);
+        }
+        (void)sizeof(A);
+    }
+};
+template <class T> struct SubReg<T, 1> {
+    __device__ __forceinline__ static void run(const St<T, 1>& S, const T& t, bool neg, uint64_t mask, int nsel,
+                                               Acc<T>& acc, unsigned long long* err) {
+        using A = Arith<T>;
+        const T det = A::norm(A::rank1(A::mul(S.e[0], S.e[2]), S.e[1], S.e[1]));
+        if (nonpositive(A::hi(det))) report_breakdown(err, mask | 1ull, 2 * nsel + 1);
+        const T tn = A::mul(t, A::rsqrt(det));
+        acc.add(tn, !neg);
+    }
+};
+
+// Lane subtree rooted at an L-mode view in shared memory: emits the node's own
+// term and all 2^L - 1 extensions.
+template <class T, int L>
+__device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t, bool neg, uint64_t mask, int nsel,
+                                          Acc<T>& acc, unsigned long long* err) {
+    using A = Arith<T>;
+    constexpr int M = 2 * L;
+    acc.add(t, neg);
+    const uint64_t bit = 1ull << (L - 1);
+    {
+        // include the first view mode: elimination reads shared memory
+        const T a = A::norm(S[tri_ix(d, sr, sr)]);
+        const bool bad0 = nonpositive(A::hi(a));
+        const T r1 = A::rsqrt(a);
+        const T u1 = A::mul(S[tri_ix(d, sr, sr + 1)], r1);
+        const T b = A::norm(A::rank1(S[tri_ix(d, sr + 1, sr + 1)], u1, u1));
+        const bool bad1 = nonpositive(A::hi(b));
+        const T r2 = A::rsqrt(b);
+        if (bad0 || bad1) report_breakdown(err, mask | bit, 2 * nsel + (bad0 ? 0 : 1));
+        const T tn = A::mul(A::mul(t, r1), r2);
+        T u[M], w[M];
+#pragma unroll
+        for (int j = 2; j < M; ++j) {
+            u[j] = A::mul(S[tri_ix(d, sr, sr + j)], r1);
+            w[j] = A::mul(A::rank1(S[tri_ix(d, sr + 1, sr + j)], u1, u[j]), r2);
+        }
+        St<T, L - 1> Sn;
+#pragma unroll
+        for (int i = 2; i < M; ++i)
+#pragma unroll
+            for (int j = i; j < M; ++j)
+                Sn.e[cix<M - 2>(i - 2, j - 2)] = A::rank2(S[tri_ix(d, sr + i, sr + j)], u[i], u[j], w[i], w[j]);
+        acc.add(tn, !neg);
+        SubReg<T, L - 1>::run(Sn, tn, !neg, mask | bit, nsel + 1, acc, err);
+    }
+    {
+        St<T, L - 1> Sx;
+#pragma unroll
+        for (int i = 2; i < M; ++i)
+#pragma unroll
+            for (int j = i; j < M; ++j) Sx.e[cix<M - 2>(i - 2, j - 2)] = S[tri_ix(d, sr + i, sr + j)];
+        SubReg<T, L - 1>::run(Sx, t, neg, mask, nsel, acc, err);
+    }
+}
+
+// --------------------------------------------------------- subtree kernel ----
+template <class T> struct WarpSmem {
+    static constexpr int L = Cfg<T>::L;
+    static constexpr int Q0 = L + FAN;
+    // level e buffers: 2^(e-1) x tri(2(Q0-e)); level 0: the root (copy of the leaf view)
+    __host__ __device__ static constexpr int lvl_off(int e) {
+        int o = tri_sz(2 * Q0);
+        for (int x = 1; x < e; ++x) o += (1 << (x - 1)) * tri_sz(2 * (Q0 - x));
+        return e == 0 ? 0 : o;
+    }
+    static constexpr int kBufEntries = lvl_off(FAN + 1);
+    static constexpr int kTOff = kBufEntries;                 // t per level buffer (index 2^(e-1)-1+p)
+    static constexpr int kPivOff = kTOff + 32;                // r1, u1, r2 per elimination (16 each)
+    static constexpr int kUwOff = kPivOff + 48;               // u/w vectors: 16 elims x 4 x Q0
+    __host__ __device__ static constexpr int uw_need() {
+        int mx = 4 * 24;  // DFS eliminations: 4q entries, q <= kMaxJobModes
+        for (int e = 1; e <= FAN; ++e) {
+            const int need = (1 << (e - 1)) * 2 * 2 * (Q0 - e + 1);
+            if (need > mx) mx = need;
+        }
+        return mx;
+    }
+    static constexpr int kUwEntries = uw_need();
+    static constexpr int kDfsT = kUwOff + kUwEntries;         // DFS slot t values
+    static constexpr int kEntries = kDfsT + 64;
+    static constexpr size_t kBytes = kEntries * sizeof(T);
+};
+
+template <class T, int Q0>
+__device__ __forceinline__ void lane_view(const T* sm, int c, const T*& base, int& dim, int& skip, T& t,
+                                          const T* tvals, int e) {
+    // node (e, c) of the breadth-first fan-out rooted at the copied root (level 0)
+    if (c == 0) {
+        base = sm;
+        dim = 2 * Q0;
+        skip = e;
+        t = tvals[31];  // root t stored at slot 31
+        return;
+    }
+    const int tz = __ffs(c) - 1;
+    const int lvl = e - tz;
+    const int p = (c >> tz) >> 1;
+    dim = 2 * (Q0 - lvl);
+    base = sm + WarpSmem<T>::lvl_off(lvl) + p * tri_sz(dim);
+    skip = tz;
+    t = tvals[(1 << (lvl - 1)) - 1 + p];
+}
+
+template <class T>
+__global__ void __launch_bounds__(32 * Cfg<T>::WPB)
+    subtree_kernel(const Job<T>* jobs, uint64_t njobs, int nmodes, int rjob, T* scratch, size_t scratch_stride,
+                   double* partials, unsigned long long* err, unsigned long long* job_counter) {
+    using A = Arith<T>;
+    using SM = WarpSmem<T>;
+    constexpr int L = Cfg<T>::L;
+    constexpr int Q0 = SM::Q0;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int wib = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    T* sm = reinterpret_cast<T*>(smem_raw) + wib * SM::kEntries;
+    T* tvals = sm + SM::kTOff;
+    T* piv = sm + SM::kPivOff;
+    T* uwv = sm + SM::kUwOff;
+    T* dfs_t = sm + SM::kDfsT;
+    const int gw = blockIdx.x * Cfg<T>::WPB + wib;
+    T* slots = scratch + static_cast<size_t>(gw) * scratch_stride;
+    const int D = rjob - Q0;
+
+    for (;;) {
+        unsigned long long job = 0;
+        if (lane == 0) job = atomicAdd(job_counter, 1ull);
+        job = __shfl_sync(0xffffffffu, job, 0);
+        if (job >= njobs) break;
+        const Job<T> J = jobs[job];
+        Acc<T> acc;
+
+        for (uint64_t leaf = 0; leaf < (1ull << D); ++leaf) {
+            if (leaf > 0) {
+                // flip exclude->include at depth kd (lowest set bit of leaf)
+                const int b = __ffsll(static_cast<long long>(leaf)) - 1;
+                const int kd = D - 1 - b;
+                const uint64_t above = leaf >> (b + 1);
+                const T* src;
+                int sd, ssk;
+                T st;
+                if (above == 0) {
+                    src = J.base;
+                    sd = J.dim;
+                    ssk = J.skip + kd;
+                    st = J.t;
+                } else {
+                    const int tz = __ffsll(static_cast<long long>(above)) - 1;
+                    const int s = kd - tz;  // slot index (depth after that include)
+                    size_t off = 0;
+                    for (int x = 1; x < s; ++x) off += tri_sz(2 * (rjob - x));
+                    src = slots + off;
+                    sd = 2 * (rjob - s);
+                    ssk = tz;
+                    st = dfs_t[s];
+                }
+                size_t doff = 0;
+                for (int x = 1; x < kd + 1; ++x) doff += tri_sz(2 * (rjob - x));
+                const uint64_t lmask = J.mask | ((above << 1 | 1ull) << (rjob - kd - 1));
+                const int lsel = J.nsel + __popcll(above);
+                warp_elim<T>(src, sd, 2 * ssk, rjob - kd, slots + doff, st, dfs_t + kd + 1, uwv, lmask, lsel, err);
+            }
+            // leaf view (depth D of the job) -> copy the Q0-mode root into shared memory
+            const T* lb;
+            int ld, lsk;
+            T lt;
+            if (leaf == 0) {
+                lb = J.base;
+                ld = J.dim;
+                lsk = J.skip + D;
+                lt = J.t;
+            } else {
+                const int tz = __ffsll(static_cast<long long>(leaf)) - 1;
+                const int s = D - tz;
+                size_t off = 0;
+                for (int x = 1; x < s; ++x) off += tri_sz(2 * (rjob - x));
+                lb = slots + off;
+                ld = 2 * (rjob - s);
+                lsk = tz;
+                lt = dfs_t[s];
+            }
+            __syncwarp();
+            {
+                constexpr int RM = 2 * Q0;
+                const int sr = 2 * lsk;
+                int i = 0, k0 = lane;
+                while (i < RM && k0 >= RM - i) {
+                    k0 -= RM - i;
+                    ++i;
+                }
+                int j = i + k0;
+                for (int k = lane; k < tri_sz(RM); k += 32) {
+                    sm[k] = lb[tri_ix(ld, sr + i, sr + j)];
+                    j += 32;
+                    while (i < RM && j >= RM) {
+                        j -= RM - (i + 1);
+                        ++i;
+                    }
+                }
+                if (lane == 0) tvals[31] = lt;
+            }
+            __syncwarp();
+            const uint64_t leaf_mask = J.mask | (leaf << Q0);
+            const int leaf_sel = J.nsel + __popcll(leaf);
+
+            // breadth-first fan-out: level e creates 2^(e-1) include buffers
+#pragma unroll
+            for (int e = 1; e <= FAN; ++e) {
+                const int E = 1 << (e - 1);
+                const int q = Q0 - e + 1;  // parent modes
+                const int m = 2 * q;
+                // pivots: lane x < E handles elimination x (parent node (e-1, x))
+                {
+                    const int x = lane & (E - 1);
+                    const T* pb;
+                    int pd, psk;
+                    T pt;
+                    lane_view<T, Q0>(sm, x, pb, pd, psk, pt, tvals, e - 1);
+                    const int sr = 2 * psk;
+                    const T a = A::norm(pb[tri_ix(pd, sr, sr)]);
+                    const bool bad0 = nonpositive(A::hi(a));
+                    const T r1 = A::rsqrt(a);
+                    const T u1 = A::mul(pb[tri_ix(pd, sr, sr + 1)], r1);
+                    const T bb = A::norm(A::rank1(pb[tri_ix(pd, sr + 1, sr + 1)], u1, u1));
+                    const bool bad1 = nonpositive(A::hi(bb));
+                    const T r2 = A::rsqrt(bb);
+                    if (lane < E) {
+                        const uint64_t nm = leaf_mask | (static_cast<uint64_t>((x << 1) | 1) << (Q0 - e));
+                        if (bad0 || bad1)
+                            report_breakdown(err, nm, 2 * (leaf_sel + __popc(x)) + (bad0 ? 0 : 1));
+                        piv[x] = r1;
+                        piv[16 + x] = u1;
+                        piv[32 + x] = r2;
+                        tvals[E - 1 + x] = A::mul(A::mul(pt, r1), r2);
+                    }
+                }
+                __syncwarp();
+                // pivot-row vectors
+                for (int it = lane; it < E * (m - 2); it += 32) {
+                    const int x = it / (m - 2);
+                    const int j = 2 + it % (m - 2);
+                    const T* pb;
+                    int pd, psk;
+                    T pt;
+                    lane_view<T, Q0>(sm, x, pb, pd, psk, pt, tvals, e - 1);
+                    const int sr = 2 * psk;
+                    const T uj = A::mul(pb[tri_ix(pd, sr, sr + j)], piv[x]);
+                    const T wj = A::mul(A::rank1(pb[tri_ix(pd, sr + 1, sr + j)], piv[16 + x], uj), piv[32 + x]);
+                    uwv[x * 2 * m + j] = uj;
+                    uwv[x * 2 * m + m + j] = wj;
+                }
+                __syncwarp();
+                // trailing updates into the level-e buffers
+                const int dn = m - 2;
+                const int tn = tri_sz(dn);
+                T* lvl = sm + SM::lvl_off(e);
+                for (int it = lane; it < E * tn; it += 32) {
+                    const int x = it / tn;
+                    int k = it % tn;
+                    int i = 0;
+                    while (k >= dn - i) {
+                        k -= dn - i;
+                        ++i;
+                    }
+                    const int j = i + k;
+                    const T* pb;
+                    int pd, psk;
+                    T pt;
+                    lane_view<T, Q0>(sm, x, pb, pd, psk, pt, tvals, e - 1);
+                    const int sr = 2 * psk;
+                    const T* uw = uwv + x * 2 * m;
+                    lvl[x * tn + tri_ix(dn, i, j)] =
+                        A::rank2(pb[tri_ix(pd, sr + 2 + i, sr + 2 + j)], uw[2 + i], uw[2 + j], uw[m + 2 + i], uw[m + 2 + j]);
+                }
+                __syncwarp();
+            }
+            // lanes: node (FAN, lane)
+            {
+                const T* vb;
+                int vd, vsk;
+                T vt;
+                lane_view<T, Q0>(sm, lane, vb, vd, vsk, vt, tvals, FAN);
+                const int pc = __popc(lane);
+                const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(lane) << L);
+                const int lsel = leaf_sel + pc;
+                // term sign of the node: (-1)^(n - |Z|)
+                const bool nodeneg = ((nmodes - lsel) & 1) != 0;
+                lane_tree<T, L>(vb, vd, 2 * vsk, vt, nodeneg, lmask, lsel, acc, err);
+            }
+            __syncwarp();
+        }
+        warp_fold<T>(acc);
+        if (lane == 0) {
+            double w[4];
+            acc.words(w);
+            double* o = partials + job * 5;
+            o[0] = w[0];
+            o[1] = w[1];
+            o[2] = w[2];
+            o[3] = w[3];
+            o[4] = acc.abs_sum;
+        }
+        __syncwarp();
+    }
+}
+
+
+// ----------------------------------------------------------- small jobs ----
+// Jobs whose state has fewer than Q0 modes (small n, deep slices): one thread per
+// job enumerates all 2^r subsets W of the job modes with a direct Cholesky of the
+// gathered 2|W| x 2|W| Schur-complement submatrix.
+template <class T, int RMAX>
+__global__ void small_job_kernel(const Job<T>* jobs, uint64_t njobs, int nmodes, int rjob, double* partials,
+                                 unsigned long long* err) {
+    using A = Arith<T>;
+    const uint64_t jid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (jid >= njobs) return;
+    const Job<T> J = jobs[jid];
+    Acc<T> acc;
+    T M[tri_sz(2 * RMAX)];
+    int sel[RMAX];
+    for (uint64_t w = 0; w < (1ull << rjob); ++w) {
+        int z = 0;
+        for (int m = 0; m < rjob; ++m)
+            if ((w >> (rjob - 1 - m)) & 1) sel[z++] = m;
+        const int d = 2 * z;
+        for (int a = 0; a < d; ++a)
+            for (int b = a; b < d; ++b) {
+                const int ra = 2 * (J.skip + sel[a >> 1]) + (a & 1);
+                const int rb = 2 * (J.skip + sel[b >> 1]) + (b & 1);
+                M[tri_ix(d, a, b)] = J.base[tri_ix(J.dim, ra, rb)];
+            }
+        T t = J.t;
+        const uint64_t mask = J.mask | w;
+        for (int k = 0; k < d; ++k) {
+            const T p = A::norm(M[tri_ix(d, k, k)]);
+            if (nonpositive(A::hi(p))) report_breakdown(err, mask, 2 * J.nsel + k);
+            const T r = A::rsqrt(p);
+            t = A::mul(t, r);
+            for (int j = k + 1; j < d; ++j) M[tri_ix(d, k, j)] = A::mul(M[tri_ix(d, k, j)], r);
+            for (int i = k + 1; i < d; ++i)
+                for (int j = i; j < d; ++j)
+                    M[tri_ix(d, i, j)] = A::rank1(M[tri_ix(d, i, j)], M[tri_ix(d, k, i)], M[tri_ix(d, k, j)]);
+        }
+        const bool neg = ((nmodes - J.nsel - z) & 1) != 0;
+        acc.add(t, neg);
+    }
+    double wds[4];
+    acc.words(wds);
+    double* o = partials + jid * 5;
+    for (int i = 0; i < 4; ++i) o[i] = wds[i];
+    o[4] = acc.abs_sum;
+}
+
+// ------------------------------------------------------------- reduction ----
+template <class T> __host__ __device__ inline void merge_words(double* a, const double* b) {
+    if constexpr (sizeof(T) == sizeof(qd)) {
+        const qd x{{a[0], a[1], a[2], a[3]}};
+        const qd y{{b[0], b[1], b[2], b[3]}};
+        const qd r = qd_add(x, y);
+        for (int i = 0; i < 4; ++i) a[i] = r.x[i];
+    } else {
+        const dd r = dd_add(dd{a[0], a[1]}, dd{b[0], b[1]});
+        a[0] = r.hi;
+        a[1] = r.lo;
+        a[2] = 0.0;
+        a[3] = 0.0;
+    }
+    a[4] += b[4];
+}
+
+// One block per instance: in-place fixed binary tree over the instance's `per`
+// consecutive job partials (5 doubles each); result in partials[inst*per].
+template <class T>
+__global__ void fold_kernel(double* partials, uint64_t per) {
+    double* p = partials + blockIdx.x * per * 5;
+    for (uint64_t s = 1; s < per; s <<= 1) {
+        for (uint64_t i = threadIdx.x * 2 * s; i + s < per; i += static_cast<uint64_t>(blockDim.x) * 2 * s)
+            merge_words<T>(p + i * 5, p + (i + s) * 5);
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------ host side ----
+#define CK(x)                                                                         \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess) {                                                      \
+            err = std::string(#x) + ": " + cudaGetErrorString(e_);                    \
+            return static_cast<int>(e_);                                              \
+        }                                                                             \
+    } while (0)
+
+constexpr int kMaxJobModes = 24;
+
+int ilog2_floor(uint64_t v) {
+    int r = -1;
+    while (v) {
+        v >>= 1;
+        ++r;
+    }
+    return r;
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+template <class T>
+int run_impl(int device, const std::vector<PreparedInput>& inputs, const WorkRange& range,
+             std::vector<EngineOut>& out, EngineStats* stats, std::string& err) {
+    constexpr int K = Arith<T>::K;
+    constexpr int L = Cfg<T>::L;
+    constexpr int Q0 = L + FAN;
+    const int ninst = static_cast<int>(inputs.size());
+    const int n = inputs[0].n;
+    const int kbits = range.class_bits;
+    const uint64_t clo = range.class_lo, chi = range.class_hi;
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{st};
+    cudaEvent_t ev0, ev1, ev2, ev3;
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    CK(cudaEventCreate(&ev2));
+    CK(cudaEventCreate(&ev3));
+    struct EvGuard {
+        cudaEvent_t a, b, c, d;
+        ~EvGuard() {
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+            cudaEventDestroy(c);
+            cudaEventDestroy(d);
+        }
+    } eg{ev0, ev1, ev2, ev3};
+    uint64_t launches = 0;
+
+    // ---- prefix depth: enough jobs to fill the GPU, job states <= kMaxJobModes modes
+    const uint64_t want_jobs = 16384;
+    int c = 0;
+    if (n >= Q0) {
+        int cw = 0;
+        while ((static_cast<uint64_t>(ninst) << cw) < want_jobs && cw < n - Q0) ++cw;
+        c = std::max(cw, n - kMaxJobModes);
+        c = std::min(c, n - Q0);
+    }
+    const bool use_levels = kbits <= c;
+    const int cj = use_levels ? c : kbits;  // depth at which jobs sit
+    const int rjob = n - cj;
+    const uint64_t per = use_levels ? ((chi - clo) << (c - kbits)) : (chi - clo);
+    const uint64_t njobs = per * ninst;
+
+    // ---- geometry & device memory
+    PrefixGeom g{};
+    g.n = n;
+    g.c = use_levels ? c : 0;
+    size_t o = 0, to = 0;
+    g.off[0] = 0;
+    g.toff[0] = 0;
+    o = tri_sz(2 * n);
+    for (int e = 1; e <= g.c; ++e) {
+        g.off[e] = o;
+        g.toff[e] = to;
+        o += (static_cast<size_t>(1) << (e - 1)) * tri_sz(2 * (n - e));
+        to += static_cast<size_t>(1) << (e - 1);
+    }
+    g.inst_entries = o;
+    g.inst_ts = std::max<size_t>(to, 1);
+
+    DevBuf dpool, dtpool, djobs, dpart, derr, dctr, dscr, dwork;
+    CK(cudaMalloc(&dpool.p, sizeof(T) * g.inst_entries * ninst));
+    CK(cudaMalloc(&dtpool.p, sizeof(T) * g.inst_ts * ninst));
+    CK(cudaMalloc(&djobs.p, sizeof(Job<T>) * njobs));
+    CK(cudaMalloc(&dpart.p, sizeof(double) * 5 * njobs));
+    CK(cudaMalloc(&derr.p, sizeof(unsigned long long)));
+    CK(cudaMalloc(&dctr.p, sizeof(unsigned long long)));
+    T* pool = static_cast<T*>(dpool.p);
+    T* tpool = static_cast<T*>(dtpool.p);
+    Job<T>* jobs = static_cast<Job<T>*>(djobs.p);
+    double* parts = static_cast<double*>(dpart.p);
+    unsigned long long* derrp = static_cast<unsigned long long*>(derr.p);
+    unsigned long long* dctrp = static_cast<unsigned long long*>(dctr.p);
+
+    // upload R of every instance (host -> device, pinned staging is the caller's concern)
+    {
+        std::vector<T> host(static_cast<size_t>(tri_sz(2 * n)));
+        for (int i = 0; i < ninst; ++i) {
+            const auto& R = inputs[i].R;
+            for (size_t k = 0; k < host.size(); ++k) {
+                double w[4] = {0, 0, 0, 0};
+                for (int x = 0; x < K; ++x) w[x] = R[k * K + x];
+                if constexpr (K == 1) host[k] = w[0];
+                else if constexpr (K == 2) host[k] = dd{w[0], w[1]};
+                else host[k] = qd{{w[0], w[1], w[2], w[3]}};
+            }
+            CK(cudaMemcpyAsync(pool + i * g.inst_entries, host.data(), sizeof(T) * host.size(),
+                               cudaMemcpyHostToDevice, st));
+            CK(cudaStreamSynchronize(st));
+        }
+    }
+    const unsigned long long no_err = ~0ull;
+    CK(cudaMemcpyAsync(derrp, &no_err, sizeof(no_err), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(dctrp, 0, sizeof(unsigned long long), st));
+    CK(cudaEventRecord(ev0, st));
+
+    // ---- prefix
+    if (use_levels) {
+        const int wpb = 4;
+        const size_t sm = sizeof(T) * 4 * n * wpb;
+        for (int e = 1; e <= g.c; ++e) {
+            const uint64_t items = (1ull << (e - 1)) * ninst;
+            const uint64_t blocks = std::min<uint64_t>((items + wpb - 1) / wpb, 65535ull * 4);
+            prefix_level_kernel<T><<<static_cast<unsigned>(blocks), 32 * wpb, sm, st>>>(g, pool, tpool, e, ninst,
+                                                                                          derrp);
+            ++launches;
+        }
+        const uint64_t lo = clo << (c - kbits), hi = chi << (c - kbits);
+        const uint64_t blocks = std::min<uint64_t>((njobs + 255) / 256, 1ull << 20);
+        make_jobs_kernel<T><<<static_cast<unsigned>(blocks), 256, 0, st>>>(g, pool, tpool, ninst, lo, hi, jobs);
+        ++launches;
+    } else {
+        const size_t stride = 2 * static_cast<size_t>(tri_sz(2 * n));
+        CK(cudaMalloc(&dwork.p, sizeof(T) * stride * njobs));
+        const int wpb = 4;
+        const size_t sm = sizeof(T) * (4 * n * wpb + wpb);
+        const uint64_t blocks = std::min<uint64_t>((njobs + wpb - 1) / wpb, 65535ull * 4);
+        direct_prefix_kernel<T><<<static_cast<unsigned>(blocks), 32 * wpb, sm, st>>>(
+            n, kbits, pool, ninst, g.inst_entries, clo, chi, static_cast<T*>(dwork.p), stride, jobs, derrp);
+        ++launches;
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ev1, st));
+
+    // ---- subtrees
+    if (rjob >= Q0) {
+        using SM = WarpSmem<T>;
+        constexpr int WPB = Cfg<T>::WPB;
+        const size_t smem = SM::kBytes * WPB;
+        CK(cudaFuncSetAttribute(subtree_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+        int bps = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, subtree_kernel<T>, 32 * WPB, smem));
+        if (bps < 1) {
+            err = "subtree kernel does not fit on an SM";
+            return -1;
+        }
+        uint64_t blocks = static_cast<uint64_t>(bps) * prop.multiProcessorCount;
+        blocks = std::min<uint64_t>(blocks, (njobs + WPB - 1) / WPB);
+        const int D = rjob - Q0;
+        size_t stride = 0;
+        for (int x = 1; x <= D; ++x) stride += tri_sz(2 * (rjob - x));
+        stride = std::max<size_t>(stride, 1);
+        CK(cudaMalloc(&dscr.p, sizeof(T) * stride * blocks * WPB));
+        subtree_kernel<T><<<static_cast<unsigned>(blocks), 32 * WPB, smem, st>>>(
+            jobs, njobs, n, rjob, static_cast<T*>(dscr.p), stride, parts, derrp, dctrp);
+        ++launches;
+    } else {
+        const uint64_t blocks = (njobs + 127) / 128;
+        small_job_kernel<T, Q0 - 1><<<static_cast<unsigned>(blocks), 128, 0, st>>>(jobs, njobs, n, rjob, parts,
+                                                                                   derrp);
+        ++launches;
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ev2, st));
+
+    // ---- per-instance fixed-order fold
+    fold_kernel<T><<<ninst, 256, 0, st>>>(parts, per);
+    ++launches;
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ev3, st));
+
+    std::vector<double> res(static_cast<size_t>(ninst) * 5);
+    for (int i = 0; i < ninst; ++i)
+        CK(cudaMemcpyAsync(&res[i * 5], parts + static_cast<size_t>(i) * per * 5, 5 * sizeof(double),
+                           cudaMemcpyDeviceToHost, st));
+    unsigned long long herr = 0;
+    CK(cudaMemcpyAsync(&herr, derrp, sizeof(herr), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+
+    out.assign(ninst, EngineOut{});
+    const uint64_t terms = (chi - clo) << (n - kbits);
+    for (int i = 0; i < ninst; ++i) {
+        for (int x = 0; x < 4; ++x) out[i].words[x] = res[i * 5 + x];
+        out[i].sum_abs = res[i * 5 + 4];
+        out[i].terms = terms;
+        if (herr != ~0ull) {
+            out[i].breakdown = true;
+            out[i].bad_mask = herr >> 8;
+            out[i].bad_row = static_cast<int>(herr & 0xff);
+        }
+    }
+    if (stats) {
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, ev1, ev2);
+        cudaEventElapsedTime(&b, ev0, ev3);
+        stats->kernel_ms = a;
+        stats->total_ms = b;
+        stats->launches = launches;
+        stats->prefix_depth = cj;
+        stats->jobs = njobs;
+    }
+    return 0;
+}
+
+}  // namespace
+
+int engine_tree_min_n(int mode) {
+    return mode == MODE_QD ? Cfg<qd>::L + FAN : Cfg<dd>::L + FAN;
+}
+
+int engine_run(int device, int mode, const std::vector<PreparedInput>& inputs, const WorkRange& range,
+               std::vector<EngineOut>& out, EngineStats* stats, std::string& err) {
+    if (inputs.empty()) {
+        out.clear();
+        return 0;
+    }
+    switch (mode) {
+        case MODE_FP64:
+            return run_impl<double>(device, inputs, range, out, stats, err);
+        case MODE_DD:
+            return run_impl<dd>(device, inputs, range, out, stats, err);
+        case MODE_QD:
+            return run_impl<qd>(device, inputs, range, out, stats, err);
+        default:
+            err = "bad mode";
+            return -1;
+    }
+}
+
+void fold_words(int mode, const double* parts, int count, double* out5) {
+    // same pairwise tree as fold_kernel over `count` shard partials (5 doubles each)
+    std::vector<double> p(parts, parts + 5 * static_cast<size_t>(count));
+    for (int s = 1; s < count; s <<= 1)
+        for (int i = 0; i + s < count; i += 2 * s) {
+            if (mode == MODE_QD) merge_words<qd>(&p[5 * i], &p[5 * (i + s)]);
+            else merge_words<dd>(&p[5 * i], &p[5 * (i + s)]);
+        }
+    for (int i = 0; i < 5; ++i) out5[i] = count ? p[i] : 0.0;
+}
+
+}  // namespace tor

@@ -1,0 +1,69 @@
+// Torontonian engine: internal host-side interface of the sm_100a kernels.
+//
+// Replaces the reference's per-subset O(z^3) evaluation loop
+//   torontonian_partial<W> (torontonian.cpp:72-103) -> extract_i_minus_az (:44-65)
+//   -> hermitian_det_fixed (linalg.cpp:7-61) -> fp_rsqrt (fixed_point.cpp:110)
+// and its thread fan-out run_engine<W> (torontonian.cpp:112-147) with a
+// prefix-tree Schur-complement recursion on the real symmetric matrix
+// R = T (I - O) T^H (pair order x_j, p_j), amortised O(1) work per subset.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace tor {
+
+enum Mode : int { MODE_FP64 = 0, MODE_DD = 1, MODE_QD = 2 };
+
+inline int mode_words(int mode) { return mode == MODE_FP64 ? 1 : (mode == MODE_DD ? 2 : 4); }
+
+// One problem instance after host preparation: the exact R matrix in the mode's
+// word format (packed upper triangle of the 2n x 2n matrix, pair order, `words`
+// doubles per entry).
+struct PreparedInput {
+    int n = 0;
+    std::vector<double> R;  // tri(2n) * words
+};
+
+// Work selection: prefix classes of the top `class_bits` reference-mask bits
+// (bit N-1-j = mode j, subsets.hpp:11-13), classes [class_lo, class_hi).
+// class_bits = 0 and [0,1) means the whole Torontonian.
+struct WorkRange {
+    int class_bits = 0;
+    uint64_t class_lo = 0;
+    uint64_t class_hi = 1;
+};
+
+// Per-instance outcome.
+struct EngineOut {
+    double words[4] = {0, 0, 0, 0};  // signed sum, multi-word (1/2/4 significant words)
+    double sum_abs = 0.0;            // sum |term| (fp64)
+    uint64_t terms = 0;
+    bool breakdown = false;
+    uint64_t bad_mask = 0;           // reference mask convention
+    int bad_row = -1;                // pair-order pivot row (2k: x_k, 2k+1: p_k)
+};
+
+struct EngineStats {
+    double kernel_ms = 0.0;       // subtree kernel (device time, CUDA events)
+    double total_ms = 0.0;        // whole device pipeline incl. prefix + reduction
+    uint64_t launches = 0;        // kernels launched
+    int prefix_depth = 0;
+    uint64_t jobs = 0;
+};
+
+// Runs the engine on `device` for all instances (same n) over `range`.
+// Returns 0 or a CUDA error code; errors are described in `err`.
+int engine_run(int device, int mode, const std::vector<PreparedInput>& inputs, const WorkRange& range,
+               std::vector<EngineOut>& out, EngineStats* stats, std::string& err);
+
+// Fixed-order binary fold of per-shard partials (power-of-two aligned shards),
+// identical to the device reduction tree so results are bit-identical for any
+// shard count.  `parts` are `count` x 5 doubles (4 words + sum_abs).
+void fold_words(int mode, const double* parts, int count, double* out5);
+
+// Minimum instance size handled by the tree kernel; smaller n uses the direct path.
+int engine_tree_min_n(int mode);
+
+}  // namespace tor

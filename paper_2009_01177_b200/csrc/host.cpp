@@ -1,0 +1,291 @@
+// Host-side restatement of the reference's validation / precision logic for the C
+// ABI.  The decisions (widths, bit budgets, fraction bits, k_corr) must be
+// bit-identical to the reference's select_precision / force_width, so the
+// floating-point expressions keep the reference's evaluation order; the cited
+// lines are the behaviour each function reproduces.  Built with -O3 and
+// -ffp-contract=off.
+#include "host.hpp"
+
+#include <algorithm>
+#include <cmath>
+
+#include "../../include/tor_capi.h"
+#include "arith.cuh"
+
+namespace tor {
+
+namespace {
+
+constexpr double kTol = 1e-12;          // matrix_io.hpp:62
+constexpr double kCorrMin = 0.0009;     // precision.cpp:11
+constexpr double kCorrMax = 0.0035;     // precision.cpp:12
+
+inline size_t tri(int n, int i, int j) {
+    return static_cast<size_t>(i) * n - static_cast<size_t>(i) * (i + 1) / 2 + static_cast<size_t>(j);
+}
+
+// Packed complex upper triangle of dim d (HermitianFloat, linalg.hpp:27-30).
+struct HermF {
+    int d = 0;
+    std::vector<std::complex<double>> u;
+    std::complex<double>& at(int i, int j) { return u[tri(d, i, j)]; }
+};
+
+// hermitian_det_float (linalg.cpp:66-88): pivot product of the upper-triangle
+// elimination in double; non-finite -> PrecisionError("linalg/nonfinite").
+double herm_det(HermF m) {
+    const int n = m.d;
+    double det = 1.0;
+    for (int k = 0; k < n; ++k) {
+        const double pivot = m.at(k, k).real();
+        det *= pivot;
+        if (k == n - 1) break;
+        const double pinv = 1.0 / pivot;
+        for (int i = k + 1; i < n; ++i) {
+            const std::complex<double> s = std::conj(m.at(k, i)) * pinv;
+            m.at(i, i) -= std::complex<double>((s * m.at(k, i)).real(), 0.0);
+            for (int j = i + 1; j < n; ++j) m.at(i, j) -= s * m.at(k, j);
+        }
+    }
+    if (!std::isfinite(det))
+        throw HostError(TOR_E_PRECISION, "linalg/nonfinite", "non-finite determinant in float elimination");
+    return det;
+}
+
+int upper_bits(const Input& a) {  // precision.cpp:73-78
+    const double det = det_i_minus_a_float(a);
+    if (!(det > 0.0)) throw HostError(TOR_E_PRECISION, "precision/det-nonpositive", "det(I-A) must be positive");
+    return std::max(1, static_cast<int>(std::ceil(-std::log2(det))));
+}
+
+int lower_bits(int N, double a_repr, double k_corr) {  // precision.cpp:52-71
+    if (N < 1) throw HostError(TOR_E_INVALID, "precision/range", "N must be >= 1");
+    if (a_repr <= 0.0) return 0;
+    if (!(a_repr < 1.0))
+        throw HostError(TOR_E_PRECISION, "precision/model-range", "representative diagonal must be < 1");
+    const double one_minus_a = 1.0 - a_repr;
+    if (!(k_corr * N / one_minus_a < one_minus_a))
+        throw HostError(TOR_E_PRECISION, "precision/model-range",
+                        "correction term leaves the model's validity domain");
+    const double base = (a_repr / one_minus_a) * std::pow(1.0 - k_corr * N / (one_minus_a * one_minus_a), 2);
+    const double bits = -static_cast<double>(N) * std::log2(base);
+    return std::max(0, static_cast<int>(std::ceil(bits)));
+}
+
+}  // namespace
+
+std::complex<double> Input::a00_at(int i, int j) const {
+    if (i <= j) return a00[tri(n, i, j)];
+    return std::conj(a00[tri(n, j, i)]);
+}
+std::complex<double> Input::a01_at(int i, int j) const {
+    if (i <= j) return a01[tri(n, i, j)];
+    return a01[tri(n, j, i)];
+}
+
+Input make_input(int n, const double* a00, const double* a01) {
+    Input m;
+    m.n = n;
+    const size_t t = static_cast<size_t>(n) * (n + 1) / 2;
+    m.a00.resize(t);
+    m.a01.resize(t);
+    for (size_t i = 0; i < t; ++i) {
+        m.a00[i] = {a00[2 * i], a00[2 * i + 1]};
+        m.a01[i] = {a01[2 * i], a01[2 * i + 1]};
+    }
+    return m;
+}
+
+std::vector<std::complex<double>> to_dense(const Input& a) {  // matrix_io.cpp:265-283
+    const int n = a.n, d = 2 * n;
+    std::vector<std::complex<double>> m(static_cast<size_t>(d) * d);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            const auto v00 = a.a00_at(i, j);
+            const auto v01 = a.a01_at(i, j);
+            m[static_cast<size_t>(i) * d + j] = v00;
+            m[static_cast<size_t>(i) * d + n + j] = v01;
+            m[static_cast<size_t>(n + i) * d + j] = std::conj(v01);
+            m[static_cast<size_t>(n + i) * d + n + j] = std::conj(v00);
+        }
+    return m;
+}
+
+SymReport check_symmetries(const std::vector<std::complex<double>>& dense, int two_n) {  // matrix_io.cpp:285-305
+    if (two_n < 2 || two_n % 2 != 0 || dense.size() != static_cast<size_t>(two_n) * two_n)
+        throw HostError(TOR_E_INVALID, "matrixio/dim", "dense matrix must be 2N x 2N");
+    const int n = two_n / 2;
+    auto at = [&](int i, int j) { return dense[static_cast<size_t>(i) * two_n + j]; };
+    SymReport r;
+    for (int i = 0; i < two_n; ++i)
+        for (int j = 0; j < two_n; ++j) r.hermitian_dev = std::max(r.hermitian_dev, std::abs(at(i, j) - std::conj(at(j, i))));
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            r.a01_sym_dev = std::max(r.a01_sym_dev, std::abs(at(i, n + j) - at(j, n + i)));
+            r.block_conj_dev = std::max(r.block_conj_dev, std::abs(at(i, j) - std::conj(at(n + i, n + j))));
+        }
+    r.pass = r.hermitian_dev <= kTol && r.a01_sym_dev <= kTol && r.block_conj_dev <= kTol;
+    return r;
+}
+
+double det_i_minus_a_float(const Input& a) {  // precision.cpp:16-36
+    const int n = a.n, d = 2 * n;
+    HermF m;
+    m.d = d;
+    m.u.resize(static_cast<size_t>(d) * (d + 1) / 2);
+    for (int i = 0; i < d; ++i)
+        for (int j = i; j < d; ++j) {
+            std::complex<double> v;
+            if (j < n) v = a.a00_at(i, j);
+            else if (i < n) v = a.a01_at(i, j - n);
+            else v = std::conj(a.a00_at(i - n, j - n));
+            m.at(i, j) = (i == j) ? 1.0 - v : -v;
+        }
+    return herm_det(m);
+}
+
+PrecCfg select_precision(const Input& a, int N, int sig, double alpha) {  // precision.cpp:80-121
+    if (N < 1) throw HostError(TOR_E_INVALID, "precision/range", "N must be >= 1");
+    if (sig < 1) throw HostError(TOR_E_INVALID, "precision/range", "need at least one significant digit");
+    if (!(alpha > 0.0)) throw HostError(TOR_E_INVALID, "precision/range", "alpha must be positive");
+    PrecCfg c;
+    c.alpha = alpha;
+    c.b_sgn = static_cast<int>(std::ceil(sig * std::log2(10.0)));
+    c.b_accum = static_cast<int>(std::ceil(std::log2(alpha) + N + 2.0 * std::log2(N)));
+    c.b_upper = upper_bits(a);
+    double diag_sum = 0.0;
+    for (int i = 0; i < a.n; ++i) diag_sum += a.a00_at(i, i).real();
+    c.a_repr = diag_sum / a.n;
+    const double det = det_i_minus_a_float(a);
+    double k_fit = kCorrMax;
+    if (c.a_repr > 0.0 && c.a_repr < 1.0) {
+        const double one_minus_a = 1.0 - c.a_repr;
+        const double fitted = (one_minus_a * one_minus_a - std::pow(det, 1.0 / N)) / N;
+        if (std::isfinite(fitted)) k_fit = fitted;
+    }
+    c.k_corr = std::clamp(k_fit, kCorrMin, kCorrMax);
+    c.b_lower = lower_bits(N, c.a_repr, c.k_corr);
+    const int B = c.total_bits();
+    if (B <= 128) c.width_bits = 128;
+    else if (B <= 256) c.width_bits = 256;
+    else
+        throw HostError(TOR_E_PRECISION, "precision/unsupported",
+                        "required bit budget exceeds 256 bits (B = " + std::to_string(B) + ")");
+    c.frac_bits = static_cast<unsigned>(c.width_bits - 1 - c.b_upper);
+    return c;
+}
+
+PrecCfg force_width(const Input& a, int width_bits) {  // precision.cpp:123-148
+    if (width_bits != 128 && width_bits != 256)
+        throw HostError(TOR_E_INVALID, "precision/range", "width must be 128 or 256");
+    PrecCfg c;
+    c.width_bits = width_bits;
+    c.b_sgn = static_cast<int>(std::ceil(3 * std::log2(10.0)));
+    c.b_upper = upper_bits(a);
+    const int N = a.n;
+    c.b_accum = static_cast<int>(std::ceil(std::log2(0.5) + N + 2.0 * std::log2(N)));
+    double diag_sum = 0.0;
+    for (int i = 0; i < N; ++i) diag_sum += a.a00_at(i, i).real();
+    c.a_repr = diag_sum / N;
+    c.k_corr = kCorrMax;
+    const int f = width_bits - 1 - c.b_upper;
+    if (f < 1)
+        throw HostError(TOR_E_PRECISION, "precision/scaling",
+                        "upper bound leaves no room for fraction bits at this width");
+    c.frac_bits = static_cast<unsigned>(f);
+    try {
+        c.b_lower = lower_bits(N, c.a_repr, c.k_corr);
+    } catch (const HostError&) {
+        c.b_lower = 0;
+    }
+    return c;
+}
+
+// R = T (I - O) T^H, T = (1/sqrt2)[[I, I], [-iI, iI]] per mode, P = I - A00 (diagonal
+// 1 - Re a_ii rounded to double exactly as extract_i_minus_az does,
+// torontonian.cpp:58), Q = -A01:
+//   R(x_i,x_j) = Re P + Re Q   R(x_i,p_j) = Im Q - Im P
+//   R(p_i,x_j) = Im P + Im Q   R(p_i,p_j) = Re P - Re Q
+// Each entry is the sum of two input doubles: exact as a DD (TwoSum), rounded once
+// in fp64 mode.
+std::vector<double> build_R(const Input& a, int words) {
+    const int n = a.n, d = 2 * n;
+    std::vector<double> R(static_cast<size_t>(d) * (d + 1) / 2 * words, 0.0);
+    auto P = [&](int i, int j) -> std::complex<double> {
+        if (i == j) return {1.0 - a.a00_at(i, i).real(), 0.0};
+        return -a.a00_at(i, j);
+    };
+    auto Q = [&](int i, int j) -> std::complex<double> { return -a.a01_at(i, j); };
+    for (int r = 0; r < d; ++r)
+        for (int s = r; s < d; ++s) {
+            const int i = r >> 1, j = s >> 1;
+            const bool ri = r & 1, sj = s & 1;
+            const auto p = P(i, j);
+            const auto q = Q(i, j);
+            double x, y;
+            if (!ri && !sj) { x = p.real(); y = q.real(); }
+            else if (!ri && sj) { x = q.imag(); y = -p.imag(); }
+            else if (ri && !sj) { x = p.imag(); y = q.imag(); }
+            else { x = p.real(); y = -q.real(); }
+            double hi, lo;
+            two_sum(x, y, hi, lo);
+            double* e = &R[tri(d, r, s) * words];
+            e[0] = hi;
+            if (words >= 2) e[1] = lo;
+        }
+    return R;
+}
+
+unsigned __int128 total_op_count(int n) {  // flops.cpp:15-31 (Eq. 8)
+    unsigned __int128 total = 0, binom = 1;
+    for (int z = 1; z <= n; ++z) {
+        binom = binom * (n - z + 1) / z;
+        const unsigned __int128 dd_ = 2 * static_cast<unsigned __int128>(z);
+        total += binom * ((4 * dd_ * dd_ * dd_ + 3 * dd_ * dd_ - 4 * dd_) / 3);
+    }
+    return total;
+}
+
+void op_counts(int n, uint64_t& mults, uint64_t& adds, uint64_t& recips, uint64_t& rsqrts) {
+    // Per d x d elimination (linalg.cpp:7-61): for each pivot with r rows below it,
+    // 1 det mult, r x (6 mults + 4 adds), and r(r-1)/2 x (4 mults + 4 adds).
+    unsigned __int128 m = 0, ad = 0, rc = 0, binom = 1;
+    for (int z = 1; z <= n; ++z) {
+        binom = binom * (n - z + 1) / z;
+        const int d = 2 * z;
+        unsigned __int128 mz = 0, az = 0;
+        for (int r = 0; r < d; ++r) {
+            mz += 1 + 6 * static_cast<unsigned __int128>(r) + 2 * static_cast<unsigned __int128>(r) * (r > 0 ? r - 1 : 0);
+            az += 4 * static_cast<unsigned __int128>(r) + 2 * static_cast<unsigned __int128>(r) * (r > 0 ? r - 1 : 0);
+        }
+        m += binom * mz;
+        ad += binom * az;
+        rc += binom * static_cast<unsigned __int128>(d - 1);
+    }
+    mults = static_cast<uint64_t>(m);
+    adds = static_cast<uint64_t>(ad);
+    recips = static_cast<uint64_t>(rc);
+    rsqrts = (n >= 64) ? ~0ull : ((1ull << n) - 1);
+}
+
+Input extract_submatrix(const Input& full, uint64_t bits) {  // matrix_io.cpp:360-382
+    std::vector<int> sel;
+    for (int k = 0; k < full.n; ++k)
+        if (bits >> k & 1) sel.push_back(k);
+    if (full.n < 64 && (bits >> full.n) != 0)
+        throw HostError(TOR_E_INVALID, "matrixio/dim", "pattern mode count mismatch");
+    if (sel.empty()) throw HostError(TOR_E_INVALID, "matrixio/pattern", "empty click pattern");
+    Input out;
+    out.n = static_cast<int>(sel.size());
+    const size_t t = static_cast<size_t>(out.n) * (out.n + 1) / 2;
+    out.a00.resize(t);
+    out.a01.resize(t);
+    for (int i = 0; i < out.n; ++i)
+        for (int j = i; j < out.n; ++j) {
+            out.a00[tri(out.n, i, j)] = full.a00_at(sel[i], sel[j]);
+            out.a01[tri(out.n, i, j)] = full.a01_at(sel[i], sel[j]);
+        }
+    return out;
+}
+
+}  // namespace tor
