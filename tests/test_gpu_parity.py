@@ -1,0 +1,227 @@
+"""GPU parity: the CUDA engine (through the C ABI) vs the reference's own outputs.
+
+Golden values come from the unmodified reference engine (tests/golden/reference_values.json,
+written by tests/golden/make_golden.py through oracle/_ref).  Tolerances are absolute,
+against sum |terms| because the alternating sum cancels:
+    fp64 vs torontonian_reference  2^-44 sum|t|
+    DD   vs fixed-128              2^-88 sum|t|
+    QD   vs fixed-256              2^-180 sum|t|
+plus |rel| <= 1e-3 (b_sgn = 3 digits) wherever the mode keeps the digits.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2009_01177_b200 as T
+from paper_2009_01177_b200 import workloads as W
+from paper_2009_01177_b200.matrix import InputMatrix, _upper
+from tests._util import EPS, fixed_value, within, words_value
+
+pytestmark = pytest.mark.gpu
+
+
+def diag_instance(n, a, c=None):
+    a00 = np.zeros((n, n), complex)
+    a01 = np.zeros((n, n), complex)
+    for i in range(n):
+        a00[i, i] = a[i]
+        if c is not None:
+            a01[i, i] = c[i]
+    return InputMatrix(n, _upper(a00), _upper(a01))
+
+
+def small_instance(name):
+    if name.startswith("zero_"):
+        n = int(name.split("_")[1])
+        return diag_instance(n, [0.0] * n)
+    fixed = {
+        "half_1": lambda: diag_instance(1, [0.5]),
+        "one_mode": lambda: diag_instance(1, [0.3], [0.1]),
+        "diag3": lambda: diag_instance(3, [0.1, 0.2, 0.3]),
+        "two_half": lambda: diag_instance(2, [0.5, 0.5]),
+        "breakdown6": lambda: diag_instance(6, [0.5] * 6, [0.5 - 2.0 ** -20] * 6),
+        "gen10_s1": lambda: W.generate_instance(10, 0.16, 0.06, 1),
+        "gen10_s2": lambda: W.generate_instance(10, 0.16, 0.06, 2),
+        "gen10_s3": lambda: W.generate_instance(10, 0.16, 0.06, 3),
+        "gen8_s99": lambda: W.generate_instance(8, 0.16, 0.06, 99),
+        "gen10_s321": lambda: W.generate_instance(10, 0.16, 0.06, 321),
+        "gen4_s2026": lambda: W.generate_instance(4, 0.16, 0.06, 2026),
+        "gen6_s42": lambda: W.generate_instance(6, 0.16, 0.06, 42),
+        "gen12_s7": lambda: W.generate_instance(12, 0.16, 0.06, 7),
+        "gen14_s11": lambda: W.generate_instance(14, 0.2, 0.05, 11),
+        "cfg1": lambda: W.load_config_instance(1),
+        "cfg2": lambda: W.load_config_instance(2),
+    }
+    return fixed[name]()
+
+
+GEN_CASES = ["gen10_s1", "gen10_s2", "gen10_s3", "gen8_s99", "gen10_s321", "gen4_s2026", "gen6_s42",
+             "gen12_s7", "gen14_s11", "cfg1", "cfg2"]
+
+
+@pytest.mark.parametrize("n", range(1, 11))
+def test_zero_matrix_exactly_zero(n, golden):
+    """test_torontonian.cpp:49-61: Tor(0) = 0 limb-exact, term_count = 2^N."""
+    m = small_instance(f"zero_{n}")
+    for prec in ("auto", "128", "256", "fp64"):
+        r = T.torontonian(m, prec)
+        assert r["value"] == 0.0
+        assert all(w == 0.0 for w in r["words"])
+        assert r["raw_limbs"] == (0, 0, 0, 0)
+        assert r["term_count"] == 1 << n
+    assert T.torontonian_reference(m) == 0.0
+    assert golden[f"zero_{n}"]["fixedauto"]["raw"] == "0"
+
+
+def test_closed_forms():
+    """test_torontonian.cpp:63-81 single-mode and diagonal closed forms, at DD accuracy."""
+    cases = [
+        (small_instance("half_1"), 1.0),
+        (small_instance("one_mode"), 1.0 / math.sqrt(0.7 * 0.7 - 0.01) - 1.0),
+        (small_instance("diag3"), (0.1 / 0.9) * (0.2 / 0.8) * (0.3 / 0.7)),
+        (small_instance("two_half"), 1.0),
+    ]
+    for m, want in cases:
+        for prec in ("auto", "128", "256"):
+            assert T.torontonian(m, prec)["value"] == pytest.approx(want, rel=1e-12)
+        assert T.torontonian_reference(m) == pytest.approx(want, rel=1e-12)
+
+
+@pytest.mark.parametrize("name", GEN_CASES)
+def test_modes_vs_reference(name, golden):
+    g = golden[name]
+    m = small_instance(name)
+    # DD vs reference fixed-128, QD vs fixed-256 (same inputs)
+    for prec, key, mode in (("128", "fixed128", "dd"), ("256", "fixed256", "qd")):
+        r = T.torontonian(m, prec)
+        want = fixed_value(g[key]["raw"], g[key]["frac_bits"])
+        ok, rel = within(words_value(r["words"]), want, r["sum_abs_terms"], mode)
+        assert ok, f"{name} {mode}: err = {rel:.3g} sum|t| (eps {EPS[mode]:.3g})"
+        assert abs(r["value"] - float(want)) <= 1e-3 * abs(float(want))
+        assert r["config"]["frac_bits"] == g[key]["frac_bits"]
+        assert r["counters"] == g[key]["counters"]
+    # fp64 mode vs the reference fp64 oracle (both accurate to ~2^-44 sum|t| only)
+    if isinstance(g.get("fp64_reference"), float):
+        v = T.torontonian_reference(m)
+        r = T.torontonian(m, "fp64")
+        ok, rel = within(v, g["fp64_reference"], r["sum_abs_terms"], "fp64")
+        assert ok, f"{name} fp64: err = {rel:.3g} sum|t|"
+        # and the GPU fp64 vs the exact (fixed-256) value
+        ok2, rel2 = within(v, fixed_value(g["fixed256"]["raw"], g["fixed256"]["frac_bits"]), r["sum_abs_terms"], "fp64")
+        assert ok2, f"{name} fp64 vs fixed256: {rel2:.3g}"
+
+
+@pytest.mark.parametrize("name", GEN_CASES)
+def test_auto_matches_reference_selection(name, golden):
+    g = golden[name]
+    m = small_instance(name)
+    r = T.torontonian(m, "auto")
+    sel = g["select_precision"]
+    assert r["config"]["width_bits"] == sel["width_bits"]
+    assert r["config"]["frac_bits"] == sel["frac_bits"]
+    assert r["width_bits"] == sel["width_bits"] or r["escalated"]
+
+
+def test_breakdown_instance_succeeds_in_floating_words(golden):
+    """test_torontonian.cpp:218-244: fixed-128 breaks down (fraction bits exhausted);
+    DD/QD keep relative precision and reproduce the closed form."""
+    g = golden["breakdown6"]
+    assert g["fixed128"]["error"] == "linalg/breakdown"
+    m = small_instance("breakdown6")
+    c = 0.5 - 2.0 ** -20
+    want = (1.0 / math.sqrt(0.25 - c * c) - 1.0) ** 6
+    for prec in ("128", "256"):
+        r = T.torontonian(m, prec)
+        assert abs(r["value"] - want) / want < 1e-9
+    # the reference's own 256-bit value is only good to ~3e-5 here
+    assert abs(g["fixed256"]["value"] - want) / want < 1e-3
+
+
+def test_cfg3_items(golden):
+    items = golden["cfg3_items"]
+    ms = [W.load_config_instance(3, int(i)) for i in sorted(items, key=int)]
+    batch_dd = T.torontonian_batch(ms, "128")
+    batch_64 = T.torontonian_batch(ms, "fp64")
+    for k, (i, g) in enumerate(sorted(items.items(), key=lambda kv: int(kv[0]))):
+        want = fixed_value(g["fixed128"]["raw"], g["fixed128"]["frac_bits"])
+        ok, rel = within(words_value(batch_dd[k]["words"]), want, batch_dd[k]["sum_abs_terms"], "dd")
+        assert ok, f"cfg3 item {i}: {rel:.3g}"
+        single = T.torontonian(ms[k], "128")
+        assert single["words"] == batch_dd[k]["words"], "batch must be bit-identical to single runs"
+        ok, rel = within(words_value(batch_64[k]["words"]), want, batch_64[k]["sum_abs_terms"], "fp64")
+        assert ok, f"cfg3 item {i} fp64: {rel:.3g}"
+
+
+@pytest.mark.parametrize("cfg", ["cfg4_slices", "cfg5_slices"])
+def test_large_n_slices(cfg, golden):
+    """n=32 / 40: prefix-class slices through the reference's per-mask templates."""
+    g = golden[cfg]
+    m = W.load_config_instance(4 if cfg == "cfg4_slices" else 5)
+    k = g["k"]
+    for width, mode, prec in (("128", "dd", "128"), ("256", "qd", "256")):
+        if width not in g["widths"]:
+            continue
+        gw = g["widths"][width]
+        for c in gw["classes"]:
+            p = T.torontonian_slice(m, prec, k, c["cls"], c["cls"] + 1)
+            want = fixed_value(c["raw"], gw["frac_bits"])
+            ok, rel = within(words_value(p["words"]), want, c["sum_abs"], mode)
+            assert ok, f"{cfg} class {c['cls']:#x} {mode}: {rel:.3g} sum|t|"
+            assert p["sum_abs"] == pytest.approx(c["sum_abs"], rel=1e-9)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_shards_fold_bit_identical(world):
+    m = W.load_config_instance(2)
+    for prec in ("128", "256", "fp64"):
+        whole = T.torontonian(m, prec)
+        parts = [T.torontonian_shard(m, prec, r, world) for r in range(world)]
+        folded = T.fold_partials(parts, m)
+        assert folded["words"] == whole["words"]
+        assert folded["sum_abs_terms"] == whole["sum_abs_terms"]
+
+
+def test_determinism_reruns():
+    m = W.load_config_instance(1)
+    a = T.torontonian(m, "128")
+    b = T.torontonian(m, "128")
+    assert a["words"] == b["words"]
+
+
+def test_input_validation():
+    big = diag_instance(41, [0.0] * 41)
+    with pytest.raises(T.InvalidArgument):
+        T.torontonian(big)
+    wide = diag_instance(21, [0.0] * 21)
+    with pytest.raises(T.InvalidArgument):
+        T.torontonian_reference(wide)
+    skew = diag_instance(2, [0.2, 0.2])
+    skew.a00[0] = 0.2 + 0.05j
+    with pytest.raises(T.TorfpError) as e:
+        T.torontonian(skew)
+    assert e.value.code == "torontonian/symmetry"
+    indef = diag_instance(1, [0.5], [0.7])
+    with pytest.raises(T.PrecisionError):
+        T.torontonian(indef)
+
+
+def test_indefinite_breakdown_reports_mask():
+    """A non-positive pivot in working precision raises linalg/breakdown with a mask."""
+    m = diag_instance(3, [0.1, 0.5, 0.1], [0.0, 0.7, 0.0])
+    with pytest.raises((T.BreakdownError, T.PrecisionError)):
+        T.torontonian(m, "128")
+
+
+def test_probabilities():
+    """test_torontonian.cpp:246-268."""
+    a = diag_instance(1, [0.3], [0.1])
+    det = 0.7 * 0.7 - 0.01
+    p1 = T.probability(a, 1)
+    p0 = T.probability(a, 0)
+    assert p1 == pytest.approx(1.0 - math.sqrt(det), rel=1e-12)
+    assert p0 == pytest.approx(math.sqrt(det), rel=1e-12)
+    m = W.generate_instance(4, 0.16, 0.06, 1234)
+    assert sum(T.probability_reference(m, b) for b in range(16)) == pytest.approx(1.0, rel=1e-9)
