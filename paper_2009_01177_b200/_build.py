@@ -12,7 +12,7 @@ from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "build")
+BUILD = os.environ.get("TOR_BUILD_DIR") or os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libtor_b200.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -52,15 +52,16 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in srcs)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    lib_path = out or LIB
+    if not force and out is None and up_to_date():
         return LIB
     ch = cuda_home()
     nvcc = os.path.join(ch, "bin", "nvcc")
     inc = ["-I" + os.path.join(ch, "include"), "-I" + os.path.join(os.path.dirname(PKG), "include")]
     os.makedirs(BUILD, exist_ok=True)
     jobs = [
-        ([nvcc] + NVCC_FLAGS + inc + ["-c", os.path.join(CSRC, "engine.cu"), "-o", os.path.join(BUILD, "engine.o")],
+        ([nvcc] + NVCC_FLAGS + [f"-D{d}" for d in defines] + inc + ["-c", os.path.join(CSRC, "engine.cu"), "-o", os.path.join(BUILD, "engine.o")],
          os.path.join(BUILD, "engine.log")),
         (["g++"] + CXX_FLAGS + inc + ["-c", os.path.join(CSRC, "host.cpp"), "-o", os.path.join(BUILD, "host.o")],
          os.path.join(BUILD, "host.log")),
@@ -69,14 +70,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     ]
     with ThreadPoolExecutor(len(jobs)) as ex:
         list(ex.map(lambda j: _run(*j), jobs))
-    tmp = LIB + ".tmp"
+    tmp = lib_path + ".tmp"
     _run([nvcc] + ARCH + ["-shared", "-o", tmp, os.path.join(BUILD, "engine.o"), os.path.join(BUILD, "host.o"),
                           os.path.join(BUILD, "capi.o"), "-lcudart_static", "-lrt", "-lpthread", "-ldl"],
          os.path.join(BUILD, "link.log"))
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib_path)
     if verbose:
         print(open(os.path.join(BUILD, "engine.log")).read())
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":

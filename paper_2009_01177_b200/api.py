@@ -19,7 +19,7 @@ from . import errors as E
 from .matrix import InputMatrix
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libtor_b200.so")
+LIB_PATH = os.environ.get("TOR_B200_LIB") or os.path.join(_PKG, "libtor_b200.so")
 
 PREC_AUTO, PREC_DD, PREC_QD, PREC_FP64 = 0, 1, 2, 3
 _PREC = {"auto": PREC_AUTO, "128": PREC_DD, "dd": PREC_DD, "256": PREC_QD, "qd": PREC_QD,

@@ -351,6 +351,7 @@ template <> struct Acc<double> {
         s.lo += e;
         abs_sum += fabs(t);
     }
+    TOR_HD void flush() {}
     TOR_HD void merge(const Acc& o) {
         s = dd_add(s, o.s);
         abs_sum += o.abs_sum;
@@ -365,11 +366,26 @@ template <> struct Acc<double> {
 };
 
 template <> struct Acc<dd> {
+    // running sum s (accurate DD) + a lazily renormalised block (h, c): per term one
+    // TwoSum on the leading words and one plain add for the low words; the block is
+    // folded into s by flush() every few terms (lane subtrees), keeping the lazy
+    // error below 2^-98 of the block's term magnitudes.
     dd s{0.0, 0.0};
+    double h = 0.0, c = 0.0;
     double abs_sum = 0.0;
     TOR_HD void add(const dd& t, bool negative) {
-        s = dd_add(s, negative ? dd_neg(t) : t);
+        const double th = negative ? -t.hi : t.hi;
+        const double tl = negative ? -t.lo : t.lo;
+        double nh, e;
+        two_sum(h, th, nh, e);
+        h = nh;
+        c += tl + e;
         abs_sum += fabs(t.hi);
+    }
+    TOR_HD void flush() {
+        s = dd_add(s, dd_norm(dd{h, c}));
+        h = 0.0;
+        c = 0.0;
     }
     TOR_HD void merge(const Acc& o) {
         s = dd_add(s, o.s);
@@ -390,6 +406,7 @@ template <> struct Acc<qd> {
         s = qd_add(s, negative ? qd_neg(t) : t);
         abs_sum += fabs(t.x[0]);
     }
+    TOR_HD void flush() {}
     TOR_HD void merge(const Acc& o) {
         s = qd_add(s, o.s);
         abs_sum += o.abs_sum;

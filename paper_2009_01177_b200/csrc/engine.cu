@@ -21,7 +21,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "arith.cuh"
@@ -33,6 +35,7 @@ namespace {
 
 constexpr int FAN = 5;  // breadth-first fan-out levels -> 32 lane nodes
 constexpr int MAX_LEVELS = 48;
+constexpr int kMaxJobModes = 24;
 
 __host__ __device__ constexpr int tri_sz(int d) { return d * (d + 1) / 2; }
 __host__ __device__ __forceinline__ int tri_ix(int d, int i, int j) {
@@ -120,6 +123,45 @@ template <> __device__ __forceinline__ void warp_fold<double>(Acc<double>& a) {
     }
 }
 
+// Pivot chain of one mode elimination (rows 0,1 of the view): Cholesky pivots
+// rho1 = 1/sqrt(s00) and rho2 = 1/sqrt(s11 - s01^2/s00), computed as
+// rho2 = sqrt(s00) * rhod with rhod = 1/sqrt(det2), det2 = s00 s11 - s01^2, so the
+// two reciprocal square roots are independent (half the dependent latency of the
+// textbook chain); the child's term factor is t * rhod.
+template <class T> struct Piv {
+    T r1, u1, r2, tn;
+    bool bad0, bad1;
+};
+template <class T>
+__device__ __forceinline__ Piv<T> pivot2(const T& s00, const T& s01, const T& s11, const T& t) {
+    using A = Arith<T>;
+    Piv<T> p;
+    const T a = A::norm(s00);
+    p.bad0 = nonpositive(A::hi(a));
+    p.r1 = A::rsqrt(a);
+    const T det = A::norm(A::rank1(A::mul(a, s11), s01, s01));
+    p.bad1 = nonpositive(A::hi(det));
+    const T rd = A::rsqrt(det);
+    p.u1 = A::mul(s01, p.r1);
+    p.r2 = A::mul(A::mul(a, p.r1), rd);
+    p.tn = A::mul(t, rd);
+    return p;
+}
+
+#ifdef TOR_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[32];
+#define PHASE_T0() long long _pt = clock64()
+#define PHASE_MARK(k)                                                                \
+    do {                                                                             \
+        const long long _pn = clock64();                                             \
+        if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[k], (unsigned long long)(_pn - _pt)); \
+        _pt = _pn;                                                                   \
+    } while (0)
+#else
+#define PHASE_T0()
+#define PHASE_MARK(k)
+#endif
+
 // ------------------------------------------------ warp-cooperative elimination --
 // Eliminates the first mode (rows 0,1) of the q-mode view (S, d, sr) into the
 // packed (2q-2)-row triangle dst; t_out = t * rho1 * rho2.  uw: shared scratch of
@@ -129,16 +171,11 @@ __device__ void warp_elim(const T* S, int d, int sr, int q, T* dst, const T& t_i
                           uint64_t mask, int nsel, unsigned long long* err) {
     using A = Arith<T>;
     const int lane = threadIdx.x & 31;
-    const T a = A::norm(S[tri_ix(d, sr, sr)]);
-    const bool bad0 = nonpositive(A::hi(a));
-    const T r1 = A::rsqrt(a);
-    const T u1 = A::mul(S[tri_ix(d, sr, sr + 1)], r1);
-    const T b = A::norm(A::rank1(S[tri_ix(d, sr + 1, sr + 1)], u1, u1));
-    const bool bad1 = nonpositive(A::hi(b));
-    const T r2 = A::rsqrt(b);
+    const Piv<T> pv = pivot2<T>(S[tri_ix(d, sr, sr)], S[tri_ix(d, sr, sr + 1)], S[tri_ix(d, sr + 1, sr + 1)], t_in);
+    const T r1 = pv.r1, u1 = pv.u1, r2 = pv.r2;
     if (lane == 0) {
-        if (bad0 || bad1) report_breakdown(err, mask, 2 * nsel + (bad0 ? 0 : 1));
-        *t_out = A::mul(A::mul(t_in, r1), r2);
+        if (pv.bad0 || pv.bad1) report_breakdown(err, mask, 2 * nsel + (pv.bad0 ? 0 : 1));
+        *t_out = pv.tn;
     }
     const int m = 2 * q;
     for (int j = 2 + lane; j < m; j += 32) {
@@ -148,6 +185,8 @@ __device__ void warp_elim(const T* S, int d, int sr, int q, T* dst, const T& t_i
         uw[m + j] = wj;
     }
     __syncwarp();
+    // trailing update: 4 entries per lane per round, loads issued together so the
+    // (L2-resident) source reads overlap; positions advance incrementally.
     const int dn = m - 2;
     const int total = tri_sz(dn);
     int i = 0, k0 = lane;
@@ -156,13 +195,26 @@ __device__ void warp_elim(const T* S, int d, int sr, int q, T* dst, const T& t_i
         ++i;
     }
     int j = i + k0;
-    for (int k = lane; k < total; k += 32) {
-        dst[k] = A::rank2(S[tri_ix(d, sr + 2 + i, sr + 2 + j)], uw[2 + i], uw[2 + j], uw[m + 2 + i],
-                          uw[m + 2 + j]);
-        j += 32;
-        while (i < dn && j >= dn) {
-            j -= dn - (i + 1);
-            ++i;
+    for (int kb = 0; kb < total; kb += 128) {
+        int ii[4], jj[4];
+        T sv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const bool ok = kb + lane + 32 * u < total;
+            ii[u] = ok ? i : 0;
+            jj[u] = ok ? j : 0;
+            sv[u] = S[tri_ix(d, sr + 2 + ii[u], sr + 2 + jj[u])];
+            j += 32;
+            while (i < dn && j >= dn) {
+                j -= dn - (i + 1);
+                ++i;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const T v = A::rank2(sv[u], uw[2 + ii[u]], uw[2 + jj[u]], uw[m + 2 + ii[u]], uw[m + 2 + jj[u]]);
+            const int k = kb + lane + 32 * u;
+            if (k < total) dst[k] = v;
         }
     }
     __syncwarp();
@@ -308,15 +360,10 @@ __device__ __forceinline__ void elim_reg(const St<T, Q>& S, St<T, Q - 1>& out, c
                                          int nsel, unsigned long long* err) {
     using A = Arith<T>;
     constexpr int M = 2 * Q;
-    const T a = A::norm(S.e[cix<M>(0, 0)]);
-    const bool bad0 = nonpositive(A::hi(a));
-    const T r1 = A::rsqrt(a);
-    const T u1 = A::mul(S.e[cix<M>(0, 1)], r1);
-    const T b = A::norm(A::rank1(S.e[cix<M>(1, 1)], u1, u1));
-    const bool bad1 = nonpositive(A::hi(b));
-    const T r2 = A::rsqrt(b);
-    if (bad0 || bad1) report_breakdown(err, mask, 2 * nsel + (bad0 ? 0 : 1));
-    tout = A::mul(A::mul(t, r1), r2);
+    const Piv<T> pv = pivot2<T>(S.e[cix<M>(0, 0)], S.e[cix<M>(0, 1)], S.e[cix<M>(1, 1)], t);
+    const T r1 = pv.r1, u1 = pv.u1, r2 = pv.r2;
+    if (pv.bad0 || pv.bad1) report_breakdown(err, mask, 2 * nsel + (pv.bad0 ? 0 : 1));
+    tout = pv.tn;
     T u[M], w[M];
 #pragma unroll
     for (int j = 2; j < M; ++j) {
@@ -332,28 +379,43 @@ __device__ __forceinline__ void elim_reg(const St<T, Q>& S, St<T, Q - 1>& out, c
 
 // All nonempty subsets of the Q register modes (the node's own term excluded).
 // neg: sign of the current node's term; bits: reference mask of the node.
+// Levels with Q >= kLoopQ run their include/exclude branches as a 2-trip loop so
+// the subtree below is emitted once (instruction-cache footprint grows with L, not
+// 2^L); lower levels stay fully unrolled for instruction-level parallelism.
+#ifndef TOR_LOOPQ
+#define TOR_LOOPQ 3
+#endif
+constexpr int kLoopQ = TOR_LOOPQ;
+
 template <class T, int Q> struct SubReg {
-    __device__ __forceinline__ static void run(const St<T, Q>& S, const T& t, bool neg, uint64_t mask, int nsel,
-                                               Acc<T>& acc, unsigned long long* err) {
-        using A = Arith<T>;
+    __device__ __forceinline__ static void branch(const St<T, Q>& S, int br, const T& t, bool neg, uint64_t mask,
+                                                  int nsel, Acc<T>& acc, unsigned long long* err) {
+        constexpr int M = 2 * Q;
         const uint64_t bit = 1ull << (Q - 1);
-        {
-            St<T, Q - 1> Sn;
-            T tn;
+        St<T, Q - 1> Sn;
+        T tn;
+        if (br == 0) {
             elim_reg<T, Q>(S, Sn, t, tn, mask | bit, nsel, err);
             acc.add(tn, !neg);
-            SubReg<T, Q - 1>::run(Sn, tn, !neg, mask | bit, nsel + 1, acc, err);
-        }
-        {
-            St<T, Q - 1> Sx;
-            constexpr int M = 2 * Q;
+        } else {
 #pragma unroll
             for (int i = 2; i < M; ++i)
 #pragma unroll
-                for (int j = i; j < M; ++j) Sx.e[cix<M - 2>(i - 2, j - 2)] = S.e[cix<M>(i, j)];
-            SubReg<T, Q - 1>::run(Sx, t, neg, mask, nsel, acc, err);
+                for (int j = i; j < M; ++j) Sn.e[cix<M - 2>(i - 2, j - 2)] = S.e[cix<M>(i, j)];
+            tn = t;
         }
-        (void)sizeof(A);
+        SubReg<T, Q - 1>::run(Sn, tn, br == 0 ? !neg : neg, br == 0 ? (mask | bit) : mask, nsel + (br == 0),
+                              acc, err);
+    }
+    __device__ __forceinline__ static void run(const St<T, Q>& S, const T& t, bool neg, uint64_t mask, int nsel,
+                                               Acc<T>& acc, unsigned long long* err) {
+        if constexpr (Q >= kLoopQ) {
+#pragma unroll 1
+            for (int br = 0; br < 2; ++br) branch(S, br, t, neg, mask, nsel, acc, err);
+        } else {
+            branch(S, 0, t, neg, mask, nsel, acc, err);
+            branch(S, 1, t, neg, mask, nsel, acc, err);
+        }
     }
 };
 template <class T> struct SubReg<T, 1> {
@@ -368,7 +430,8 @@ template <class T> struct SubReg<T, 1> {
 };
 
 // Lane subtree rooted at an L-mode view in shared memory: emits the node's own
-// term and all 2^L - 1 extensions.
+// term and all 2^L - 1 extensions.  Branch 0 includes the first view mode (its
+// elimination reads shared memory), branch 1 excludes it (loads the trailing block).
 template <class T, int L>
 __device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t, bool neg, uint64_t mask, int nsel,
                                           Acc<T>& acc, unsigned long long* err) {
@@ -376,68 +439,78 @@ __device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t,
     constexpr int M = 2 * L;
     acc.add(t, neg);
     const uint64_t bit = 1ull << (L - 1);
-    {
-        // include the first view mode: elimination reads shared memory
-        const T a = A::norm(S[tri_ix(d, sr, sr)]);
-        const bool bad0 = nonpositive(A::hi(a));
-        const T r1 = A::rsqrt(a);
-        const T u1 = A::mul(S[tri_ix(d, sr, sr + 1)], r1);
-        const T b = A::norm(A::rank1(S[tri_ix(d, sr + 1, sr + 1)], u1, u1));
-        const bool bad1 = nonpositive(A::hi(b));
-        const T r2 = A::rsqrt(b);
-        if (bad0 || bad1) report_breakdown(err, mask | bit, 2 * nsel + (bad0 ? 0 : 1));
-        const T tn = A::mul(A::mul(t, r1), r2);
-        T u[M], w[M];
-#pragma unroll
-        for (int j = 2; j < M; ++j) {
-            u[j] = A::mul(S[tri_ix(d, sr, sr + j)], r1);
-            w[j] = A::mul(A::rank1(S[tri_ix(d, sr + 1, sr + j)], u1, u[j]), r2);
-        }
+#pragma unroll 1
+    for (int br = 0; br < 2; ++br) {
         St<T, L - 1> Sn;
+        T tn;
+        if (br == 0) {
+            const Piv<T> pv = pivot2<T>(S[tri_ix(d, sr, sr)], S[tri_ix(d, sr, sr + 1)], S[tri_ix(d, sr + 1, sr + 1)], t);
+            const T r1 = pv.r1, u1 = pv.u1, r2 = pv.r2;
+            if (pv.bad0 || pv.bad1) report_breakdown(err, mask | bit, 2 * nsel + (pv.bad0 ? 0 : 1));
+            tn = pv.tn;
+            T u[M], w[M];
 #pragma unroll
-        for (int i = 2; i < M; ++i)
+            for (int j = 2; j < M; ++j) {
+                u[j] = A::mul(S[tri_ix(d, sr, sr + j)], r1);
+                w[j] = A::mul(A::rank1(S[tri_ix(d, sr + 1, sr + j)], u1, u[j]), r2);
+            }
 #pragma unroll
-            for (int j = i; j < M; ++j)
-                Sn.e[cix<M - 2>(i - 2, j - 2)] = A::rank2(S[tri_ix(d, sr + i, sr + j)], u[i], u[j], w[i], w[j]);
-        acc.add(tn, !neg);
-        SubReg<T, L - 1>::run(Sn, tn, !neg, mask | bit, nsel + 1, acc, err);
-    }
-    {
-        St<T, L - 1> Sx;
+            for (int i = 2; i < M; ++i)
 #pragma unroll
-        for (int i = 2; i < M; ++i)
+                for (int j = i; j < M; ++j)
+                    Sn.e[cix<M - 2>(i - 2, j - 2)] =
+                        A::rank2(S[tri_ix(d, sr + i, sr + j)], u[i], u[j], w[i], w[j]);
+            acc.add(tn, !neg);
+        } else {
 #pragma unroll
-            for (int j = i; j < M; ++j) Sx.e[cix<M - 2>(i - 2, j - 2)] = S[tri_ix(d, sr + i, sr + j)];
-        SubReg<T, L - 1>::run(Sx, t, neg, mask, nsel, acc, err);
+            for (int i = 2; i < M; ++i)
+#pragma unroll
+                for (int j = i; j < M; ++j) Sn.e[cix<M - 2>(i - 2, j - 2)] = S[tri_ix(d, sr + i, sr + j)];
+            tn = t;
+        }
+        SubReg<T, L - 1>::run(Sn, tn, br == 0 ? !neg : neg, br == 0 ? (mask | bit) : mask, nsel + (br == 0), acc,
+                              err);
     }
 }
 
 // --------------------------------------------------------- subtree kernel ----
+// Per-warp shared memory: the Q0-mode root (copy of the DFS leaf view), the
+// include buffers of the 5 fan-out levels, their t values, pivots, pivot-row
+// vectors and per-level parent descriptors.  Per block: (i,j) lookup tables of
+// the packed triangles the kernel walks (built once per block).
 template <class T> struct WarpSmem {
     static constexpr int L = Cfg<T>::L;
     static constexpr int Q0 = L + FAN;
-    // level e buffers: 2^(e-1) x tri(2(Q0-e)); level 0: the root (copy of the leaf view)
     __host__ __device__ static constexpr int lvl_off(int e) {
         int o = tri_sz(2 * Q0);
         for (int x = 1; x < e; ++x) o += (1 << (x - 1)) * tri_sz(2 * (Q0 - x));
         return e == 0 ? 0 : o;
     }
     static constexpr int kBufEntries = lvl_off(FAN + 1);
-    static constexpr int kTOff = kBufEntries;                 // t per level buffer (index 2^(e-1)-1+p)
-    static constexpr int kPivOff = kTOff + 32;                // r1, u1, r2 per elimination (16 each)
-    static constexpr int kUwOff = kPivOff + 48;               // u/w vectors: 16 elims x 4 x Q0
+    static constexpr int kTOff = kBufEntries;   // t of level buffers at 2^(e-1)-1+p, root t at 31
+    static constexpr int kPivOff = kTOff + 32;  // r1 / u1 / r2 of up to 16 eliminations
     __host__ __device__ static constexpr int uw_need() {
-        int mx = 4 * 24;  // DFS eliminations: 4q entries, q <= kMaxJobModes
+        int mx = 4 * kMaxJobModes;  // DFS eliminations: 4q entries
         for (int e = 1; e <= FAN; ++e) {
             const int need = (1 << (e - 1)) * 2 * 2 * (Q0 - e + 1);
             if (need > mx) mx = need;
         }
         return mx;
     }
+    static constexpr int kUwOff = kPivOff + 48;
     static constexpr int kUwEntries = uw_need();
-    static constexpr int kDfsT = kUwOff + kUwEntries;         // DFS slot t values
-    static constexpr int kEntries = kDfsT + 64;
-    static constexpr size_t kBytes = kEntries * sizeof(T);
+    static constexpr int kDfsT = kUwOff + kUwEntries;  // DFS slot t values (<= 32)
+    static constexpr int kEntries = kDfsT + 32;
+    static constexpr int kDescInts = 16 * 4;           // per-level parent descriptors
+    static constexpr size_t kWarpBytes = kEntries * sizeof(T) + kDescInts * sizeof(int);
+    // (i,j) tables for triangle dims 2*(Q0-e), e = 0..FAN  (u16: i << 8 | j)
+    __host__ __device__ static constexpr int tab_off(int e) {
+        int o = 0;
+        for (int x = 0; x < e; ++x) o += tri_sz(2 * (Q0 - x));
+        return o;
+    }
+    static constexpr int kTabEntries = tab_off(FAN + 1);
+    static constexpr size_t kTabBytes = ((kTabEntries * 2 + 15) / 16) * 16;
 };
 
 template <class T, int Q0>
@@ -448,35 +521,168 @@ __device__ __forceinline__ void lane_view(const T* sm, int c, const T*& base, in
         base = sm;
         dim = 2 * Q0;
         skip = e;
-        t = tvals[31];  // root t stored at slot 31
+        t = tvals[31];
         return;
     }
     const int tz = __ffs(c) - 1;
     const int lvl = e - tz;
     const int p = (c >> tz) >> 1;
     dim = 2 * (Q0 - lvl);
-    base = sm + WarpSmem<T>::lvl_off(lvl) + p * tri_sz(dim);
+    int off = tri_sz(2 * Q0);
+#pragma unroll
+    for (int x = 1; x < FAN; ++x)
+        if (x < lvl) off += (1 << (x - 1)) * tri_sz(2 * (Q0 - x));
+    base = sm + off + p * tri_sz(dim);
     skip = tz;
     t = tvals[(1 << (lvl - 1)) - 1 + p];
 }
+
+// One breadth-first level: the E = 2^(e-1) include nodes of level e each eliminate
+// the first mode of their parent (level e-1 node x) into level-e buffer x.
+template <class T, int E_LVL> struct FanLevel {
+    static constexpr int Q0 = WarpSmem<T>::Q0;
+    static constexpr int E = 1 << (E_LVL - 1);
+    static constexpr int q = Q0 - E_LVL + 1;  // parent modes
+    static constexpr int m = 2 * q;
+    static constexpr int dn = m - 2;
+    static constexpr int tn = tri_sz(dn);
+    __device__ __forceinline__ static void run(T* sm, T* tvals, T* piv, T* uwv, int* desc, const uint16_t* tabs,
+                                               uint64_t leaf_mask, int leaf_sel, unsigned long long* err) {
+        using A = Arith<T>;
+        const int lane = threadIdx.x & 31;
+        PHASE_T0();
+        {
+            const int x = lane & (E - 1);
+            const T* pb;
+            int pd, psk;
+            T pt;
+            lane_view<T, Q0>(sm, x, pb, pd, psk, pt, tvals, E_LVL - 1);
+            const int sr = 2 * psk;
+            const Piv<T> pv = pivot2<T>(pb[tri_ix(pd, sr, sr)], pb[tri_ix(pd, sr, sr + 1)], pb[tri_ix(pd, sr + 1, sr + 1)], pt);
+            if (lane < E) {
+                const uint64_t nm = leaf_mask | (static_cast<uint64_t>((x << 1) | 1) << (Q0 - E_LVL));
+                if (pv.bad0 || pv.bad1) report_breakdown(err, nm, 2 * (leaf_sel + __popc(x)) + (pv.bad0 ? 0 : 1));
+                piv[x] = pv.r1;
+                piv[16 + x] = pv.u1;
+                piv[32 + x] = pv.r2;
+                tvals[E - 1 + x] = pv.tn;
+                desc[4 * x + 0] = static_cast<int>(pb - sm);
+                desc[4 * x + 1] = pd;
+                desc[4 * x + 2] = sr;
+            }
+        }
+        __syncwarp();
+        PHASE_MARK(5 + 3 * (E_LVL - 1));
+        // pivot-row vectors u_j, w_j (j = 2..m-1) of every elimination.  Loops are
+        // branch-free (clamped item, predicated store) so unrolled iterations overlap.
+        constexpr int NV = E * (m - 2);
+        constexpr int NVI = (NV + 31) / 32;
+        {
+            T s0v[NVI], s1v[NVI], r1v[NVI], u1v[NVI], r2v[NVI];
+            int xo[NVI];
+#pragma unroll
+            for (int u = 0; u < NVI; ++u) {
+                const int it0 = lane + 32 * u;
+                const int it = it0 < NV ? it0 : NV - 1;
+                const int x = it / (m - 2);
+                const int j = 2 + it - x * (m - 2);
+                const T* pb = sm + desc[4 * x];
+                const int pd = desc[4 * x + 1], sr = desc[4 * x + 2];
+                s0v[u] = pb[tri_ix(pd, sr, sr + j)];
+                s1v[u] = pb[tri_ix(pd, sr + 1, sr + j)];
+                r1v[u] = piv[x];
+                u1v[u] = piv[16 + x];
+                r2v[u] = piv[32 + x];
+                xo[u] = x * 2 * m + j;
+            }
+#pragma unroll
+            for (int u = 0; u < NVI; ++u) {
+                s0v[u] = A::mul(s0v[u], r1v[u]);
+                s1v[u] = A::mul(A::rank1(s1v[u], u1v[u], s0v[u]), r2v[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < NVI; ++u)
+                if (lane + 32 * u < NV) {
+                    uwv[xo[u]] = s0v[u];
+                    uwv[xo[u] + m] = s1v[u];
+                }
+        }
+        __syncwarp();
+        PHASE_MARK(6 + 3 * (E_LVL - 1));
+        // trailing updates into the level-e buffers
+        T* lvl = sm + WarpSmem<T>::lvl_off(E_LVL);
+        const uint16_t* tab = tabs + WarpSmem<T>::tab_off(E_LVL);
+        constexpr int NE = E * tn;
+        constexpr int NIT = (NE + 31) / 32;
+        constexpr int UB = 4;  // items per batch: all loads of a batch precede its stores
+#pragma unroll 1
+        for (int s0 = 0; s0 < NIT; s0 += UB) {
+            T sv[UB], ui[UB], uj[UB], wi[UB], wj[UB];
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const int it0 = lane + 32 * (s0 + u);
+                const int it = it0 < NE ? it0 : NE - 1;
+                const int x = it / tn;
+                const int k = it - x * tn;
+                const int ij = tab[k];
+                const int i = ij >> 8, j = ij & 0xff;
+                const T* pb = sm + desc[4 * x];
+                const int pd = desc[4 * x + 1], sr = desc[4 * x + 2];
+                const T* uw = uwv + x * 2 * m;
+                sv[u] = pb[tri_ix(pd, sr + 2 + i, sr + 2 + j)];
+                ui[u] = uw[2 + i];
+                uj[u] = uw[2 + j];
+                wi[u] = uw[m + 2 + i];
+                wj[u] = uw[m + 2 + j];
+            }
+#pragma unroll
+            for (int u = 0; u < UB; ++u) sv[u] = A::rank2(sv[u], ui[u], uj[u], wi[u], wj[u]);
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const int it0 = lane + 32 * (s0 + u);
+                if (it0 < NE && s0 + u < NIT) lvl[it0] = sv[u];
+            }
+        }
+        __syncwarp();
+        PHASE_MARK(7 + 3 * (E_LVL - 1));
+        __syncwarp();
+    }
+};
+
 
 template <class T>
 __global__ void __launch_bounds__(32 * Cfg<T>::WPB)
     subtree_kernel(const Job<T>* jobs, uint64_t njobs, int nmodes, int rjob, T* scratch, size_t scratch_stride,
                    double* partials, unsigned long long* err, unsigned long long* job_counter) {
-    using A = Arith<T>;
     using SM = WarpSmem<T>;
     constexpr int L = Cfg<T>::L;
     constexpr int Q0 = SM::Q0;
+    constexpr int WPB = Cfg<T>::WPB;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint16_t* tabs = reinterpret_cast<uint16_t*>(smem_raw);
+    // block-wide (i,j) tables
+    for (int e = 0; e <= FAN; ++e) {
+        const int D = 2 * (Q0 - e);
+        for (int k = threadIdx.x; k < tri_sz(D); k += blockDim.x) {
+            int i = 0, r = k;
+            while (r >= D - i) {
+                r -= D - i;
+                ++i;
+            }
+            tabs[SM::tab_off(e) + k] = static_cast<uint16_t>((i << 8) | (i + r));
+        }
+    }
+    __syncthreads();
     const int wib = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    T* sm = reinterpret_cast<T*>(smem_raw) + wib * SM::kEntries;
+    unsigned char* wbase = smem_raw + SM::kTabBytes + wib * SM::kWarpBytes;
+    T* sm = reinterpret_cast<T*>(wbase);
+    int* desc = reinterpret_cast<int*>(wbase + SM::kEntries * sizeof(T));
     T* tvals = sm + SM::kTOff;
     T* piv = sm + SM::kPivOff;
     T* uwv = sm + SM::kUwOff;
     T* dfs_t = sm + SM::kDfsT;
-    const int gw = blockIdx.x * Cfg<T>::WPB + wib;
+    const int gw = blockIdx.x * WPB + wib;
     T* slots = scratch + static_cast<size_t>(gw) * scratch_stride;
     const int D = rjob - Q0;
 
@@ -489,6 +695,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB)
         Acc<T> acc;
 
         for (uint64_t leaf = 0; leaf < (1ull << D); ++leaf) {
+            PHASE_T0();
             if (leaf > 0) {
                 // flip exclude->include at depth kd (lowest set bit of leaf)
                 const int b = __ffsll(static_cast<long long>(leaf)) - 1;
@@ -518,6 +725,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB)
                 const int lsel = J.nsel + __popcll(above);
                 warp_elim<T>(src, sd, 2 * ssk, rjob - kd, slots + doff, st, dfs_t + kd + 1, uwv, lmask, lsel, err);
             }
+            PHASE_MARK(0);
             // leaf view (depth D of the job) -> copy the Q0-mode root into shared memory
             const T* lb;
             int ld, lsk;
@@ -539,113 +747,46 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB)
             }
             __syncwarp();
             {
-                constexpr int RM = 2 * Q0;
+                constexpr int RT = tri_sz(2 * Q0);
+                constexpr int RI = (RT + 31) / 32;
                 const int sr = 2 * lsk;
-                int i = 0, k0 = lane;
-                while (i < RM && k0 >= RM - i) {
-                    k0 -= RM - i;
-                    ++i;
+                T rv[RI];
+#pragma unroll
+                for (int s = 0; s < RI; ++s) {
+                    const int k0 = lane + 32 * s;
+                    const int ij = tabs[k0 < RT ? k0 : RT - 1];
+                    rv[s] = lb[tri_ix(ld, sr + (ij >> 8), sr + (ij & 0xff))];
                 }
-                int j = i + k0;
-                for (int k = lane; k < tri_sz(RM); k += 32) {
-                    sm[k] = lb[tri_ix(ld, sr + i, sr + j)];
-                    j += 32;
-                    while (i < RM && j >= RM) {
-                        j -= RM - (i + 1);
-                        ++i;
-                    }
-                }
+#pragma unroll
+                for (int s = 0; s < RI; ++s)
+                    if (lane + 32 * s < RT) sm[lane + 32 * s] = rv[s];
                 if (lane == 0) tvals[31] = lt;
             }
             __syncwarp();
             const uint64_t leaf_mask = J.mask | (leaf << Q0);
             const int leaf_sel = J.nsel + __popcll(leaf);
 
-            // breadth-first fan-out: level e creates 2^(e-1) include buffers
-#pragma unroll
-            for (int e = 1; e <= FAN; ++e) {
-                const int E = 1 << (e - 1);
-                const int q = Q0 - e + 1;  // parent modes
-                const int m = 2 * q;
-                // pivots: lane x < E handles elimination x (parent node (e-1, x))
-                {
-                    const int x = lane & (E - 1);
-                    const T* pb;
-                    int pd, psk;
-                    T pt;
-                    lane_view<T, Q0>(sm, x, pb, pd, psk, pt, tvals, e - 1);
-                    const int sr = 2 * psk;
-                    const T a = A::norm(pb[tri_ix(pd, sr, sr)]);
-                    const bool bad0 = nonpositive(A::hi(a));
-                    const T r1 = A::rsqrt(a);
-                    const T u1 = A::mul(pb[tri_ix(pd, sr, sr + 1)], r1);
-                    const T bb = A::norm(A::rank1(pb[tri_ix(pd, sr + 1, sr + 1)], u1, u1));
-                    const bool bad1 = nonpositive(A::hi(bb));
-                    const T r2 = A::rsqrt(bb);
-                    if (lane < E) {
-                        const uint64_t nm = leaf_mask | (static_cast<uint64_t>((x << 1) | 1) << (Q0 - e));
-                        if (bad0 || bad1)
-                            report_breakdown(err, nm, 2 * (leaf_sel + __popc(x)) + (bad0 ? 0 : 1));
-                        piv[x] = r1;
-                        piv[16 + x] = u1;
-                        piv[32 + x] = r2;
-                        tvals[E - 1 + x] = A::mul(A::mul(pt, r1), r2);
-                    }
-                }
-                __syncwarp();
-                // pivot-row vectors
-                for (int it = lane; it < E * (m - 2); it += 32) {
-                    const int x = it / (m - 2);
-                    const int j = 2 + it % (m - 2);
-                    const T* pb;
-                    int pd, psk;
-                    T pt;
-                    lane_view<T, Q0>(sm, x, pb, pd, psk, pt, tvals, e - 1);
-                    const int sr = 2 * psk;
-                    const T uj = A::mul(pb[tri_ix(pd, sr, sr + j)], piv[x]);
-                    const T wj = A::mul(A::rank1(pb[tri_ix(pd, sr + 1, sr + j)], piv[16 + x], uj), piv[32 + x]);
-                    uwv[x * 2 * m + j] = uj;
-                    uwv[x * 2 * m + m + j] = wj;
-                }
-                __syncwarp();
-                // trailing updates into the level-e buffers
-                const int dn = m - 2;
-                const int tn = tri_sz(dn);
-                T* lvl = sm + SM::lvl_off(e);
-                for (int it = lane; it < E * tn; it += 32) {
-                    const int x = it / tn;
-                    int k = it % tn;
-                    int i = 0;
-                    while (k >= dn - i) {
-                        k -= dn - i;
-                        ++i;
-                    }
-                    const int j = i + k;
-                    const T* pb;
-                    int pd, psk;
-                    T pt;
-                    lane_view<T, Q0>(sm, x, pb, pd, psk, pt, tvals, e - 1);
-                    const int sr = 2 * psk;
-                    const T* uw = uwv + x * 2 * m;
-                    lvl[x * tn + tri_ix(dn, i, j)] =
-                        A::rank2(pb[tri_ix(pd, sr + 2 + i, sr + 2 + j)], uw[2 + i], uw[2 + j], uw[m + 2 + i], uw[m + 2 + j]);
-                }
-                __syncwarp();
-            }
+            PHASE_MARK(1);
+            FanLevel<T, 1>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err);
+            FanLevel<T, 2>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err);
+            FanLevel<T, 3>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err);
+            FanLevel<T, 4>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err);
+            FanLevel<T, 5>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err);
+
             // lanes: node (FAN, lane)
             {
                 const T* vb;
                 int vd, vsk;
                 T vt;
                 lane_view<T, Q0>(sm, lane, vb, vd, vsk, vt, tvals, FAN);
-                const int pc = __popc(lane);
                 const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(lane) << L);
-                const int lsel = leaf_sel + pc;
-                // term sign of the node: (-1)^(n - |Z|)
-                const bool nodeneg = ((nmodes - lsel) & 1) != 0;
+                const int lsel = leaf_sel + __popc(lane);
+                const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
                 lane_tree<T, L>(vb, vd, 2 * vsk, vt, nodeneg, lmask, lsel, acc, err);
+                acc.flush();
             }
             __syncwarp();
+            PHASE_MARK(4);
         }
         warp_fold<T>(acc);
         if (lane == 0) {
@@ -661,7 +802,6 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB)
         __syncwarp();
     }
 }
-
 
 // ----------------------------------------------------------- small jobs ----
 // Jobs whose state has fewer than Q0 modes (small n, deep slices): one thread per
@@ -702,6 +842,7 @@ __global__ void small_job_kernel(const Job<T>* jobs, uint64_t njobs, int nmodes,
         }
         const bool neg = ((nmodes - J.nsel - z) & 1) != 0;
         acc.add(t, neg);
+        acc.flush();
     }
     double wds[4];
     acc.words(wds);
@@ -749,8 +890,6 @@ __global__ void fold_kernel(double* partials, uint64_t per) {
         }                                                                             \
     } while (0)
 
-constexpr int kMaxJobModes = 24;
-
 int ilog2_floor(uint64_t v) {
     int r = -1;
     while (v) {
@@ -777,9 +916,18 @@ int run_impl(int device, const std::vector<PreparedInput>& inputs, const WorkRan
     const int n = inputs[0].n;
     const int kbits = range.class_bits;
     const uint64_t clo = range.class_lo, chi = range.class_hi;
+    const bool dbg = std::getenv("TOR_DEBUG_TIMING") != nullptr;
+    auto tick = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!dbg) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[tor] %-10s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - tick).count());
+        tick = now;
+    };
     CK(cudaSetDevice(device));
-    cudaDeviceProp prop;
-    CK(cudaGetDeviceProperties(&prop, device));
+    int sm_count = 0;
+    CK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device));
+    lap("setdevice");
     cudaStream_t st;
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     struct StreamGuard {
@@ -865,6 +1013,7 @@ int run_impl(int device, const std::vector<PreparedInput>& inputs, const WorkRan
             CK(cudaStreamSynchronize(st));
         }
     }
+    lap("alloc+up");
     const unsigned long long no_err = ~0ull;
     CK(cudaMemcpyAsync(derrp, &no_err, sizeof(no_err), cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(dctrp, 0, sizeof(unsigned long long), st));
@@ -902,7 +1051,7 @@ int run_impl(int device, const std::vector<PreparedInput>& inputs, const WorkRan
     if (rjob >= Q0) {
         using SM = WarpSmem<T>;
         constexpr int WPB = Cfg<T>::WPB;
-        const size_t smem = SM::kBytes * WPB;
+        const size_t smem = SM::kTabBytes + SM::kWarpBytes * WPB;
         CK(cudaFuncSetAttribute(subtree_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
         int bps = 0;
@@ -911,7 +1060,7 @@ int run_impl(int device, const std::vector<PreparedInput>& inputs, const WorkRan
             err = "subtree kernel does not fit on an SM";
             return -1;
         }
-        uint64_t blocks = static_cast<uint64_t>(bps) * prop.multiProcessorCount;
+        uint64_t blocks = static_cast<uint64_t>(bps) * sm_count;
         blocks = std::min<uint64_t>(blocks, (njobs + WPB - 1) / WPB);
         const int D = rjob - Q0;
         size_t stride = 0;
@@ -943,6 +1092,22 @@ int run_impl(int device, const std::vector<PreparedInput>& inputs, const WorkRan
     unsigned long long herr = 0;
     CK(cudaMemcpyAsync(&herr, derrp, sizeof(herr), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    lap("device");
+#ifdef TOR_PHASE_TIMING
+    {
+        unsigned long long pc[32];
+        cudaMemcpyFromSymbol(pc, g_phase_cycles, sizeof(pc));
+        const char* names[20] = {"dfs_elim", "root_copy", "-", "-", "lane_tree",
+                                 "L1 piv", "L1 vec", "L1 ent", "L2 piv", "L2 vec", "L2 ent", "L3 piv", "L3 vec", "L3 ent",
+                                 "L4 piv", "L4 vec", "L4 ent", "L5 piv", "L5 vec", "L5 ent"};
+        double tot = 0;
+        for (int i = 0; i < 20; ++i) tot += pc[i];
+        for (int i = 0; i < 20; ++i)
+            if (pc[i]) std::fprintf(stderr, "[phase] %-10s %6.2f%%  %.3e warp-cycles\n", names[i], 100.0 * pc[i] / tot, (double)pc[i]);
+        unsigned long long z[32] = {0};
+        cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+    }
+#endif
 
     out.assign(ninst, EngineOut{});
     const uint64_t terms = (chi - clo) << (n - kbits);
