@@ -119,6 +119,8 @@ typedef struct {
     double cancellation_bits; /* log2(sum|t| / |Tor|) */
     double bits_left;         /* mantissa - cancellation - growth allowance */
     uint64_t kernel_launches; /* device kernels launched by the call */
+    uint64_t h2d_bytes;       /* host->device bytes copied by the call */
+    uint64_t d2h_bytes;       /* device->host bytes copied by the call */
 } tor_result;
 
 /* Shard partial for multi-GPU / multi-process folds: a contiguous, power-of-two
@@ -181,6 +183,16 @@ int tor_fold_partials(const tor_partial* parts, int count, const tor_input* in, 
 /* p(S) = Tor(A_S) sqrt(det(I - A)) (torontonian.cpp:202-209); pattern bit k = mode k. */
 int tor_probability(const tor_input* full, uint64_t pattern_bits, tor_precision prec, int device,
                     double* p, tor_error* err);
+
+/* Prepared evaluation with device-resident inputs (the exact R is uploaded once):
+ * create -> execute (repeatable; runs the whole device pipeline and reads back the
+ * result words) -> destroy.  The range is [class_lo, class_hi) of the top class_bits
+ * mask bits ([0,1) of 0 bits = the whole Torontonian).  prec must not be AUTO. */
+typedef struct tor_plan tor_plan;
+int tor_plan_create(const tor_input* in, tor_precision prec, int class_bits, uint64_t class_lo,
+                    uint64_t class_hi, int device, tor_plan** out, tor_error* err);
+int tor_plan_execute(tor_plan* plan, tor_result* out, tor_error* err);
+void tor_plan_destroy(tor_plan* plan);
 
 /* Number of CUDA devices visible (0 without a GPU). */
 int tor_device_count(void);

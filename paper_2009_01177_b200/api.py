@@ -48,7 +48,8 @@ class TorResult(C.Structure):
                 ("mults", C.c_uint64), ("adds", C.c_uint64), ("recips", C.c_uint64), ("rsqrts", C.c_uint64),
                 ("wall_seconds", C.c_double), ("device_ms", C.c_double), ("kernel_ms", C.c_double),
                 ("devices", C.c_int), ("escalated", C.c_int), ("sum_abs_terms", C.c_double),
-                ("cancellation_bits", C.c_double), ("bits_left", C.c_double), ("kernel_launches", C.c_uint64)]
+                ("cancellation_bits", C.c_double), ("bits_left", C.c_double), ("kernel_launches", C.c_uint64),
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
 
 
 class TorPartial(C.Structure):
@@ -60,7 +61,7 @@ class TorPartial(C.Structure):
 EXPORTS = ("tor_abi_version", "tor_check_symmetries", "tor_check_dense", "tor_det_i_minus_a",
            "tor_select_precision", "tor_force_width", "tor_torontonian", "tor_torontonian_reference",
            "tor_torontonian_batch", "tor_torontonian_slice", "tor_torontonian_shard", "tor_fold_partials",
-           "tor_probability", "tor_device_count")
+           "tor_probability", "tor_device_count", "tor_plan_create", "tor_plan_execute", "tor_plan_destroy")
 
 _lib = None
 
@@ -89,6 +90,11 @@ def lib():
         L.tor_check_dense.argtypes = [C.c_int, P(C.c_double), P(C.c_double), P(C.c_int), P(TorError)]
         L.tor_det_i_minus_a.argtypes = [P(TorInput), P(C.c_double), P(TorError)]
         L.tor_probability.argtypes = [P(TorInput), C.c_uint64, C.c_int, C.c_int, P(C.c_double), P(TorError)]
+        L.tor_plan_create.argtypes = [P(TorInput), C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int,
+                                      P(C.c_void_p), P(TorError)]
+        L.tor_plan_execute.argtypes = [C.c_void_p, P(TorResult), P(TorError)]
+        L.tor_plan_destroy.argtypes = [C.c_void_p]
+        L.tor_plan_destroy.restype = None
         _lib = L
     return _lib
 
@@ -159,6 +165,8 @@ def _result_dict(r: TorResult, workers: int) -> dict:
         "cancellation_bits": r.cancellation_bits,
         "bits_left": r.bits_left,
         "kernel_launches": r.kernel_launches,
+        "h2d_bytes": r.h2d_bytes,
+        "d2h_bytes": r.d2h_bytes,
     }
 
 
@@ -282,6 +290,36 @@ def probability(matrix: InputMatrix, pattern_bits: int, workers: int = 0, precis
 
 def probability_reference(matrix: InputMatrix, pattern_bits: int) -> float:
     return probability(matrix, pattern_bits, precision="fp64")
+
+
+class Plan:
+    """Device-resident evaluation (tor_plan_*): inputs uploaded once, execute() reruns the
+    whole device pipeline.  Used by bench.py for the HBM-resident throughput figure."""
+
+    def __init__(self, matrix: InputMatrix, precision, class_bits: int = 0, class_lo: int = 0,
+                 class_hi: int = 1, device: int = 0):
+        self._inp = _In(matrix)
+        self._h = C.c_void_p()
+        err = TorError()
+        _check(lib().tor_plan_create(C.byref(self._inp.s), _prec(precision), class_bits, class_lo, class_hi,
+                                     device, C.byref(self._h), C.byref(err)), err)
+
+    def execute(self) -> dict:
+        r = TorResult()
+        err = TorError()
+        _check(lib().tor_plan_execute(self._h, C.byref(r), C.byref(err)), err)
+        return _result_dict(r, 1)
+
+    def close(self) -> None:
+        if self._h:
+            lib().tor_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def device_count() -> int:

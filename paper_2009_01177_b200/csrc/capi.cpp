@@ -125,9 +125,19 @@ void fill_result(const Input& a, int mode, const PrecCfg& cfg, const EngineOut& 
     // error growth allowance: log2(n) + 4 bits over the working precision
     r->bits_left = mantissa_bits(mode) - r->cancellation_bits - (std::log2(static_cast<double>(a.n)) + 4.0);
     r->kernel_launches = st.launches;
+    r->h2d_bytes = st.h2d_bytes;
+    r->d2h_bytes = st.d2h_bytes;
 }
 
 }  // namespace
+
+struct tor_plan {
+    Input in;
+    int mode = MODE_DD;
+    PrecCfg cfg;
+    Plan* plan = nullptr;
+    ~tor_plan() { delete plan; }
+};
 
 extern "C" {
 
@@ -387,6 +397,67 @@ int tor_fold_partials(const tor_partial* parts, int count, const tor_input* in, 
         return fail(err, h);
     }
 }
+
+int tor_plan_create(const tor_input* in, tor_precision prec, int class_bits, uint64_t class_lo, uint64_t class_hi,
+                    int device, tor_plan** out, tor_error* err) {
+    try {
+        clear_err(err);
+        *out = nullptr;
+        const Input a = checked_input(in, 40);
+        if (prec == TOR_PREC_AUTO || prec < TOR_PREC_AUTO || prec > TOR_PREC_FP64)
+            throw HostError(TOR_E_INVALID, "precision/range", "plan needs an explicit mode");
+        if (class_bits < 0 || class_bits > a.n || class_hi <= class_lo || class_hi > (1ull << class_bits))
+            throw HostError(TOR_E_INVALID, "torontonian/slice", "bad class range");
+        device_check(device);
+        auto* p = new tor_plan();
+        p->in = a;
+        p->mode = mode_of(prec);
+        if (p->mode == MODE_FP64) p->cfg.width_bits = 64;
+        else p->cfg = force_width(a, p->mode == MODE_DD ? 128 : 256);
+        PreparedInput pi;
+        pi.n = a.n;
+        pi.R = build_R(a, mode_words(p->mode));
+        WorkRange wr;
+        wr.class_bits = class_bits;
+        wr.class_lo = class_lo;
+        wr.class_hi = class_hi;
+        std::string e;
+        if (plan_create(device, p->mode, {pi}, wr, &p->plan, e) != 0) {
+            delete p;
+            throw HostError(TOR_E_DEVICE, "device/cuda", e);
+        }
+        *out = p;
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+int tor_plan_execute(tor_plan* plan, tor_result* out, tor_error* err) {
+    try {
+        clear_err(err);
+        if (!plan || !plan->plan) throw HostError(TOR_E_INVALID, "torontonian/plan", "null plan");
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<EngineOut> res;
+        EngineStats st;
+        std::string e;
+        if (plan->plan->execute(res, &st, e) != 0) throw HostError(TOR_E_DEVICE, "device/cuda", e);
+        if (res[0].breakdown) {
+            HostError h(TOR_E_BREAKDOWN, "linalg/breakdown", "non-positive pivot in elimination");
+            h.pivot_row = res[0].bad_row;
+            h.subset_mask = res[0].bad_mask;
+            throw h;
+        }
+        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        st.h2d_bytes = 0;  // inputs are resident
+        fill_result(plan->in, plan->mode, plan->cfg, res[0], st, wall, 1, out);
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+void tor_plan_destroy(tor_plan* plan) { delete plan; }
 
 int tor_probability(const tor_input* full, uint64_t pattern_bits, tor_precision prec, int device, double* p,
                     tor_error* err) {

@@ -890,116 +890,97 @@ __global__ void fold_kernel(double* partials, uint64_t per) {
         }                                                                             \
     } while (0)
 
-int ilog2_floor(uint64_t v) {
-    int r = -1;
-    while (v) {
-        v >>= 1;
-        ++r;
-    }
-    return r;
-}
-
 struct DevBuf {
     void* p = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() {
         if (p) cudaFree(p);
     }
 };
 
+// A prepared evaluation: geometry chosen, device buffers allocated, the exact R of
+// every instance resident in HBM.  execute() runs the whole device pipeline
+// (prefix levels -> jobs -> subtree kernel -> fixed-order fold) and reads back
+// 5 doubles per instance; it can be called repeatedly (inputs stay resident).
 template <class T>
-int run_impl(int device, const std::vector<PreparedInput>& inputs, const WorkRange& range,
-             std::vector<EngineOut>& out, EngineStats* stats, std::string& err) {
-    constexpr int K = Arith<T>::K;
-    constexpr int L = Cfg<T>::L;
-    constexpr int Q0 = L + FAN;
-    const int ninst = static_cast<int>(inputs.size());
-    const int n = inputs[0].n;
-    const int kbits = range.class_bits;
-    const uint64_t clo = range.class_lo, chi = range.class_hi;
-    const bool dbg = std::getenv("TOR_DEBUG_TIMING") != nullptr;
-    auto tick = std::chrono::steady_clock::now();
-    auto lap = [&](const char* what) {
-        if (!dbg) return;
-        const auto now = std::chrono::steady_clock::now();
-        std::fprintf(stderr, "[tor] %-10s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - tick).count());
-        tick = now;
-    };
-    CK(cudaSetDevice(device));
-    int sm_count = 0;
-    CK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device));
-    lap("setdevice");
-    cudaStream_t st;
-    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    struct StreamGuard {
-        cudaStream_t s;
-        ~StreamGuard() { cudaStreamDestroy(s); }
-    } sg{st};
-    cudaEvent_t ev0, ev1, ev2, ev3;
-    CK(cudaEventCreate(&ev0));
-    CK(cudaEventCreate(&ev1));
-    CK(cudaEventCreate(&ev2));
-    CK(cudaEventCreate(&ev3));
-    struct EvGuard {
-        cudaEvent_t a, b, c, d;
-        ~EvGuard() {
-            cudaEventDestroy(a);
-            cudaEventDestroy(b);
-            cudaEventDestroy(c);
-            cudaEventDestroy(d);
+class PlanImpl final : public Plan {
+  public:
+    int init(int device, const std::vector<PreparedInput>& inputs, const WorkRange& range, std::string& err) {
+        constexpr int K = Arith<T>::K;
+        constexpr int Q0 = Cfg<T>::L + FAN;
+        device_ = device;
+        ninst_ = static_cast<int>(inputs.size());
+        n_ = inputs[0].n;
+        kbits_ = range.class_bits;
+        clo_ = range.class_lo;
+        chi_ = range.class_hi;
+        CK(cudaSetDevice(device));
+        CK(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+        for (auto& e : ev_) CK(cudaEventCreate(&e));
+
+        // prefix depth: enough jobs to fill the GPU, job states <= kMaxJobModes modes
+        const uint64_t want_jobs = 16384;
+        c_ = 0;
+        if (n_ >= Q0) {
+            int cw = 0;
+            while ((static_cast<uint64_t>(ninst_) << cw) < want_jobs && cw < n_ - Q0) ++cw;
+            c_ = std::max(cw, n_ - kMaxJobModes);
+            c_ = std::min(c_, n_ - Q0);
         }
-    } eg{ev0, ev1, ev2, ev3};
-    uint64_t launches = 0;
+        use_levels_ = kbits_ <= c_;
+        cj_ = use_levels_ ? c_ : kbits_;
+        rjob_ = n_ - cj_;
+        per_ = use_levels_ ? ((chi_ - clo_) << (c_ - kbits_)) : (chi_ - clo_);
+        njobs_ = per_ * ninst_;
 
-    // ---- prefix depth: enough jobs to fill the GPU, job states <= kMaxJobModes modes
-    const uint64_t want_jobs = 16384;
-    int c = 0;
-    if (n >= Q0) {
-        int cw = 0;
-        while ((static_cast<uint64_t>(ninst) << cw) < want_jobs && cw < n - Q0) ++cw;
-        c = std::max(cw, n - kMaxJobModes);
-        c = std::min(c, n - Q0);
-    }
-    const bool use_levels = kbits <= c;
-    const int cj = use_levels ? c : kbits;  // depth at which jobs sit
-    const int rjob = n - cj;
-    const uint64_t per = use_levels ? ((chi - clo) << (c - kbits)) : (chi - clo);
-    const uint64_t njobs = per * ninst;
+        g_ = PrefixGeom{};
+        g_.n = n_;
+        g_.c = use_levels_ ? c_ : 0;
+        size_t o = tri_sz(2 * n_), to = 0;
+        for (int e = 1; e <= g_.c; ++e) {
+            g_.off[e] = o;
+            g_.toff[e] = to;
+            o += (static_cast<size_t>(1) << (e - 1)) * tri_sz(2 * (n_ - e));
+            to += static_cast<size_t>(1) << (e - 1);
+        }
+        g_.inst_entries = o;
+        g_.inst_ts = std::max<size_t>(to, 1);
 
-    // ---- geometry & device memory
-    PrefixGeom g{};
-    g.n = n;
-    g.c = use_levels ? c : 0;
-    size_t o = 0, to = 0;
-    g.off[0] = 0;
-    g.toff[0] = 0;
-    o = tri_sz(2 * n);
-    for (int e = 1; e <= g.c; ++e) {
-        g.off[e] = o;
-        g.toff[e] = to;
-        o += (static_cast<size_t>(1) << (e - 1)) * tri_sz(2 * (n - e));
-        to += static_cast<size_t>(1) << (e - 1);
-    }
-    g.inst_entries = o;
-    g.inst_ts = std::max<size_t>(to, 1);
-
-    DevBuf dpool, dtpool, djobs, dpart, derr, dctr, dscr, dwork;
-    CK(cudaMalloc(&dpool.p, sizeof(T) * g.inst_entries * ninst));
-    CK(cudaMalloc(&dtpool.p, sizeof(T) * g.inst_ts * ninst));
-    CK(cudaMalloc(&djobs.p, sizeof(Job<T>) * njobs));
-    CK(cudaMalloc(&dpart.p, sizeof(double) * 5 * njobs));
-    CK(cudaMalloc(&derr.p, sizeof(unsigned long long)));
-    CK(cudaMalloc(&dctr.p, sizeof(unsigned long long)));
-    T* pool = static_cast<T*>(dpool.p);
-    T* tpool = static_cast<T*>(dtpool.p);
-    Job<T>* jobs = static_cast<Job<T>*>(djobs.p);
-    double* parts = static_cast<double*>(dpart.p);
-    unsigned long long* derrp = static_cast<unsigned long long*>(derr.p);
-    unsigned long long* dctrp = static_cast<unsigned long long*>(dctr.p);
-
-    // upload R of every instance (host -> device, pinned staging is the caller's concern)
-    {
-        std::vector<T> host(static_cast<size_t>(tri_sz(2 * n)));
-        for (int i = 0; i < ninst; ++i) {
+        CK(cudaMalloc(&pool_.p, sizeof(T) * g_.inst_entries * ninst_));
+        CK(cudaMalloc(&tpool_.p, sizeof(T) * g_.inst_ts * ninst_));
+        CK(cudaMalloc(&jobs_.p, sizeof(Job<T>) * njobs_));
+        CK(cudaMalloc(&parts_.p, sizeof(double) * 5 * njobs_));
+        CK(cudaMalloc(&errw_.p, sizeof(unsigned long long)));
+        CK(cudaMalloc(&ctr_.p, sizeof(unsigned long long)));
+        if (!use_levels_) {
+            work_stride_ = 2 * static_cast<size_t>(tri_sz(2 * n_));
+            CK(cudaMalloc(&work_.p, sizeof(T) * work_stride_ * njobs_));
+        }
+        if (rjob_ >= Q0) {
+            using SM = WarpSmem<T>;
+            constexpr int WPB = Cfg<T>::WPB;
+            smem_ = SM::kTabBytes + SM::kWarpBytes * WPB;
+            CK(cudaFuncSetAttribute(subtree_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem_)));
+            int bps = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, subtree_kernel<T>, 32 * WPB, smem_));
+            if (bps < 1) {
+                err = "subtree kernel does not fit on an SM";
+                return -1;
+            }
+            blocks_ = std::min<uint64_t>(static_cast<uint64_t>(bps) * sm_count_, (njobs_ + WPB - 1) / WPB);
+            const int D = rjob_ - Q0;
+            size_t stride = 0;
+            for (int x = 1; x <= D; ++x) stride += tri_sz(2 * (rjob_ - x));
+            scr_stride_ = std::max<size_t>(stride, 1);
+            CK(cudaMalloc(&scr_.p, sizeof(T) * scr_stride_ * blocks_ * WPB));
+        }
+        // resident inputs: the exact R of every instance
+        std::vector<T> host(static_cast<size_t>(tri_sz(2 * n_)));
+        for (int i = 0; i < ninst_; ++i) {
             const auto& R = inputs[i].R;
             for (size_t k = 0; k < host.size(); ++k) {
                 double w[4] = {0, 0, 0, 0};
@@ -1008,129 +989,147 @@ int run_impl(int device, const std::vector<PreparedInput>& inputs, const WorkRan
                 else if constexpr (K == 2) host[k] = dd{w[0], w[1]};
                 else host[k] = qd{{w[0], w[1], w[2], w[3]}};
             }
-            CK(cudaMemcpyAsync(pool + i * g.inst_entries, host.data(), sizeof(T) * host.size(),
-                               cudaMemcpyHostToDevice, st));
-            CK(cudaStreamSynchronize(st));
+            CK(cudaMemcpyAsync(pool() + i * g_.inst_entries, host.data(), sizeof(T) * host.size(),
+                               cudaMemcpyHostToDevice, st_));
+            CK(cudaStreamSynchronize(st_));
         }
+        h2d_bytes_ = sizeof(T) * host.size() * ninst_;
+        return 0;
     }
-    lap("alloc+up");
-    const unsigned long long no_err = ~0ull;
-    CK(cudaMemcpyAsync(derrp, &no_err, sizeof(no_err), cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(dctrp, 0, sizeof(unsigned long long), st));
-    CK(cudaEventRecord(ev0, st));
 
-    // ---- prefix
-    if (use_levels) {
-        const int wpb = 4;
-        const size_t sm = sizeof(T) * 4 * n * wpb;
-        for (int e = 1; e <= g.c; ++e) {
-            const uint64_t items = (1ull << (e - 1)) * ninst;
-            const uint64_t blocks = std::min<uint64_t>((items + wpb - 1) / wpb, 65535ull * 4);
-            prefix_level_kernel<T><<<static_cast<unsigned>(blocks), 32 * wpb, sm, st>>>(g, pool, tpool, e, ninst,
-                                                                                          derrp);
+    ~PlanImpl() override {
+        for (auto& e : ev_)
+            if (e) cudaEventDestroy(e);
+        if (st_) cudaStreamDestroy(st_);
+    }
+
+    int execute(std::vector<EngineOut>& out, EngineStats* stats, std::string& err) override {
+        constexpr int Q0 = Cfg<T>::L + FAN;
+        CK(cudaSetDevice(device_));
+        uint64_t launches = 0;
+        unsigned long long* errw = static_cast<unsigned long long*>(errw_.p);
+        unsigned long long* ctr = static_cast<unsigned long long*>(ctr_.p);
+        double* parts = static_cast<double*>(parts_.p);
+        Job<T>* jobs = static_cast<Job<T>*>(jobs_.p);
+        CK(cudaMemsetAsync(errw, 0xff, sizeof(unsigned long long), st_));
+        CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st_));
+        CK(cudaEventRecord(ev_[0], st_));
+        if (use_levels_) {
+            const int wpb = 4;
+            const size_t sm = sizeof(T) * 4 * n_ * wpb;
+            for (int e = 1; e <= g_.c; ++e) {
+                const uint64_t items = (1ull << (e - 1)) * ninst_;
+                const uint64_t blocks = std::min<uint64_t>((items + wpb - 1) / wpb, 65535ull * 4);
+                prefix_level_kernel<T><<<static_cast<unsigned>(blocks), 32 * wpb, sm, st_>>>(g_, pool(), tpool(), e,
+                                                                                               ninst_, errw);
+                ++launches;
+            }
+            const uint64_t lo = clo_ << (c_ - kbits_), hi = chi_ << (c_ - kbits_);
+            const uint64_t blocks = std::min<uint64_t>((njobs_ + 255) / 256, 1ull << 20);
+            make_jobs_kernel<T><<<static_cast<unsigned>(blocks), 256, 0, st_>>>(g_, pool(), tpool(), ninst_, lo, hi,
+                                                                                jobs);
+            ++launches;
+        } else {
+            const int wpb = 4;
+            const size_t sm = sizeof(T) * (4 * n_ * wpb + wpb);
+            const uint64_t blocks = std::min<uint64_t>((njobs_ + wpb - 1) / wpb, 65535ull * 4);
+            direct_prefix_kernel<T><<<static_cast<unsigned>(blocks), 32 * wpb, sm, st_>>>(
+                n_, kbits_, pool(), ninst_, g_.inst_entries, clo_, chi_, static_cast<T*>(work_.p), work_stride_, jobs,
+                errw);
             ++launches;
         }
-        const uint64_t lo = clo << (c - kbits), hi = chi << (c - kbits);
-        const uint64_t blocks = std::min<uint64_t>((njobs + 255) / 256, 1ull << 20);
-        make_jobs_kernel<T><<<static_cast<unsigned>(blocks), 256, 0, st>>>(g, pool, tpool, ninst, lo, hi, jobs);
-        ++launches;
-    } else {
-        const size_t stride = 2 * static_cast<size_t>(tri_sz(2 * n));
-        CK(cudaMalloc(&dwork.p, sizeof(T) * stride * njobs));
-        const int wpb = 4;
-        const size_t sm = sizeof(T) * (4 * n * wpb + wpb);
-        const uint64_t blocks = std::min<uint64_t>((njobs + wpb - 1) / wpb, 65535ull * 4);
-        direct_prefix_kernel<T><<<static_cast<unsigned>(blocks), 32 * wpb, sm, st>>>(
-            n, kbits, pool, ninst, g.inst_entries, clo, chi, static_cast<T*>(dwork.p), stride, jobs, derrp);
-        ++launches;
-    }
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(ev1, st));
-
-    // ---- subtrees
-    if (rjob >= Q0) {
-        using SM = WarpSmem<T>;
-        constexpr int WPB = Cfg<T>::WPB;
-        const size_t smem = SM::kTabBytes + SM::kWarpBytes * WPB;
-        CK(cudaFuncSetAttribute(subtree_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)));
-        int bps = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, subtree_kernel<T>, 32 * WPB, smem));
-        if (bps < 1) {
-            err = "subtree kernel does not fit on an SM";
-            return -1;
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(ev_[1], st_));
+        if (rjob_ >= Q0) {
+            constexpr int WPB = Cfg<T>::WPB;
+            subtree_kernel<T><<<static_cast<unsigned>(blocks_), 32 * WPB, smem_, st_>>>(
+                jobs, njobs_, n_, rjob_, static_cast<T*>(scr_.p), scr_stride_, parts, errw, ctr);
+        } else {
+            const uint64_t blocks = (njobs_ + 127) / 128;
+            small_job_kernel<T, Q0 - 1><<<static_cast<unsigned>(blocks), 128, 0, st_>>>(jobs, njobs_, n_, rjob_,
+                                                                                        parts, errw);
         }
-        uint64_t blocks = static_cast<uint64_t>(bps) * sm_count;
-        blocks = std::min<uint64_t>(blocks, (njobs + WPB - 1) / WPB);
-        const int D = rjob - Q0;
-        size_t stride = 0;
-        for (int x = 1; x <= D; ++x) stride += tri_sz(2 * (rjob - x));
-        stride = std::max<size_t>(stride, 1);
-        CK(cudaMalloc(&dscr.p, sizeof(T) * stride * blocks * WPB));
-        subtree_kernel<T><<<static_cast<unsigned>(blocks), 32 * WPB, smem, st>>>(
-            jobs, njobs, n, rjob, static_cast<T*>(dscr.p), stride, parts, derrp, dctrp);
         ++launches;
-    } else {
-        const uint64_t blocks = (njobs + 127) / 128;
-        small_job_kernel<T, Q0 - 1><<<static_cast<unsigned>(blocks), 128, 0, st>>>(jobs, njobs, n, rjob, parts,
-                                                                                   derrp);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(ev_[2], st_));
+        fold_kernel<T><<<ninst_, 256, 0, st_>>>(parts, per_);
         ++launches;
-    }
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(ev2, st));
-
-    // ---- per-instance fixed-order fold
-    fold_kernel<T><<<ninst, 256, 0, st>>>(parts, per);
-    ++launches;
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(ev3, st));
-
-    std::vector<double> res(static_cast<size_t>(ninst) * 5);
-    for (int i = 0; i < ninst; ++i)
-        CK(cudaMemcpyAsync(&res[i * 5], parts + static_cast<size_t>(i) * per * 5, 5 * sizeof(double),
-                           cudaMemcpyDeviceToHost, st));
-    unsigned long long herr = 0;
-    CK(cudaMemcpyAsync(&herr, derrp, sizeof(herr), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    lap("device");
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(ev_[3], st_));
+        std::vector<double> res(static_cast<size_t>(ninst_) * 5);
+        for (int i = 0; i < ninst_; ++i)
+            CK(cudaMemcpyAsync(&res[i * 5], parts + static_cast<size_t>(i) * per_ * 5, 5 * sizeof(double),
+                               cudaMemcpyDeviceToHost, st_));
+        unsigned long long herr = 0;
+        CK(cudaMemcpyAsync(&herr, errw, sizeof(herr), cudaMemcpyDeviceToHost, st_));
+        CK(cudaStreamSynchronize(st_));
 #ifdef TOR_PHASE_TIMING
-    {
-        unsigned long long pc[32];
-        cudaMemcpyFromSymbol(pc, g_phase_cycles, sizeof(pc));
-        const char* names[20] = {"dfs_elim", "root_copy", "-", "-", "lane_tree",
-                                 "L1 piv", "L1 vec", "L1 ent", "L2 piv", "L2 vec", "L2 ent", "L3 piv", "L3 vec", "L3 ent",
-                                 "L4 piv", "L4 vec", "L4 ent", "L5 piv", "L5 vec", "L5 ent"};
-        double tot = 0;
-        for (int i = 0; i < 20; ++i) tot += pc[i];
-        for (int i = 0; i < 20; ++i)
-            if (pc[i]) std::fprintf(stderr, "[phase] %-10s %6.2f%%  %.3e warp-cycles\n", names[i], 100.0 * pc[i] / tot, (double)pc[i]);
-        unsigned long long z[32] = {0};
-        cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
-    }
-#endif
-
-    out.assign(ninst, EngineOut{});
-    const uint64_t terms = (chi - clo) << (n - kbits);
-    for (int i = 0; i < ninst; ++i) {
-        for (int x = 0; x < 4; ++x) out[i].words[x] = res[i * 5 + x];
-        out[i].sum_abs = res[i * 5 + 4];
-        out[i].terms = terms;
-        if (herr != ~0ull) {
-            out[i].breakdown = true;
-            out[i].bad_mask = herr >> 8;
-            out[i].bad_row = static_cast<int>(herr & 0xff);
+        {
+            unsigned long long pc[32];
+            cudaMemcpyFromSymbol(pc, g_phase_cycles, sizeof(pc));
+            const char* names[20] = {"dfs_elim", "root_copy", "-", "-", "lane_tree", "L1 piv", "L1 vec",
+                                     "L1 ent", "L2 piv", "L2 vec", "L2 ent", "L3 piv", "L3 vec", "L3 ent",
+                                     "L4 piv", "L4 vec", "L4 ent", "L5 piv", "L5 vec", "L5 ent"};
+            double tot = 0;
+            for (int i = 0; i < 20; ++i) tot += pc[i];
+            for (int i = 0; i < 20; ++i)
+                if (pc[i])
+                    std::fprintf(stderr, "[phase] %-10s %6.2f%%  %.3e warp-cycles\n", names[i], 100.0 * pc[i] / tot,
+                                 (double)pc[i]);
+            unsigned long long z[32] = {0};
+            cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
         }
+#endif
+        out.assign(ninst_, EngineOut{});
+        const uint64_t terms = (chi_ - clo_) << (n_ - kbits_);
+        for (int i = 0; i < ninst_; ++i) {
+            for (int x = 0; x < 4; ++x) out[i].words[x] = res[i * 5 + x];
+            out[i].sum_abs = res[i * 5 + 4];
+            out[i].terms = terms;
+            if (herr != ~0ull) {
+                out[i].breakdown = true;
+                out[i].bad_mask = herr >> 8;
+                out[i].bad_row = static_cast<int>(herr & 0xff);
+            }
+        }
+        if (stats) {
+            float a = 0, b = 0;
+            cudaEventElapsedTime(&a, ev_[1], ev_[2]);
+            cudaEventElapsedTime(&b, ev_[0], ev_[3]);
+            stats->kernel_ms = a;
+            stats->total_ms = b;
+            stats->launches = launches;
+            stats->prefix_depth = cj_;
+            stats->jobs = njobs_;
+            stats->h2d_bytes = h2d_bytes_;
+            stats->d2h_bytes = res.size() * sizeof(double) + sizeof(herr);
+        }
+        return 0;
     }
-    if (stats) {
-        float a = 0, b = 0;
-        cudaEventElapsedTime(&a, ev1, ev2);
-        cudaEventElapsedTime(&b, ev0, ev3);
-        stats->kernel_ms = a;
-        stats->total_ms = b;
-        stats->launches = launches;
-        stats->prefix_depth = cj;
-        stats->jobs = njobs;
+
+  private:
+    T* pool() { return static_cast<T*>(pool_.p); }
+    T* tpool() { return static_cast<T*>(tpool_.p); }
+    int device_ = 0, ninst_ = 0, n_ = 0, kbits_ = 0, sm_count_ = 0, c_ = 0, cj_ = 0, rjob_ = 0;
+    uint64_t clo_ = 0, chi_ = 1, per_ = 0, njobs_ = 0, blocks_ = 0;
+    bool use_levels_ = true;
+    PrefixGeom g_{};
+    size_t smem_ = 0, scr_stride_ = 1, work_stride_ = 0, h2d_bytes_ = 0;
+    cudaStream_t st_ = nullptr;
+    cudaEvent_t ev_[4] = {nullptr, nullptr, nullptr, nullptr};
+    DevBuf pool_, tpool_, jobs_, parts_, errw_, ctr_, scr_, work_;
+};
+
+template <class T>
+int make_plan(int device, const std::vector<PreparedInput>& inputs, const WorkRange& range, Plan** out,
+              std::string& err) {
+    auto* p = new PlanImpl<T>();
+    const int st = p->init(device, inputs, range, err);
+    if (st != 0) {
+        delete p;
+        return st;
     }
+    *out = p;
     return 0;
 }
 
@@ -1140,23 +1139,38 @@ int engine_tree_min_n(int mode) {
     return mode == MODE_QD ? Cfg<qd>::L + FAN : Cfg<dd>::L + FAN;
 }
 
+int plan_create(int device, int mode, const std::vector<PreparedInput>& inputs, const WorkRange& range, Plan** out,
+                std::string& err) {
+    *out = nullptr;
+    if (inputs.empty()) {
+        err = "no inputs";
+        return -1;
+    }
+    switch (mode) {
+        case MODE_FP64:
+            return make_plan<double>(device, inputs, range, out, err);
+        case MODE_DD:
+            return make_plan<dd>(device, inputs, range, out, err);
+        case MODE_QD:
+            return make_plan<qd>(device, inputs, range, out, err);
+        default:
+            err = "bad mode";
+            return -1;
+    }
+}
+
 int engine_run(int device, int mode, const std::vector<PreparedInput>& inputs, const WorkRange& range,
                std::vector<EngineOut>& out, EngineStats* stats, std::string& err) {
     if (inputs.empty()) {
         out.clear();
         return 0;
     }
-    switch (mode) {
-        case MODE_FP64:
-            return run_impl<double>(device, inputs, range, out, stats, err);
-        case MODE_DD:
-            return run_impl<dd>(device, inputs, range, out, stats, err);
-        case MODE_QD:
-            return run_impl<qd>(device, inputs, range, out, stats, err);
-        default:
-            err = "bad mode";
-            return -1;
-    }
+    Plan* p = nullptr;
+    const int st = plan_create(device, mode, inputs, range, &p, err);
+    if (st != 0) return st;
+    const int rs = p->execute(out, stats, err);
+    delete p;
+    return rs;
 }
 
 void fold_words(int mode, const double* parts, int count, double* out5) {

@@ -51,7 +51,19 @@ struct EngineStats {
     uint64_t launches = 0;        // kernels launched
     int prefix_depth = 0;
     uint64_t jobs = 0;
+    uint64_t h2d_bytes = 0;       // inputs uploaded when the plan was created
+    uint64_t d2h_bytes = 0;       // results read back per execute()
 };
+
+// Prepared evaluation with device-resident inputs (see PlanImpl in engine.cu).
+class Plan {
+  public:
+    virtual ~Plan() = default;
+    virtual int execute(std::vector<EngineOut>& out, EngineStats* stats, std::string& err) = 0;
+};
+
+int plan_create(int device, int mode, const std::vector<PreparedInput>& inputs, const WorkRange& range, Plan** out,
+                std::string& err);
 
 // Runs the engine on `device` for all instances (same n) over `range`.
 // Returns 0 or a CUDA error code; errors are described in `err`.
