@@ -44,10 +44,35 @@ __host__ __device__ __forceinline__ int tri_ix(int d, int i, int j) {
 
 // Lane-level register depth per word type (register budget: the L-mode state is
 // read from shared memory, states of < L modes live in registers).
+// TMEM: the lane states of the last fan-out level are handed to their lanes through
+// tensor memory (each lane's own TMEM row) instead of shared-memory buffers; needs
+// 4-warp CTAs (one warp per TMEM lane quadrant).
+#ifndef TOR_DD_TMEM
+#define TOR_DD_TMEM 1
+#endif
 template <class T> struct Cfg;
-template <> struct Cfg<double> { static constexpr int L = 4; static constexpr int WPB = 4; };
-template <> struct Cfg<dd> { static constexpr int L = 4; static constexpr int WPB = 2; };
-template <> struct Cfg<qd> { static constexpr int L = 3; static constexpr int WPB = 1; };
+template <> struct Cfg<double> {
+    static constexpr int L = 4;
+    static constexpr int WPB = 4;
+    static constexpr int MINB = 1;
+    static constexpr bool TMEM = false;
+};
+template <> struct Cfg<dd> {
+    static constexpr int L = 4;
+#ifdef TOR_DD_WPB
+    static constexpr int WPB = TOR_DD_WPB;
+#else
+    static constexpr int WPB = TOR_DD_TMEM ? 4 : 2;
+#endif
+    static constexpr int MINB = TOR_DD_TMEM ? 2 : 1;
+    static constexpr bool TMEM = TOR_DD_TMEM;
+};
+template <> struct Cfg<qd> {
+    static constexpr int L = 3;
+    static constexpr int WPB = 1;
+    static constexpr int MINB = 1;
+    static constexpr bool TMEM = false;
+};
 
 template <class T> constexpr int root_modes() { return Cfg<T>::L + FAN; }
 
@@ -216,6 +241,91 @@ __device__ void warp_elim(const T* S, int d, int sr, int q, T* dst, const T& t_i
             const int k = kb + lane + 32 * u;
             if (k < total) dst[k] = v;
         }
+    }
+    __syncwarp();
+}
+
+// DFS step of the subtree kernel: eliminates the first mode of the q-mode source
+// view (HBM/L2 resident) and writes (a) the new (q-1)-mode state to its DFS slot
+// (only when later leaves read it) and (b) its trailing Q0 modes straight into the
+// shared-memory root of the leaf that follows (no separate root copy).  All global
+// loads of the common sizes (q <= 11) are issued up front: one L2 round trip.
+template <class T, int Q0>
+__device__ void dfs_elim(const T* S, int d, int sr, int q, T* slot, bool write_slot, T* root, const T& t_in,
+                         T* t_out, T* uw, uint64_t mask, int nsel, unsigned long long* err) {
+    using A = Arith<T>;
+    constexpr int NB = 8;  // entries per lane per batch
+    const int lane = threadIdx.x & 31;
+    const int m = 2 * q;
+    const int dn = m - 2;
+    const int total = tri_sz(dn);
+    const int so = dn - 2 * Q0;  // rows of the new state before the root block
+    // ---- issue loads: pivot block, this lane's pivot-row entries, first entry batch
+    const T p00 = S[tri_ix(d, sr, sr)], p01 = S[tri_ix(d, sr, sr + 1)], p11 = S[tri_ix(d, sr + 1, sr + 1)];
+    T v0[2], v1[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int j = 2 + lane + 32 * r;
+        const int jc = j < m ? j : m - 1;
+        v0[r] = S[tri_ix(d, sr, sr + jc)];
+        v1[r] = S[tri_ix(d, sr + 1, sr + jc)];
+    }
+    int i = 0, k0 = lane;
+    while (i < dn && k0 >= dn - i) {
+        k0 -= dn - i;
+        ++i;
+    }
+    int j = i + k0;
+    int ii[NB], jj[NB];
+    T sv[NB];
+    auto load_batch = [&](int kb) {
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const bool ok = kb + lane + 32 * u < total;
+            ii[u] = ok ? i : 0;
+            jj[u] = ok ? j : 0;
+            sv[u] = S[tri_ix(d, sr + 2 + ii[u], sr + 2 + jj[u])];
+            j += 32;
+            while (i < dn && j >= dn) {
+                j -= dn - (i + 1);
+                ++i;
+            }
+        }
+    };
+    load_batch(0);
+    // ---- pivots (all lanes, warp-uniform) and pivot-row vectors
+    const Piv<T> pv = pivot2<T>(p00, p01, p11, t_in);
+    if (lane == 0) {
+        if (pv.bad0 || pv.bad1) report_breakdown(err, mask, 2 * nsel + (pv.bad0 ? 0 : 1));
+        *t_out = pv.tn;
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int jv = 2 + lane + 32 * r;
+        if (jv < m) {
+            const T uj = A::mul(v0[r], pv.r1);
+            uw[jv] = uj;
+            uw[m + jv] = A::mul(A::rank1(v1[r], pv.u1, uj), pv.r2);
+        }
+    }
+    __syncwarp();
+    // ---- trailing update, batch by batch
+    for (int kb = 0;;) {
+        T out[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) out[u] = A::rank2(sv[u], uw[2 + ii[u]], uw[2 + jj[u]], uw[m + 2 + ii[u]], uw[m + 2 + jj[u]]);
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const int k = kb + lane + 32 * u;
+            if (k < total) {
+                if (write_slot) slot[k] = out[u];
+                const int ri = ii[u] - so, rj = jj[u] - so;
+                if (ri >= 0) root[tri_ix(2 * Q0, ri, rj)] = out[u];
+            }
+        }
+        kb += 32 * NB;
+        if (kb >= total) break;
+        load_batch(kb);
     }
     __syncwarp();
 }
@@ -473,6 +583,139 @@ __device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t,
     }
 }
 
+// ------------------------------------------------------------------ TMEM ----
+// Tensor memory as per-lane private storage: a warp w of a 4-warp CTA owns TMEM lanes
+// 32(w%4)..+31; lane l's row holds its level-FAN state, entry k at columns 4k..4k+3.
+__device__ __forceinline__ void tm_st4(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(taddr), "r"(a), "r"(b),
+                 "r"(c), "r"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void tm_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16};\n" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tm_ld4(uint32_t taddr, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "r"(taddr)
+                 : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+__device__ __forceinline__ void dd_to_u32(const dd& v, uint32_t* r) {
+    r[0] = static_cast<uint32_t>(__double2loint(v.hi));
+    r[1] = static_cast<uint32_t>(__double2hiint(v.hi));
+    r[2] = static_cast<uint32_t>(__double2loint(v.lo));
+    r[3] = static_cast<uint32_t>(__double2hiint(v.lo));
+}
+__device__ __forceinline__ dd u32_to_dd(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    return dd{__hiloint2double(static_cast<int>(b), static_cast<int>(a)),
+              __hiloint2double(static_cast<int>(d), static_cast<int>(c))};
+}
+// Loads entries [k0, k0+N) of this lane's TMEM state (issue only; tm_wait_ld before use).
+template <int N>
+__device__ __forceinline__ void tm_ld_entries(uint32_t row, int k0, uint32_t (&r)[4 * N]) {
+#pragma unroll
+    for (int u = 0; u < N; ++u) tm_ld4(row + 4 * (k0 + u), r[4 * u], r[4 * u + 1], r[4 * u + 2], r[4 * u + 3]);
+}
+
+// (row, col) of flat index k in a packed D-row upper triangle (compile-time)
+__host__ __device__ constexpr int tri_row(int D, int k) {
+    int i = 0;
+    while (k >= D - i) {
+        k -= D - i;
+        ++i;
+    }
+    return i;
+}
+__host__ __device__ constexpr int tri_col(int D, int k) {
+    int i = 0;
+    while (k >= D - i) {
+        k -= D - i;
+        ++i;
+    }
+    return i + k;
+}
+// Rank-2 update of trailing entries [KB, KB+CNT) whose sources are in TMEM; the (i,j)
+// of every entry is a template constant so u/w/Sn stay in registers.
+template <class T, int M, int K, int END> struct LtUpd {
+    __device__ __forceinline__ static void run(const uint32_t* rt, const T (&u)[M], const T (&w)[M],
+                                               St<T, M / 2 - 1>& Sn) {
+        if constexpr (K < END) {
+            constexpr int D = M - 2;
+            constexpr int i = tri_row(D, K), j = tri_col(D, K);
+            Sn.e[K] = Arith<T>::rank2(u32_to_dd(rt[0], rt[1], rt[2], rt[3]), u[2 + i], u[2 + j], w[2 + i], w[2 + j]);
+            LtUpd<T, M, K + 1, END>::run(rt + 4, u, w, Sn);
+        }
+    }
+};
+template <class T, int M, int KB, int CNT>
+__device__ __forceinline__ void lt_wave(uint32_t base, const T (&u)[M], const T (&w)[M], St<T, M / 2 - 1>& Sn) {
+    uint32_t rt[4 * CNT];
+#pragma unroll
+    for (int q = 0; q < CNT; ++q) tm_ld4(base + 4 * (KB + q), rt[4 * q], rt[4 * q + 1], rt[4 * q + 2], rt[4 * q + 3]);
+    tm_wait_ld();
+    LtUpd<T, M, KB, KB + CNT>::run(rt, u, w, Sn);
+}
+
+// Lane subtree whose L-mode root state sits in this lane's TMEM row (entry k of the
+// packed 2L-row triangle at columns 4k..4k+3, DD words).  Same arithmetic as
+// lane_tree; only the source of the root entries differs.
+template <class T, int L>
+__device__ __forceinline__ void lane_tree_tmem(uint32_t row, const T& t, bool neg, uint64_t mask, int nsel,
+                                               Acc<T>& acc, unsigned long long* err) {
+    using A = Arith<T>;
+    constexpr int M = 2 * L;
+    constexpr int K01 = 2 * M - 1;  // entries of rows 0 and 1
+    acc.add(t, neg);
+    const uint64_t bit = 1ull << (L - 1);
+#pragma unroll 1
+    for (int br = 0; br < 2; ++br) {
+        St<T, L - 1> Sn;
+        T tn;
+        if (br == 0) {
+            uint32_t r0[4 * K01];
+            tm_ld_entries<K01>(row, 0, r0);
+            tm_wait_ld();
+            T e0[K01];
+#pragma unroll
+            for (int k = 0; k < K01; ++k) e0[k] = u32_to_dd(r0[4 * k], r0[4 * k + 1], r0[4 * k + 2], r0[4 * k + 3]);
+            // row 0: k = j (j = 0..M-1); row 1: k = M + (j - 1) (j = 1..M-1)
+            const Piv<T> pv = pivot2<T>(e0[0], e0[1], e0[M], t);
+            if (pv.bad0 || pv.bad1) report_breakdown(err, mask | bit, 2 * nsel + (pv.bad0 ? 0 : 1));
+            tn = pv.tn;
+            T u[M], w[M];
+#pragma unroll
+            for (int j = 2; j < M; ++j) {
+                u[j] = A::mul(e0[j], pv.r1);
+                w[j] = A::mul(A::rank1(e0[M + j - 1], pv.u1, u[j]), pv.r2);
+            }
+            // trailing block in two waves to bound live registers
+            constexpr int NT = tri_sz(M - 2);
+            constexpr int H = NT / 2;
+            lt_wave<T, M, 0, H>(row + 4 * K01, u, w, Sn);
+            lt_wave<T, M, H, NT - H>(row + 4 * K01, u, w, Sn);
+            acc.add(tn, !neg);
+        } else {
+            constexpr int NT = tri_sz(M - 2);
+            uint32_t rt[4 * NT];
+            tm_ld_entries<NT>(row, K01, rt);
+            tm_wait_ld();
+#pragma unroll
+            for (int kk = 0; kk < NT; ++kk) Sn.e[kk] = u32_to_dd(rt[4 * kk], rt[4 * kk + 1], rt[4 * kk + 2], rt[4 * kk + 3]);
+            tn = t;
+        }
+        SubReg<T, L - 1>::run(Sn, tn, br == 0 ? !neg : neg, br == 0 ? (mask | bit) : mask, nsel + (br == 0), acc,
+                              err);
+    }
+}
+
 // --------------------------------------------------------- subtree kernel ----
 // Per-warp shared memory: the Q0-mode root (copy of the DFS leaf view), the
 // include buffers of the 5 fan-out levels, their t values, pivots, pivot-row
@@ -486,7 +729,8 @@ template <class T> struct WarpSmem {
         for (int x = 1; x < e; ++x) o += (1 << (x - 1)) * tri_sz(2 * (Q0 - x));
         return e == 0 ? 0 : o;
     }
-    static constexpr int kBufEntries = lvl_off(FAN + 1);
+    // with TMEM the last level's include states never touch shared memory
+    static constexpr int kBufEntries = Cfg<T>::TMEM ? lvl_off(FAN) : lvl_off(FAN + 1);
     static constexpr int kTOff = kBufEntries;   // t of level buffers at 2^(e-1)-1+p, root t at 31
     static constexpr int kPivOff = kTOff + 32;  // r1 / u1 / r2 of up to 16 eliminations
     __host__ __device__ static constexpr int uw_need() {
@@ -547,7 +791,8 @@ template <class T, int E_LVL> struct FanLevel {
     static constexpr int dn = m - 2;
     static constexpr int tn = tri_sz(dn);
     __device__ __forceinline__ static void run(T* sm, T* tvals, T* piv, T* uwv, int* desc, const uint16_t* tabs,
-                                               uint64_t leaf_mask, int leaf_sel, unsigned long long* err) {
+                                               uint64_t leaf_mask, int leaf_sel, unsigned long long* err,
+                                               uint32_t tm_row) {
         using A = Arith<T>;
         const int lane = threadIdx.x & 31;
         PHASE_T0();
@@ -609,6 +854,60 @@ template <class T, int E_LVL> struct FanLevel {
         }
         __syncwarp();
         PHASE_MARK(6 + 3 * (E_LVL - 1));
+        if constexpr (Cfg<T>::TMEM && E_LVL == FAN) {
+            // last level -> TMEM: lane 2x+1 owns include child x, lane 2x the exclude child.
+            // The pair splits the include child's tn entries (2 each per chunk of 4); the
+            // even lane's results cross over by shuffle; every lane then stores its own
+            // node's chunk into its TMEM row.  The even lane's exclude state is the
+            // parent's trailing block, i.e. exactly the rank-2 inputs.
+            static_assert(tn % 4 == 0, "chunking");
+            const int x = lane >> 1, h = lane & 1;
+            const T* pb = sm + desc[4 * x];
+            const int pd = desc[4 * x + 1], sr = desc[4 * x + 2];
+            const T* uw = uwv + x * 2 * m;
+            const uint16_t* tab = tabs + WarpSmem<T>::tab_off(E_LVL);
+            constexpr int NC = tn / 4;  // chunks of 4 entries (16 TMEM columns)
+            constexpr int CB = 3;       // chunks per batch (loads of a batch issued together)
+#pragma unroll 1
+            for (int c0 = 0; c0 < NC; c0 += CB) {
+                T sv[CB][2], vv[CB][2];
+#pragma unroll
+                for (int cc = 0; cc < CB; ++cc)
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int c = c0 + cc < NC ? c0 + cc : NC - 1;
+                        const int ij = tab[4 * c + 2 * h + u];
+                        const int i = ij >> 8, j = ij & 0xff;
+                        sv[cc][u] = pb[tri_ix(pd, sr + 2 + i, sr + 2 + j)];
+                        vv[cc][u] = A::rank2(sv[cc][u], uw[2 + i], uw[2 + j], uw[m + 2 + i], uw[m + 2 + j]);
+                    }
+#pragma unroll
+                for (int cc = 0; cc < CB; ++cc) {
+                    if (c0 + cc < NC) {
+                        T pv[2], ps[2];
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            pv[u] = shfl_xor_t(vv[cc][u], 1);
+                            ps[u] = shfl_xor_t(sv[cc][u], 1);
+                        }
+                        uint32_t r[16];
+                        if constexpr (sizeof(T) == sizeof(dd)) {
+                            // even lane: its exclude state's entries 4c..4c+3 (own inputs + partner's)
+                            // odd lane: its include state's entries (partner's results + own)
+                            dd_to_u32(h ? pv[0] : sv[cc][0], r + 0);
+                            dd_to_u32(h ? pv[1] : sv[cc][1], r + 4);
+                            dd_to_u32(h ? vv[cc][0] : ps[0], r + 8);
+                            dd_to_u32(h ? vv[cc][1] : ps[1], r + 12);
+                        }
+                        tm_st16(tm_row + 16 * (c0 + cc), r);
+                    }
+                }
+            }
+            tm_wait_st();
+            __syncwarp();
+            PHASE_MARK(7 + 3 * (E_LVL - 1));
+            return;
+        }
         // trailing updates into the level-e buffers
         T* lvl = sm + WarpSmem<T>::lvl_off(E_LVL);
         const uint16_t* tab = tabs + WarpSmem<T>::tab_off(E_LVL);
@@ -651,7 +950,7 @@ template <class T, int E_LVL> struct FanLevel {
 
 
 template <class T>
-__global__ void __launch_bounds__(32 * Cfg<T>::WPB)
+__global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
     subtree_kernel(const Job<T>* jobs, uint64_t njobs, int nmodes, int rjob, T* scratch, size_t scratch_stride,
                    double* partials, unsigned long long* err, unsigned long long* job_counter) {
     using SM = WarpSmem<T>;
@@ -672,7 +971,23 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB)
             tabs[SM::tab_off(e) + k] = static_cast<uint16_t>((i << 8) | (i + r));
         }
     }
-    __syncthreads();
+    __shared__ uint32_t tmem_base;
+    uint32_t tm_row = 0;
+    if constexpr (Cfg<T>::TMEM) {
+        static_assert(Cfg<T>::WPB == 4, "TMEM lane handoff needs one warp per TMEM lane quadrant");
+        if ((threadIdx.x >> 5) == 0) {
+            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base));
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(dst), "r"(256)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        tm_row = tmem_base + (static_cast<uint32_t>(32 * ((threadIdx.x >> 5) & 3)) << 16);
+    } else {
+        __syncthreads();
+    }
     const int wib = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     unsigned char* wbase = smem_raw + SM::kTabBytes + wib * SM::kWarpBytes;
@@ -723,30 +1038,20 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB)
                 for (int x = 1; x < kd + 1; ++x) doff += tri_sz(2 * (rjob - x));
                 const uint64_t lmask = J.mask | ((above << 1 | 1ull) << (rjob - kd - 1));
                 const int lsel = J.nsel + __popcll(above);
-                warp_elim<T>(src, sd, 2 * ssk, rjob - kd, slots + doff, st, dfs_t + kd + 1, uwv, lmask, lsel, err);
+                // the new slot kd+1 is re-read by later leaves only when b >= 1; its
+                // trailing Q0 modes are this leaf's root either way
+                dfs_elim<T, Q0>(src, sd, 2 * ssk, rjob - kd, slots + doff, b >= 1, sm, st, dfs_t + kd + 1, uwv,
+                                lmask, lsel, err);
+                if (lane == 0) tvals[31] = dfs_t[kd + 1];
+                __syncwarp();
             }
             PHASE_MARK(0);
-            // leaf view (depth D of the job) -> copy the Q0-mode root into shared memory
-            const T* lb;
-            int ld, lsk;
-            T lt;
             if (leaf == 0) {
-                lb = J.base;
-                ld = J.dim;
-                lsk = J.skip + D;
-                lt = J.t;
-            } else {
-                const int tz = __ffsll(static_cast<long long>(leaf)) - 1;
-                const int s = D - tz;
-                size_t off = 0;
-                for (int x = 1; x < s; ++x) off += tri_sz(2 * (rjob - x));
-                lb = slots + off;
-                ld = 2 * (rjob - s);
-                lsk = tz;
-                lt = dfs_t[s];
-            }
-            __syncwarp();
-            {
+                // first leaf: the root is the job state's trailing Q0 modes (HBM)
+                const T* lb = J.base;
+                const int ld = J.dim;
+                const int lsk = J.skip + D;
+                const T lt = J.t;
                 constexpr int RT = tri_sz(2 * Q0);
                 constexpr int RI = (RT + 31) / 32;
                 const int sr = 2 * lsk;
@@ -767,11 +1072,11 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB)
             const int leaf_sel = J.nsel + __popcll(leaf);
 
             PHASE_MARK(1);
-            FanLevel<T, 1>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err);
-            FanLevel<T, 2>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err);
-            FanLevel<T, 3>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err);
-            FanLevel<T, 4>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err);
-            FanLevel<T, 5>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err);
+            FanLevel<T, 1>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err, tm_row);
+            FanLevel<T, 2>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err, tm_row);
+            FanLevel<T, 3>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err, tm_row);
+            FanLevel<T, 4>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err, tm_row);
+            FanLevel<T, 5>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err, tm_row);
 
             // lanes: node (FAN, lane)
             {
@@ -782,7 +1087,8 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB)
                 const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(lane) << L);
                 const int lsel = leaf_sel + __popc(lane);
                 const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
-                lane_tree<T, L>(vb, vd, 2 * vsk, vt, nodeneg, lmask, lsel, acc, err);
+                if constexpr (Cfg<T>::TMEM) lane_tree_tmem<T, L>(tm_row, vt, nodeneg, lmask, lsel, acc, err);
+                else lane_tree<T, L>(vb, vd, 2 * vsk, vt, nodeneg, lmask, lsel, acc, err);
                 acc.flush();
             }
             __syncwarp();
@@ -800,6 +1106,13 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB)
             o[4] = acc.abs_sum;
         }
         __syncwarp();
+    }
+    if constexpr (Cfg<T>::TMEM) {
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncthreads();
+        if ((threadIdx.x >> 5) == 0)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(256)
+                         : "memory");
     }
 }
 
@@ -965,11 +1278,32 @@ class PlanImpl final : public Plan {
             smem_ = SM::kTabBytes + SM::kWarpBytes * WPB;
             CK(cudaFuncSetAttribute(subtree_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem_)));
+            CK(cudaFuncSetAttribute(subtree_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
             int bps = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, subtree_kernel<T>, 32 * WPB, smem_));
             if (bps < 1) {
                 err = "subtree kernel does not fit on an SM";
                 return -1;
+            }
+            // The occupancy API reports 1 CTA/SM for kernels that allocate TMEM; two 4-warp
+            // CTAs (256 TMEM columns each = the SM's 512) fit by registers and shared memory
+            // and do run concurrently (measured: 264 -> 173 ms at n=32 DD).
+            if (Cfg<T>::TMEM && 2 * (smem_ + 1024) <= 233472) bps = std::max(bps, 2);
+            if (const char* ov = std::getenv("TOR_BLOCKS_PER_SM")) bps = std::max(1, std::atoi(ov));
+            if (std::getenv("TOR_DEBUG_TIMING")) {
+                cudaFuncAttributes fa;
+                cudaFuncGetAttributes(&fa, subtree_kernel<T>);
+                std::fprintf(stderr, "[tor] subtree_kernel: %d blocks/SM x %d warps, smem %zu B/block, %d regs, "
+                                     "local %zu B, static smem %zu\n",
+                             bps, WPB, smem_, fa.numRegs, fa.localSizeBytes, fa.sharedSizeBytes);
+                for (size_t s2 : {size_t(0), size_t(50000), size_t(100000), size_t(110000), smem_}) {
+                    int b2 = 0;
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, subtree_kernel<T>, 32 * WPB, s2);
+                    size_t avail = 0;
+                    cudaOccupancyAvailableDynamicSMemPerBlock(&avail, subtree_kernel<T>, 2, 32 * WPB);
+                    std::fprintf(stderr, "[tor]   smem %zu -> %d blocks/SM (avail dyn smem @2 blocks: %zu)\n", s2, b2,
+                                 avail);
+                }
             }
             blocks_ = std::min<uint64_t>(static_cast<uint64_t>(bps) * sm_count_, (njobs_ + WPB - 1) / WPB);
             const int D = rjob_ - Q0;
