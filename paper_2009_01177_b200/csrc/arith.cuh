@@ -19,8 +19,16 @@
 
 #if defined(__CUDACC__)
 #define TOR_HD __host__ __device__ __forceinline__
+// large QD routines: inline by default (measured faster than out-of-line calls even
+// though the QD kernel's SASS is ~60K instructions); -DTOR_QD_NOINLINE for experiments
+#ifdef TOR_QD_NOINLINE
+#define TOR_HD_NI __host__ __device__ __noinline__
+#else
+#define TOR_HD_NI TOR_HD
+#endif
 #else
 #define TOR_HD inline
+#define TOR_HD_NI inline
 #endif
 
 namespace tor {
@@ -202,7 +210,7 @@ TOR_HD void three_sum2(double& a, double& b, double c) {
 }
 
 // Accurate-enough QD addition ("sloppy" add: pairwise TwoSums then renormalise).
-TOR_HD qd qd_add(const qd& a, const qd& b) {
+TOR_HD_NI qd qd_add(qd a, qd b) {
     double s0, s1, s2, s3, t0, t1, t2, t3;
     two_sum(a.x[0], b.x[0], s0, t0);
     two_sum(a.x[1], b.x[1], s1, t1);
@@ -217,7 +225,7 @@ TOR_HD qd qd_add(const qd& a, const qd& b) {
 TOR_HD qd qd_sub(const qd& a, const qd& b) { return qd_add(a, qd_neg(b)); }
 
 // QD product (sloppy: terms of order >= 4 in the component index dropped).
-TOR_HD qd qd_mul(const qd& a, const qd& b) {
+TOR_HD_NI qd qd_mul(qd a, qd b) {
     double p0, p1, p2, p3, p4, p5, q0, q1, q2, q3, q4, q5;
     double t0, t1, s0, s1, s2;
     two_prod(a.x[0], b.x[0], p0, q0);
@@ -265,7 +273,7 @@ TOR_HD qd qd_rank2(const qd& s, const qd& a, const qd& b, const qd& c, const qd&
 TOR_HD qd qd_rank1(const qd& s, const qd& a, const qd& b) { return qd_sub(s, qd_mul(a, b)); }
 
 // 1/sqrt(x), x > 0: DD seed then one QD Newton step y + y(1 - x y^2)/2.
-TOR_HD qd qd_rsqrt(const qd& x) {
+TOR_HD_NI qd qd_rsqrt(qd x) {
     const dd ys = dd_rsqrt(dd_norm(dd{x.x[0], x.x[1]}));
     const qd y = qd{{ys.hi, ys.lo, 0.0, 0.0}};
     const qd y2 = qd_mul(y, y);

@@ -173,19 +173,6 @@ __device__ __forceinline__ Piv<T> pivot2(const T& s00, const T& s01, const T& s1
     return p;
 }
 
-#ifdef TOR_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[32];
-#define PHASE_T0() long long _pt = clock64()
-#define PHASE_MARK(k)                                                                \
-    do {                                                                             \
-        const long long _pn = clock64();                                             \
-        if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[k], (unsigned long long)(_pn - _pt)); \
-        _pt = _pn;                                                                   \
-    } while (0)
-#else
-#define PHASE_T0()
-#define PHASE_MARK(k)
-#endif
 
 // ------------------------------------------------ warp-cooperative elimination --
 // Eliminates the first mode (rows 0,1) of the q-mode view (S, d, sr) into the
@@ -245,6 +232,20 @@ __device__ void warp_elim(const T* S, int d, int sr, int q, T* dst, const T& t_i
     __syncwarp();
 }
 
+#ifdef TOR_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[32];
+#define PHASE_T0() long long _pt = clock64()
+#define PHASE_MARK(k)                                                                \
+    do {                                                                             \
+        const long long _pn = clock64();                                             \
+        if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[k], (unsigned long long)(_pn - _pt)); \
+        _pt = _pn;                                                                   \
+    } while (0)
+#else
+#define PHASE_T0()
+#define PHASE_MARK(k)
+#endif
+
 // DFS step of the subtree kernel: eliminates the first mode of the q-mode source
 // view (HBM/L2 resident) and writes (a) the new (q-1)-mode state to its DFS slot
 // (only when later leaves read it) and (b) its trailing Q0 modes straight into the
@@ -256,6 +257,7 @@ __device__ void dfs_elim(const T* S, int d, int sr, int q, T* slot, bool write_s
     using A = Arith<T>;
     constexpr int NB = 8;  // entries per lane per batch
     const int lane = threadIdx.x & 31;
+    PHASE_T0();
     const int m = 2 * q;
     const int dn = m - 2;
     const int total = tri_sz(dn);
@@ -295,6 +297,7 @@ __device__ void dfs_elim(const T* S, int d, int sr, int q, T* slot, bool write_s
     load_batch(0);
     // ---- pivots (all lanes, warp-uniform) and pivot-row vectors
     const Piv<T> pv = pivot2<T>(p00, p01, p11, t_in);
+    PHASE_MARK(20);
     if (lane == 0) {
         if (pv.bad0 || pv.bad1) report_breakdown(err, mask, 2 * nsel + (pv.bad0 ? 0 : 1));
         *t_out = pv.tn;
@@ -309,6 +312,7 @@ __device__ void dfs_elim(const T* S, int d, int sr, int q, T* slot, bool write_s
         }
     }
     __syncwarp();
+    PHASE_MARK(21);
     // ---- trailing update, batch by batch
     for (int kb = 0;;) {
         T out[NB];
@@ -328,6 +332,7 @@ __device__ void dfs_elim(const T* S, int d, int sr, int q, T* slot, bool write_s
         load_batch(kb);
     }
     __syncwarp();
+    PHASE_MARK(22);
 }
 
 // ---------------------------------------------------------- prefix levels ----
@@ -493,7 +498,7 @@ __device__ __forceinline__ void elim_reg(const St<T, Q>& S, St<T, Q - 1>& out, c
 // the subtree below is emitted once (instruction-cache footprint grows with L, not
 // 2^L); lower levels stay fully unrolled for instruction-level parallelism.
 #ifndef TOR_LOOPQ
-#define TOR_LOOPQ 3
+#define TOR_LOOPQ 4
 #endif
 constexpr int kLoopQ = TOR_LOOPQ;
 
@@ -913,7 +918,10 @@ template <class T, int E_LVL> struct FanLevel {
         const uint16_t* tab = tabs + WarpSmem<T>::tab_off(E_LVL);
         constexpr int NE = E * tn;
         constexpr int NIT = (NE + 31) / 32;
-        constexpr int UB = 4;  // items per batch: all loads of a batch precede its stores
+#ifndef TOR_UB
+#define TOR_UB 8
+#endif
+        constexpr int UB = TOR_UB;  // items per batch: all loads of a batch precede its stores
 #pragma unroll 1
         for (int s0 = 0; s0 < NIT; s0 += UB) {
             T sv[UB], ui[UB], uj[UB], wi[UB], wj[UB];
@@ -1401,12 +1409,13 @@ class PlanImpl final : public Plan {
         {
             unsigned long long pc[32];
             cudaMemcpyFromSymbol(pc, g_phase_cycles, sizeof(pc));
-            const char* names[20] = {"dfs_elim", "root_copy", "-", "-", "lane_tree", "L1 piv", "L1 vec",
+            const char* names[23] = {"dfs_elim", "root_copy", "-", "-", "lane_tree", "L1 piv", "L1 vec",
                                      "L1 ent", "L2 piv", "L2 vec", "L2 ent", "L3 piv", "L3 vec", "L3 ent",
-                                     "L4 piv", "L4 vec", "L4 ent", "L5 piv", "L5 vec", "L5 ent"};
+                                     "L4 piv", "L4 vec", "L4 ent", "L5 piv", "L5 vec", "L5 ent",
+                                     "dfs ld+piv", "dfs vec", "dfs ent"};
             double tot = 0;
             for (int i = 0; i < 20; ++i) tot += pc[i];
-            for (int i = 0; i < 20; ++i)
+            for (int i = 0; i < 23; ++i)
                 if (pc[i])
                     std::fprintf(stderr, "[phase] %-10s %6.2f%%  %.3e warp-cycles\n", names[i], 100.0 * pc[i] / tot,
                                  (double)pc[i]);
