@@ -67,7 +67,11 @@ typedef enum {
     TOR_PREC_AUTO = 0,
     TOR_PREC_W128_DD = 1,
     TOR_PREC_W256_QD = 2,
-    TOR_PREC_FP64 = 3
+    TOR_PREC_FP64 = 3,
+    /* exact fixed-point validation modes (n <= 24): the reference's own per-subset
+     * algorithm on the GPU integer pipes; raw_limbs identical to the reference */
+    TOR_PREC_FIXED128 = 4,
+    TOR_PREC_FIXED256 = 5
 } tor_precision;
 
 typedef struct {
@@ -121,6 +125,8 @@ typedef struct {
     uint64_t kernel_launches; /* device kernels launched by the call */
     uint64_t h2d_bytes;       /* host->device bytes copied by the call */
     uint64_t d2h_bytes;       /* device->host bytes copied by the call */
+    uint64_t raw_limbs[4];    /* FixedValue limbs (exact in FIXED modes; DD/QD words
+                                 re-quantised at config.frac_bits otherwise: 0) */
 } tor_result;
 
 /* Shard partial for multi-GPU / multi-process folds: a contiguous, power-of-two

@@ -63,6 +63,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     jobs = [
         ([nvcc] + NVCC_FLAGS + [f"-D{d}" for d in defines] + inc + ["-c", os.path.join(CSRC, "engine.cu"), "-o", os.path.join(BUILD, "engine.o")],
          os.path.join(BUILD, "engine.log")),
+        ([nvcc] + NVCC_FLAGS + inc + ["-c", os.path.join(CSRC, "fixed.cu"), "-o", os.path.join(BUILD, "fixed.o")],
+         os.path.join(BUILD, "fixed.log")),
         (["g++"] + CXX_FLAGS + inc + ["-c", os.path.join(CSRC, "host.cpp"), "-o", os.path.join(BUILD, "host.o")],
          os.path.join(BUILD, "host.log")),
         (["g++"] + CXX_FLAGS + inc + ["-c", os.path.join(CSRC, "capi.cpp"), "-o", os.path.join(BUILD, "capi.o")],
@@ -71,7 +73,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     with ThreadPoolExecutor(len(jobs)) as ex:
         list(ex.map(lambda j: _run(*j), jobs))
     tmp = lib_path + ".tmp"
-    _run([nvcc] + ARCH + ["-shared", "-o", tmp, os.path.join(BUILD, "engine.o"), os.path.join(BUILD, "host.o"),
+    _run([nvcc] + ARCH + ["-shared", "-o", tmp, os.path.join(BUILD, "engine.o"), os.path.join(BUILD, "fixed.o"),
+                          os.path.join(BUILD, "host.o"),
                           os.path.join(BUILD, "capi.o"), "-lcudart_static", "-lrt", "-lpthread", "-ldl"],
          os.path.join(BUILD, "link.log"))
     os.replace(tmp, lib_path)

@@ -21,10 +21,11 @@ from .matrix import InputMatrix
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TOR_B200_LIB") or os.path.join(_PKG, "libtor_b200.so")
 
-PREC_AUTO, PREC_DD, PREC_QD, PREC_FP64 = 0, 1, 2, 3
+PREC_AUTO, PREC_DD, PREC_QD, PREC_FP64, PREC_FIXED128, PREC_FIXED256 = 0, 1, 2, 3, 4, 5
 _PREC = {"auto": PREC_AUTO, "128": PREC_DD, "dd": PREC_DD, "256": PREC_QD, "qd": PREC_QD,
-         "fp64": PREC_FP64, "64": PREC_FP64}
-_MODE_NAME = {PREC_DD: "dd", PREC_QD: "qd", PREC_FP64: "fp64"}
+         "fp64": PREC_FP64, "64": PREC_FP64, "fixed128": PREC_FIXED128, "fixed256": PREC_FIXED256}
+_MODE_NAME = {PREC_DD: "dd", PREC_QD: "qd", PREC_FP64: "fp64", PREC_FIXED128: "fixed128",
+              PREC_FIXED256: "fixed256"}
 
 
 class TorInput(C.Structure):
@@ -49,7 +50,7 @@ class TorResult(C.Structure):
                 ("wall_seconds", C.c_double), ("device_ms", C.c_double), ("kernel_ms", C.c_double),
                 ("devices", C.c_int), ("escalated", C.c_int), ("sum_abs_terms", C.c_double),
                 ("cancellation_bits", C.c_double), ("bits_left", C.c_double), ("kernel_launches", C.c_uint64),
-                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("raw_limbs", C.c_uint64 * 4)]
 
 
 class TorPartial(C.Structure):
@@ -147,7 +148,8 @@ def _result_dict(r: TorResult, workers: int) -> dict:
     return {
         # reference keys (bindings.cpp:69-85)
         "value": r.value,
-        "raw_limbs": raw_limbs(words, r.width_bits, cfg["frac_bits"]),
+        "raw_limbs": (tuple(int(x) for x in r.raw_limbs) if r.mode in (PREC_FIXED128, PREC_FIXED256)
+                      else raw_limbs(words, r.width_bits, cfg["frac_bits"])),
         "width_bits": r.width_bits,
         "config": cfg,
         "term_count": r.term_count,

@@ -129,6 +129,68 @@ void fill_result(const Input& a, int mode, const PrecCfg& cfg, const EngineOut& 
     r->d2h_bytes = st.d2h_bytes;
 }
 
+// Exact fixed-point validation mode: the reference's algorithm on the GPU (fixed.cu).
+void fixed_mode(const Input& a, int width, int dev, tor_result* r) {
+    if (a.n > 24) throw HostError(TOR_E_INVALID, "torontonian/range", "fixed-point validation mode supports N <= 24");
+    device_check(dev);
+    const PrecCfg cfg = force_width(a, width);
+    std::vector<double> w00(a.a00.size() * 2), w01(a.a01.size() * 2);
+    for (size_t i = 0; i < a.a00.size(); ++i) {
+        w00[2 * i] = a.a00[i].real();
+        w00[2 * i + 1] = a.a00[i].imag();
+        w01[2 * i] = a.a01[i].real();
+        w01[2 * i + 1] = a.a01[i].imag();
+    }
+    uint64_t limbs[4] = {0, 0, 0, 0};
+    FixedStats fs;
+    std::string e;
+    if (fixed_run(dev, width, a.n, w00.data(), w01.data(), cfg.frac_bits, limbs, &fs, e) != 0)
+        throw HostError(TOR_E_DEVICE, "device/cuda", e);
+    if (fs.breakdown) {
+        HostError h(TOR_E_BREAKDOWN, "linalg/breakdown", "non-positive pivot in elimination");
+        h.pivot_row = fs.bad_row == 0xff ? -1 : fs.bad_row;
+        h.subset_mask = fs.bad_mask;
+        throw h;
+    }
+    std::memset(r, 0, sizeof(*r));
+    r->mode = width == 128 ? TOR_PREC_FIXED128 : TOR_PREC_FIXED256;
+    r->width_bits = width;
+    r->nwords = 1;
+    // fp_to_real (fixed_point.cpp:152-162): long-double accumulation of the magnitude
+    const int W = width / 64;
+    const bool neg = (limbs[W - 1] >> 63) != 0;
+    uint64_t mag[4] = {0, 0, 0, 0};
+    if (neg) {
+        uint64_t br = 0;
+        for (int i = 0; i < W; ++i) {
+            const uint64_t d = 0 - limbs[i];
+            const uint64_t nb = limbs[i] != 0;
+            mag[i] = d - br;
+            br = nb | (d < br);
+        }
+    } else {
+        for (int i = 0; i < W; ++i) mag[i] = limbs[i];
+    }
+    long double acc = 0.0L;
+    for (int i = W - 1; i >= 0; --i) acc = std::ldexp(acc, 64) + static_cast<long double>(mag[i]);
+    const double v = static_cast<double>(std::ldexp(acc, -static_cast<int>(cfg.frac_bits)));
+    r->value = neg ? -v : v;
+    r->words[0] = r->value;
+    for (int i = 0; i < 4; ++i) r->raw_limbs[i] = limbs[i];
+    put_cfg(cfg, &r->config);
+    r->term_count = a.n >= 64 ? ~0ull : (1ull << a.n);
+    op_counts(a.n, r->mults, r->adds, r->recips, r->rsqrts);
+    r->device_ms = fs.device_ms;
+    r->kernel_ms = fs.device_ms;
+    r->devices = 1;
+    r->kernel_launches = fs.launches;
+    r->sum_abs_terms = std::nan("");
+    r->cancellation_bits = std::nan("");
+    r->bits_left = std::nan("");
+    r->h2d_bytes = 2 * w00.size() * sizeof(double);
+    r->d2h_bytes = W * 8 + 8;
+}
+
 }  // namespace
 
 struct tor_plan {
@@ -222,9 +284,14 @@ int tor_torontonian(const tor_input* in, tor_precision prec, const int* devices,
         clear_err(err);
         const auto t0 = std::chrono::steady_clock::now();
         const Input a = checked_input(in, 40);
-        if (prec < TOR_PREC_AUTO || prec > TOR_PREC_FP64)
+        if (prec < TOR_PREC_AUTO || prec > TOR_PREC_FIXED256)
             throw HostError(TOR_E_INVALID, "precision/range", "unknown precision mode");
         const int dev = (devices && ndev > 0) ? devices[0] : 0;
+        if (prec == TOR_PREC_FIXED128 || prec == TOR_PREC_FIXED256) {
+            fixed_mode(a, prec == TOR_PREC_FIXED128 ? 128 : 256, dev, out);
+            out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            return TOR_OK;
+        }
         PrecCfg cfg;
         int mode;
         if (prec == TOR_PREC_AUTO) {

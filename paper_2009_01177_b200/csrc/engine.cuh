@@ -75,6 +75,18 @@ int engine_run(int device, int mode, const std::vector<PreparedInput>& inputs, c
 // shard count.  `parts` are `count` x 5 doubles (4 words + sum_abs).
 void fold_words(int mode, const double* parts, int count, double* out5);
 
+// Exact fixed-point validation mode (fixed.cu): the reference's per-subset algorithm on
+// the GPU; limbs4 receives the raw accumulator (identical to the reference's).
+struct FixedStats {
+    double device_ms = 0.0;
+    uint64_t launches = 0;
+    bool breakdown = false;
+    uint64_t bad_mask = 0;
+    int bad_row = -1;
+};
+int fixed_run(int device, int width_bits, int n, const double* a00, const double* a01, unsigned frac_bits,
+              uint64_t* limbs4, FixedStats* stats, std::string& err);
+
 // Minimum instance size handled by the tree kernel; smaller n uses the direct path.
 int engine_tree_min_n(int mode);
 

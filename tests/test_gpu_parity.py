@@ -225,3 +225,35 @@ def test_probabilities():
     assert p0 == pytest.approx(math.sqrt(det), rel=1e-12)
     m = W.generate_instance(4, 0.16, 0.06, 1234)
     assert sum(T.probability_reference(m, b) for b in range(16)) == pytest.approx(1.0, rel=1e-9)
+
+
+# ---------------------------------------------------- exact fixed-point mode ----
+FIXED_CASES = ["gen10_s1", "gen10_s2", "gen10_s3", "gen8_s99", "gen10_s321", "gen4_s2026", "gen6_s42",
+               "gen12_s7", "gen14_s11", "cfg1", "half_1", "one_mode", "diag3", "two_half", "zero_7"]
+
+
+@pytest.mark.parametrize("name", FIXED_CASES)
+def test_fixed_point_mode_limb_exact(name, golden):
+    """GPU exact fixed-point validation mode: the reference's algorithm on the integer
+    pipes reproduces the reference's raw accumulator limbs exactly."""
+    g = golden[name]
+    m = small_instance(name)
+    for p, key in (("fixed128", "fixed128"), ("fixed256", "fixed256")):
+        r = T.torontonian(m, p)
+        ref = g.get(key) or g.get("fixedauto")
+        if key not in g and r["width_bits"] != 128:
+            continue
+        assert r["config"]["frac_bits"] == ref["frac_bits"]
+        from oracle.ref import limbs_to_int
+        assert limbs_to_int(r["raw_limbs"], r["width_bits"]) == int(ref["raw"]), f"{name} {p}"
+        assert r["value"] == ref["value"]
+
+
+def test_fixed_point_mode_breakdown_like_reference(golden):
+    m = small_instance("breakdown6")
+    with pytest.raises(T.BreakdownError) as e:
+        T.torontonian(m, "fixed128")
+    assert e.value.code == "linalg/breakdown"
+    r = T.torontonian(m, "fixed256")
+    from oracle.ref import limbs_to_int
+    assert limbs_to_int(r["raw_limbs"], 256) == int(golden["breakdown6"]["fixed256"]["raw"])
