@@ -151,6 +151,54 @@ TOR_HD dd dd_rank1(dd s, dd a, dd b) {
     return dd{s1, lo};
 }
 
+// ---- fixed-exponent DD for Schur-complement states ------------------------------
+// Every entry of every Schur complement of the (scaled) R satisfies |S_ij| <= max_k R_kk
+// (SPD: Schur complements only shrink the diagonal, |S_ij| <= sqrt(S_ii S_jj)), and the
+// Cholesky row vectors satisfy |u_i u_j| <= max_k R_kk too.  With max_k R_kk < 3.75 the
+// leading word of a state entry is kept on the grid 2^-kGridG: products are rounded to
+// that grid by the add/subtract of C, and the leading-word updates s.hi - P1 - P2 are
+// then EXACT (no TwoSum); the rounding remainders go to the low word through the FMA.
+// A rank-2 entry update costs 16 FP64 instructions instead of 24, with the same
+// backward error shape (absolute, ~2^-103 of the O(1) state scale).
+constexpr int kGridG = 49;
+constexpr double kGridC = 12.0;  // 1.5 * 2^(52 - kGridG): p + C lies in [8, 16) for |p| < 4
+
+TOR_HD double grid_round(double p) { return (p + kGridC) - kGridC; }
+
+// (x + y) as a grid state entry (host-side R construction)
+TOR_HD dd dd_to_grid(double x, double y) {
+    double sh, se;
+    two_sum(x, y, sh, se);
+    const double H = grid_round(sh);
+    return dd{H, (sh - H) + se};
+}
+
+TOR_HD dd dd_rank2_grid(dd s, dd a, dd b, dd c, dd d) {
+    const double p1 = a.hi * b.hi;
+    const double P1 = grid_round(p1);
+    const double r1 = fma_(a.hi, b.hi, -P1);
+    const double p2 = c.hi * d.hi;
+    const double P2 = grid_round(p2);
+    const double r2 = fma_(c.hi, d.hi, -P2);
+    const double hi = (s.hi - P1) - P2;
+    double lo = s.lo - r1;
+    lo = lo - r2;
+    lo = fma_(-a.hi, b.lo, lo);
+    lo = fma_(-a.lo, b.hi, lo);
+    lo = fma_(-c.hi, d.lo, lo);
+    lo = fma_(-c.lo, d.hi, lo);
+    return dd{hi, lo};
+}
+TOR_HD dd dd_rank1_grid(dd s, dd a, dd b) {
+    const double p1 = a.hi * b.hi;
+    const double P1 = grid_round(p1);
+    const double r1 = fma_(a.hi, b.hi, -P1);
+    double lo = s.lo - r1;
+    lo = fma_(-a.hi, b.lo, lo);
+    lo = fma_(-a.lo, b.hi, lo);
+    return dd{s.hi - P1, lo};
+}
+
 // 1/sqrt(x) for normalised x > 0: fp64 seed + one DD Newton step on the exact
 // residual r = 1 - x*y^2 (y^2 exact by TwoProd).  Result is (y, y*r/2), |lo| <= ulp.
 TOR_HD dd dd_rsqrt(dd x) {
@@ -299,6 +347,7 @@ template <> struct Arith<double> {
         return fma_(-c, d, fma_(-a, b, s));
     }
     TOR_HD static double rank1(double s, double a, double b) { return fma_(-a, b, s); }
+    TOR_HD static double rank1s(double s, double a, double b) { return fma_(-a, b, s); }
     TOR_HD static double rsqrt(double a) { return rsqrt_d(a); }
     TOR_HD static double neg(double a) { return -a; }
     TOR_HD static void words(double a, double* w) { w[0] = a; }
@@ -312,9 +361,21 @@ template <> struct Arith<dd> {
     TOR_HD static double hi(const dd& a) { return a.hi; }
     TOR_HD static dd norm(const dd& a) { return dd_norm(a); }
     TOR_HD static dd mul(const dd& a, const dd& b) { return dd_mul(a, b); }
+#ifndef TOR_DD_NOGRID
+    static constexpr bool kGrid = true;
+    // Schur-state updates: fixed-exponent (grid) DD
+    TOR_HD static dd rank2(const dd& s, const dd& a, const dd& b, const dd& c, const dd& d) {
+        return dd_rank2_grid(s, a, b, c, d);
+    }
+    TOR_HD static dd rank1s(const dd& s, const dd& a, const dd& b) { return dd_rank1_grid(s, a, b); }
+#else
+    static constexpr bool kGrid = false;
     TOR_HD static dd rank2(const dd& s, const dd& a, const dd& b, const dd& c, const dd& d) {
         return dd_rank2(s, a, b, c, d);
     }
+    TOR_HD static dd rank1s(const dd& s, const dd& a, const dd& b) { return dd_rank1(s, a, b); }
+#endif
+    // general (non-state) s - a*b
     TOR_HD static dd rank1(const dd& s, const dd& a, const dd& b) { return dd_rank1(s, a, b); }
     TOR_HD static dd rsqrt(const dd& a) { return dd_rsqrt(a); }
     TOR_HD static dd neg(const dd& a) { return dd_neg(a); }
@@ -336,6 +397,7 @@ template <> struct Arith<qd> {
         return qd_rank2(s, a, b, c, d);
     }
     TOR_HD static qd rank1(const qd& s, const qd& a, const qd& b) { return qd_rank1(s, a, b); }
+    TOR_HD static qd rank1s(const qd& s, const qd& a, const qd& b) { return qd_rank1(s, a, b); }
     TOR_HD static qd rsqrt(const qd& a) { return qd_rsqrt(a); }
     TOR_HD static qd neg(const qd& a) { return qd_neg(a); }
     TOR_HD static void words(const qd& a, double* w) {
@@ -348,10 +410,21 @@ template <> struct Arith<qd> {
 // QD terms in QD.  Sum |t| is carried in fp64 for the posterior cancellation check.
 template <class T> struct Acc;
 
+// term scaling for scaled inputs (R -> 2^-s R multiplies t(Z) by 2^(s|Z|)): exact
+TOR_HD double pow2i(int e) {
+#if defined(__CUDA_ARCH__)
+    return __hiloint2double((1023 + e) << 20, 0);
+#else
+    return std::ldexp(1.0, e);
+#endif
+}
+
 template <> struct Acc<double> {
     dd s{0.0, 0.0};
     double abs_sum = 0.0;
-    TOR_HD void add(double t, bool negative) {
+    int sc = 0;
+    TOR_HD void add(double t, bool negative, int z) {
+        if (sc) t *= pow2i(-sc * z);
         const double v = negative ? -t : t;
         double h, e;
         two_sum(s.hi, v, h, e);
@@ -381,7 +454,13 @@ template <> struct Acc<dd> {
     dd s{0.0, 0.0};
     double h = 0.0, c = 0.0;
     double abs_sum = 0.0;
-    TOR_HD void add(const dd& t, bool negative) {
+    int sc = 0;
+    TOR_HD void add(dd t, bool negative, int z) {
+        if (sc) {
+            const double f = pow2i(-sc * z);
+            t.hi *= f;
+            t.lo *= f;
+        }
         const double th = negative ? -t.hi : t.hi;
         const double tl = negative ? -t.lo : t.lo;
         double nh, e;
@@ -410,7 +489,9 @@ template <> struct Acc<dd> {
 template <> struct Acc<qd> {
     qd s{{0.0, 0.0, 0.0, 0.0}};
     double abs_sum = 0.0;
-    TOR_HD void add(const qd& t, bool negative) {
+    int sc = 0;
+    TOR_HD void add(const qd& t, bool negative, int z) {
+        (void)z;  // QD words are never grid-scaled
         s = qd_add(s, negative ? qd_neg(t) : t);
         abs_sum += fabs(t.x[0]);
     }

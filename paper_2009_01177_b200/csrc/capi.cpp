@@ -88,7 +88,7 @@ std::vector<EngineOut> run(int device, int mode, const std::vector<Input>& ins, 
     std::vector<PreparedInput> prep(ins.size());
     for (size_t i = 0; i < ins.size(); ++i) {
         prep[i].n = ins[i].n;
-        prep[i].R = build_R(ins[i], mode_words(mode));
+        prep[i].R = build_R(ins[i], mode_words(mode), mode == MODE_DD, &prep[i].tscale_log2);
     }
     std::vector<EngineOut> out;
     std::string err;
@@ -483,7 +483,7 @@ int tor_plan_create(const tor_input* in, tor_precision prec, int class_bits, uin
         else p->cfg = force_width(a, p->mode == MODE_DD ? 128 : 256);
         PreparedInput pi;
         pi.n = a.n;
-        pi.R = build_R(a, mode_words(p->mode));
+        pi.R = build_R(a, mode_words(p->mode), p->mode == MODE_DD, &pi.tscale_log2);
         WorkRange wr;
         wr.class_bits = class_bits;
         wr.class_lo = class_lo;

@@ -192,7 +192,7 @@ __device__ void warp_elim(const T* S, int d, int sr, int q, T* dst, const T& t_i
     const int m = 2 * q;
     for (int j = 2 + lane; j < m; j += 32) {
         const T uj = A::mul(S[tri_ix(d, sr, sr + j)], r1);
-        const T wj = A::mul(A::rank1(S[tri_ix(d, sr + 1, sr + j)], u1, uj), r2);
+        const T wj = A::mul(A::rank1s(S[tri_ix(d, sr + 1, sr + j)], u1, uj), r2);
         uw[j] = uj;
         uw[m + j] = wj;
     }
@@ -308,7 +308,7 @@ __device__ void dfs_elim(const T* S, int d, int sr, int q, T* slot, bool write_s
         if (jv < m) {
             const T uj = A::mul(v0[r], pv.r1);
             uw[jv] = uj;
-            uw[m + jv] = A::mul(A::rank1(v1[r], pv.u1, uj), pv.r2);
+            uw[m + jv] = A::mul(A::rank1s(v1[r], pv.u1, uj), pv.r2);
         }
     }
     __syncwarp();
@@ -483,7 +483,7 @@ __device__ __forceinline__ void elim_reg(const St<T, Q>& S, St<T, Q - 1>& out, c
 #pragma unroll
     for (int j = 2; j < M; ++j) {
         u[j] = A::mul(S.e[cix<M>(0, j)], r1);
-        w[j] = A::mul(A::rank1(S.e[cix<M>(1, j)], u1, u[j]), r2);
+        w[j] = A::mul(A::rank1s(S.e[cix<M>(1, j)], u1, u[j]), r2);
     }
 #pragma unroll
     for (int i = 2; i < M; ++i)
@@ -511,7 +511,7 @@ template <class T, int Q> struct SubReg {
         T tn;
         if (br == 0) {
             elim_reg<T, Q>(S, Sn, t, tn, mask | bit, nsel, err);
-            acc.add(tn, !neg);
+            acc.add(tn, !neg, nsel + 1);
         } else {
 #pragma unroll
             for (int i = 2; i < M; ++i)
@@ -540,7 +540,7 @@ template <class T> struct SubReg<T, 1> {
         const T det = A::norm(A::rank1(A::mul(S.e[0], S.e[2]), S.e[1], S.e[1]));
         if (nonpositive(A::hi(det))) report_breakdown(err, mask | 1ull, 2 * nsel + 1);
         const T tn = A::mul(t, A::rsqrt(det));
-        acc.add(tn, !neg);
+        acc.add(tn, !neg, nsel + 1);
     }
 };
 
@@ -552,7 +552,7 @@ __device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t,
                                           Acc<T>& acc, unsigned long long* err) {
     using A = Arith<T>;
     constexpr int M = 2 * L;
-    acc.add(t, neg);
+    acc.add(t, neg, nsel);
     const uint64_t bit = 1ull << (L - 1);
 #pragma unroll 1
     for (int br = 0; br < 2; ++br) {
@@ -567,7 +567,7 @@ __device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t,
 #pragma unroll
             for (int j = 2; j < M; ++j) {
                 u[j] = A::mul(S[tri_ix(d, sr, sr + j)], r1);
-                w[j] = A::mul(A::rank1(S[tri_ix(d, sr + 1, sr + j)], u1, u[j]), r2);
+                w[j] = A::mul(A::rank1s(S[tri_ix(d, sr + 1, sr + j)], u1, u[j]), r2);
             }
 #pragma unroll
             for (int i = 2; i < M; ++i)
@@ -575,7 +575,7 @@ __device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t,
                 for (int j = i; j < M; ++j)
                     Sn.e[cix<M - 2>(i - 2, j - 2)] =
                         A::rank2(S[tri_ix(d, sr + i, sr + j)], u[i], u[j], w[i], w[j]);
-            acc.add(tn, !neg);
+            acc.add(tn, !neg, nsel + 1);
         } else {
 #pragma unroll
             for (int i = 2; i < M; ++i)
@@ -678,7 +678,7 @@ __device__ __forceinline__ void lane_tree_tmem(uint32_t row, const T& t, bool ne
     using A = Arith<T>;
     constexpr int M = 2 * L;
     constexpr int K01 = 2 * M - 1;  // entries of rows 0 and 1
-    acc.add(t, neg);
+    acc.add(t, neg, nsel);
     const uint64_t bit = 1ull << (L - 1);
 #pragma unroll 1
     for (int br = 0; br < 2; ++br) {
@@ -699,14 +699,14 @@ __device__ __forceinline__ void lane_tree_tmem(uint32_t row, const T& t, bool ne
 #pragma unroll
             for (int j = 2; j < M; ++j) {
                 u[j] = A::mul(e0[j], pv.r1);
-                w[j] = A::mul(A::rank1(e0[M + j - 1], pv.u1, u[j]), pv.r2);
+                w[j] = A::mul(A::rank1s(e0[M + j - 1], pv.u1, u[j]), pv.r2);
             }
             // trailing block in two waves to bound live registers
             constexpr int NT = tri_sz(M - 2);
             constexpr int H = NT / 2;
             lt_wave<T, M, 0, H>(row + 4 * K01, u, w, Sn);
             lt_wave<T, M, H, NT - H>(row + 4 * K01, u, w, Sn);
-            acc.add(tn, !neg);
+            acc.add(tn, !neg, nsel + 1);
         } else {
             constexpr int NT = tri_sz(M - 2);
             uint32_t rt[4 * NT];
@@ -848,7 +848,7 @@ template <class T, int E_LVL> struct FanLevel {
 #pragma unroll
             for (int u = 0; u < NVI; ++u) {
                 s0v[u] = A::mul(s0v[u], r1v[u]);
-                s1v[u] = A::mul(A::rank1(s1v[u], u1v[u], s0v[u]), r2v[u]);
+                s1v[u] = A::mul(A::rank1s(s1v[u], u1v[u], s0v[u]), r2v[u]);
             }
 #pragma unroll
             for (int u = 0; u < NVI; ++u)
@@ -960,7 +960,7 @@ template <class T, int E_LVL> struct FanLevel {
 template <class T>
 __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
     subtree_kernel(const Job<T>* jobs, uint64_t njobs, int nmodes, int rjob, T* scratch, size_t scratch_stride,
-                   double* partials, unsigned long long* err, unsigned long long* job_counter) {
+                   double* partials, unsigned long long* err, unsigned long long* job_counter, int tsc) {
     using SM = WarpSmem<T>;
     constexpr int L = Cfg<T>::L;
     constexpr int Q0 = SM::Q0;
@@ -1016,6 +1016,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         if (job >= njobs) break;
         const Job<T> J = jobs[job];
         Acc<T> acc;
+        acc.sc = tsc;
 
         for (uint64_t leaf = 0; leaf < (1ull << D); ++leaf) {
             PHASE_T0();
@@ -1130,12 +1131,13 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
 // gathered 2|W| x 2|W| Schur-complement submatrix.
 template <class T, int RMAX>
 __global__ void small_job_kernel(const Job<T>* jobs, uint64_t njobs, int nmodes, int rjob, double* partials,
-                                 unsigned long long* err) {
+                                 unsigned long long* err, int tsc) {
     using A = Arith<T>;
     const uint64_t jid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (jid >= njobs) return;
     const Job<T> J = jobs[jid];
     Acc<T> acc;
+    acc.sc = tsc;
     T M[tri_sz(2 * RMAX)];
     int sel[RMAX];
     for (uint64_t w = 0; w < (1ull << rjob); ++w) {
@@ -1162,7 +1164,7 @@ __global__ void small_job_kernel(const Job<T>* jobs, uint64_t njobs, int nmodes,
                     M[tri_ix(d, i, j)] = A::rank1(M[tri_ix(d, i, j)], M[tri_ix(d, k, i)], M[tri_ix(d, k, j)]);
         }
         const bool neg = ((nmodes - J.nsel - z) & 1) != 0;
-        acc.add(t, neg);
+        acc.add(t, neg, J.nsel + z);
         acc.flush();
     }
     double wds[4];
@@ -1233,6 +1235,7 @@ class PlanImpl final : public Plan {
         constexpr int Q0 = Cfg<T>::L + FAN;
         device_ = device;
         ninst_ = static_cast<int>(inputs.size());
+        for (const auto& in : inputs) tsc_ = std::max(tsc_, in.tscale_log2);
         n_ = inputs[0].n;
         kbits_ = range.class_bits;
         clo_ = range.class_lo;
@@ -1312,6 +1315,7 @@ class PlanImpl final : public Plan {
                     std::fprintf(stderr, "[tor]   smem %zu -> %d blocks/SM (avail dyn smem @2 blocks: %zu)\n", s2, b2,
                                  avail);
                 }
+                cudaGetLastError();  // the availability query errors for TMEM kernels; not sticky
             }
             blocks_ = std::min<uint64_t>(static_cast<uint64_t>(bps) * sm_count_, (njobs_ + WPB - 1) / WPB);
             const int D = rjob_ - Q0;
@@ -1385,11 +1389,11 @@ class PlanImpl final : public Plan {
         if (rjob_ >= Q0) {
             constexpr int WPB = Cfg<T>::WPB;
             subtree_kernel<T><<<static_cast<unsigned>(blocks_), 32 * WPB, smem_, st_>>>(
-                jobs, njobs_, n_, rjob_, static_cast<T*>(scr_.p), scr_stride_, parts, errw, ctr);
+                jobs, njobs_, n_, rjob_, static_cast<T*>(scr_.p), scr_stride_, parts, errw, ctr, tsc_);
         } else {
             const uint64_t blocks = (njobs_ + 127) / 128;
             small_job_kernel<T, Q0 - 1><<<static_cast<unsigned>(blocks), 128, 0, st_>>>(jobs, njobs_, n_, rjob_,
-                                                                                        parts, errw);
+                                                                                        parts, errw, tsc_);
         }
         ++launches;
         CK(cudaGetLastError());
@@ -1453,7 +1457,7 @@ class PlanImpl final : public Plan {
   private:
     T* pool() { return static_cast<T*>(pool_.p); }
     T* tpool() { return static_cast<T*>(tpool_.p); }
-    int device_ = 0, ninst_ = 0, n_ = 0, kbits_ = 0, sm_count_ = 0, c_ = 0, cj_ = 0, rjob_ = 0;
+    int device_ = 0, ninst_ = 0, n_ = 0, kbits_ = 0, sm_count_ = 0, c_ = 0, cj_ = 0, rjob_ = 0, tsc_ = 0;
     uint64_t clo_ = 0, chi_ = 1, per_ = 0, njobs_ = 0, blocks_ = 0;
     bool use_levels_ = true;
     PrefixGeom g_{};

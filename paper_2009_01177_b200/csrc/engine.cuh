@@ -24,6 +24,7 @@ inline int mode_words(int mode) { return mode == MODE_FP64 ? 1 : (mode == MODE_D
 struct PreparedInput {
     int n = 0;
     std::vector<double> R;  // tri(2n) * words
+    int tscale_log2 = 0;    // R was scaled by 2^-s: every term is multiplied back by 2^(-s|Z|)
 };
 
 // Work selection: prefix classes of the top `class_bits` reference-mask bits

@@ -208,7 +208,7 @@ PrecCfg force_width(const Input& a, int width_bits) {  // precision.cpp:123-148
 //   R(p_i,x_j) = Im P + Im Q   R(p_i,p_j) = Re P - Re Q
 // Each entry is the sum of two input doubles: exact as a DD (TwoSum), rounded once
 // in fp64 mode.
-std::vector<double> build_R(const Input& a, int words) {
+std::vector<double> build_R(const Input& a, int words, bool grid, int* tscale_log2) {
     const int n = a.n, d = 2 * n;
     std::vector<double> R(static_cast<size_t>(d) * (d + 1) / 2 * words, 0.0);
     auto P = [&](int i, int j) -> std::complex<double> {
@@ -216,22 +216,44 @@ std::vector<double> build_R(const Input& a, int words) {
         return -a.a00_at(i, j);
     };
     auto Q = [&](int i, int j) -> std::complex<double> { return -a.a01_at(i, j); };
+    auto parts = [&](int r, int s, double& x, double& y) {
+        const int i = r >> 1, j = s >> 1;
+        const bool ri = r & 1, sj = s & 1;
+        const auto p = P(i, j);
+        const auto q = Q(i, j);
+        if (!ri && !sj) { x = p.real(); y = q.real(); }
+        else if (!ri && sj) { x = q.imag(); y = -p.imag(); }
+        else if (ri && !sj) { x = p.imag(); y = q.imag(); }
+        else { x = p.real(); y = -q.real(); }
+    };
+    // grid (fixed-exponent) DD states need max_k R_kk < 3.75 (arith.cuh); larger inputs are
+    // scaled by an exact power of two, undone per term on the device (Acc::sc)
+    int sc = 0;
+    if (grid) {
+        double dmax = 0.0;
+        for (int r = 0; r < d; ++r) {
+            double x, y;
+            parts(r, r, x, y);
+            dmax = std::max(dmax, std::fabs(x + y));
+        }
+        while (std::ldexp(dmax, -sc) >= 3.75) ++sc;
+    }
+    if (tscale_log2) *tscale_log2 = sc;
     for (int r = 0; r < d; ++r)
         for (int s = r; s < d; ++s) {
-            const int i = r >> 1, j = s >> 1;
-            const bool ri = r & 1, sj = s & 1;
-            const auto p = P(i, j);
-            const auto q = Q(i, j);
             double x, y;
-            if (!ri && !sj) { x = p.real(); y = q.real(); }
-            else if (!ri && sj) { x = q.imag(); y = -p.imag(); }
-            else if (ri && !sj) { x = p.imag(); y = q.imag(); }
-            else { x = p.real(); y = -q.real(); }
-            double hi, lo;
-            two_sum(x, y, hi, lo);
+            parts(r, s, x, y);
             double* e = &R[tri(d, r, s) * words];
-            e[0] = hi;
-            if (words >= 2) e[1] = lo;
+            if (grid) {
+                const dd g = dd_to_grid(std::ldexp(x, -sc), std::ldexp(y, -sc));
+                e[0] = g.hi;
+                e[1] = g.lo;
+            } else {
+                double hi, lo;
+                two_sum(x, y, hi, lo);
+                e[0] = hi;
+                if (words >= 2) e[1] = lo;
+            }
         }
     return R;
 }

@@ -50,7 +50,7 @@ PrecCfg force_width(const Input& a, int width_bits);
 
 // Exact R in `words` doubles per entry (1: rounded fp64, 2: DD, 4: QD), packed upper
 // triangle of the 2n x 2n matrix in pair order (x_0, p_0, x_1, p_1, ...).
-std::vector<double> build_R(const Input& a, int words);
+std::vector<double> build_R(const Input& a, int words, bool grid = false, int* tscale_log2 = nullptr);
 
 // Closed-form reference op counters (linalg.hpp:44-57, flops.cpp:9-31).
 void op_counts(int n, uint64_t& mults, uint64_t& adds, uint64_t& recips, uint64_t& rsqrts);

@@ -257,3 +257,29 @@ def test_fixed_point_mode_breakdown_like_reference(golden):
     r = T.torontonian(m, "fixed256")
     from oracle.ref import limbs_to_int
     assert limbs_to_int(r["raw_limbs"], 256) == int(golden["breakdown6"]["fixed256"]["raw"])
+
+
+def test_grid_scaling_for_large_diagonals():
+    """DD states use a fixed-exponent leading word (needs max R_kk < 15); larger inputs
+    are scaled by an exact power of two and every term is scaled back by 2^(-s|Z|)."""
+    for n, a, c in ((3, -20.0, 0.0), (10, -40.0, 5.0), (12, 0.1, 0.0)):
+        m = diag_instance(n, [a] * n, [c] * n)
+        want = (1.0 / math.sqrt((1 - a) ** 2 - c * c) - 1.0) ** n
+        for prec in ("128", "256", "fp64"):
+            r = T.torontonian(m, prec)
+            assert r["value"] == pytest.approx(want, rel=1e-11), (n, a, prec)
+
+
+@pytest.mark.parametrize("n", [24, 28])
+def test_full_pipeline_dd_vs_qd(n):
+    """The full device pipeline (prefix levels, warp DFS, fan-out, TMEM lane handoff,
+    grid-DD Schur updates) at n where every stage runs: DD vs the GPU's own QD (which
+    agrees with the reference's fixed-256 at 2^-180 sum|t| on every golden case)."""
+    from paper_2009_01177_b200.matrix import select_modes
+    m = select_modes(W.load_config_instance(5), list(range(n)))
+    dd = T.torontonian(m, "128")
+    q = T.torontonian(m, "256")
+    ok, rel = within(words_value(dd["words"]), words_value(q["words"]), q["sum_abs_terms"], "dd")
+    assert ok, f"n={n}: DD vs QD {rel:.3g} sum|t|"
+    assert rel < 2.0 ** -100
+    assert abs(dd["sum_abs_terms"] - q["sum_abs_terms"]) <= 1e-12 * q["sum_abs_terms"]
