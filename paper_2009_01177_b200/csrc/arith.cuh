@@ -360,7 +360,20 @@ template <> struct Arith<dd> {
     TOR_HD static dd from(double x) { return dd{x, 0.0}; }
     TOR_HD static double hi(const dd& a) { return a.hi; }
     TOR_HD static dd norm(const dd& a) { return dd_norm(a); }
+#ifndef TOR_DD_NORMMUL
+    // Products feed further products, rank updates or the accumulator, all of which use
+    // both words: the final renormalisation is skipped (|lo| <= 2 ulp(hi)); values are
+    // renormalised explicitly where it matters (pivots before rsqrt).
+    TOR_HD static dd mul(const dd& a, const dd& b) {
+        double p, e;
+        two_prod(a.hi, b.hi, p, e);
+        e = fma_(a.hi, b.lo, e);
+        e = fma_(a.lo, b.hi, e);
+        return dd{p, e};
+    }
+#else
     TOR_HD static dd mul(const dd& a, const dd& b) { return dd_mul(a, b); }
+#endif
 #ifndef TOR_DD_NOGRID
     static constexpr bool kGrid = true;
     // Schur-state updates: fixed-exponent (grid) DD
