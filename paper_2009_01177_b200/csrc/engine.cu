@@ -25,6 +25,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
 
 #include "arith.cuh"
 #include "engine.cuh"
@@ -41,6 +44,19 @@ __host__ __device__ constexpr int tri_sz(int d) { return d * (d + 1) / 2; }
 __host__ __device__ __forceinline__ int tri_ix(int d, int i, int j) {
     return i * d - ((i * (i + 1)) >> 1) + j;
 }
+// A view that drops the first s rows of a packed D-row triangle is itself a packed
+// (D-s)-row triangle stored contiguously at tri_ix(D, s, s):
+//   tri_ix(D, s+a, s+b) = tri_ix(D, s, s) + tri_ix(D-s, a, b).
+// So every node state (and every trailing block) is addressed as (pointer, dim).
+
+// Rank-2 trailing update of an elimination from a q-mode state (m = 2q rows): child
+// entry k (packed (m-2)-row triangle) reads parent entry 2m-1+k and the pivot-row
+// vectors at rows 2+i, 2+j.  (i,j) tables hold (2+i) | (2+j) << 16.
+__host__ __device__ constexpr uint32_t ij_word(int i, int j) {
+    return static_cast<uint32_t>(2 + i) | (static_cast<uint32_t>(2 + j) << 16);
+}
+// DFS tables in global memory: dims 2a, a = 1 .. kMaxJobModes-1, table a at ijtab_off(a)
+__host__ __device__ constexpr int ijtab_off(int a) { return 2 * (a - 1) * a * (2 * a - 1) / 6 + (a - 1) * a / 2; }
 
 // Lane-level register depth per word type (register budget: the L-mode state is
 // read from shared memory, states of < L modes live in registers).
@@ -62,9 +78,11 @@ template <> struct Cfg<dd> {
 #ifdef TOR_DD_WPB
     static constexpr int WPB = TOR_DD_WPB;
 #else
-    static constexpr int WPB = TOR_DD_TMEM ? 4 : 2;
+    // one 8-warp CTA per SM (two warps per TMEM lane quadrant, 256 columns each):
+    // measured 123 ms vs 138 ms for two 4-warp CTAs at n=32
+    static constexpr int WPB = TOR_DD_TMEM ? 8 : 2;
 #endif
-    static constexpr int MINB = TOR_DD_TMEM ? 2 : 1;
+    static constexpr int MINB = (TOR_DD_TMEM && WPB == 4) ? 2 : 1;
     static constexpr bool TMEM = TOR_DD_TMEM;
 };
 template <> struct Cfg<qd> {
@@ -75,6 +93,9 @@ template <> struct Cfg<qd> {
 };
 
 template <class T> constexpr int root_modes() { return Cfg<T>::L + FAN; }
+
+constexpr int kIjTabEntries = ijtab_off(kMaxJobModes);
+__device__ uint32_t g_ijtab[kIjTabEntries];
 
 // ----------------------------------------------------------------- jobs ----
 template <class T> struct Job {
@@ -247,51 +268,42 @@ __device__ unsigned long long g_phase_cycles[32];
 #endif
 
 // DFS step of the subtree kernel: eliminates the first mode of the q-mode source
-// view (HBM/L2 resident) and writes (a) the new (q-1)-mode state to its DFS slot
-// (only when later leaves read it) and (b) its trailing Q0 modes straight into the
-// shared-memory root of the leaf that follows (no separate root copy).  All global
-// loads of the common sizes (q <= 11) are issued up front: one L2 round trip.
+// state P (contiguous packed 2q-row triangle, HBM/L2 resident) and writes (a) the new
+// (q-1)-mode state to its DFS slot (only when later leaves read it) and (b) its
+// trailing Q0 modes -- the contiguous tail of the new state -- straight into the
+// shared-memory root of the leaf that follows.  Entry k of the new state reads P at
+// 2m-1+k; its (i,j) comes from the global table tb.  All loads of the first batch
+// are issued before the pivot chain: one L2 round trip.
 template <class T, int Q0>
-__device__ void dfs_elim(const T* S, int d, int sr, int q, T* slot, bool write_slot, T* root, const T& t_in,
-                         T* t_out, T* uw, uint64_t mask, int nsel, unsigned long long* err) {
+__device__ void dfs_elim(const T* P, int q, T* slot, bool write_slot, T* root, const T& t_in, T* t_out, T* uw,
+                         const uint32_t* tb, uint64_t mask, int nsel, unsigned long long* err) {
     using A = Arith<T>;
     constexpr int NB = 8;  // entries per lane per batch
+    constexpr int RT = tri_sz(2 * Q0);
     const int lane = threadIdx.x & 31;
     PHASE_T0();
     const int m = 2 * q;
-    const int dn = m - 2;
-    const int total = tri_sz(dn);
-    const int so = dn - 2 * Q0;  // rows of the new state before the root block
+    const int total = tri_sz(m - 2);
+    const T* Pt = P + 2 * m - 1;
     // ---- issue loads: pivot block, this lane's pivot-row entries, first entry batch
-    const T p00 = S[tri_ix(d, sr, sr)], p01 = S[tri_ix(d, sr, sr + 1)], p11 = S[tri_ix(d, sr + 1, sr + 1)];
+    const T p00 = P[0], p01 = P[1], p11 = P[m];
     T v0[2], v1[2];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
         const int j = 2 + lane + 32 * r;
         const int jc = j < m ? j : m - 1;
-        v0[r] = S[tri_ix(d, sr, sr + jc)];
-        v1[r] = S[tri_ix(d, sr + 1, sr + jc)];
+        v0[r] = P[jc];
+        v1[r] = P[m - 1 + jc];
     }
-    int i = 0, k0 = lane;
-    while (i < dn && k0 >= dn - i) {
-        k0 -= dn - i;
-        ++i;
-    }
-    int j = i + k0;
-    int ii[NB], jj[NB];
+    uint32_t ij[NB];
     T sv[NB];
     auto load_batch = [&](int kb) {
 #pragma unroll
         for (int u = 0; u < NB; ++u) {
-            const bool ok = kb + lane + 32 * u < total;
-            ii[u] = ok ? i : 0;
-            jj[u] = ok ? j : 0;
-            sv[u] = S[tri_ix(d, sr + 2 + ii[u], sr + 2 + jj[u])];
-            j += 32;
-            while (i < dn && j >= dn) {
-                j -= dn - (i + 1);
-                ++i;
-            }
+            const int k = kb + lane + 32 * u;
+            const int kc = k < total ? k : total - 1;
+            sv[u] = Pt[kc];
+            ij[u] = __ldg(tb + kc);
         }
     };
     load_batch(0);
@@ -314,17 +326,20 @@ __device__ void dfs_elim(const T* S, int d, int sr, int q, T* slot, bool write_s
     __syncwarp();
     PHASE_MARK(21);
     // ---- trailing update, batch by batch
+    T* rootb = root - (total - RT);  // entry k >= total-RT is root entry k-(total-RT)
     for (int kb = 0;;) {
         T out[NB];
 #pragma unroll
-        for (int u = 0; u < NB; ++u) out[u] = A::rank2(sv[u], uw[2 + ii[u]], uw[2 + jj[u]], uw[m + 2 + ii[u]], uw[m + 2 + jj[u]]);
+        for (int u = 0; u < NB; ++u) {
+            const int i = static_cast<int>(ij[u] & 0xffffu), j = static_cast<int>(ij[u] >> 16);
+            out[u] = A::rank2(sv[u], uw[i], uw[j], uw[m + i], uw[m + j]);
+        }
 #pragma unroll
         for (int u = 0; u < NB; ++u) {
             const int k = kb + lane + 32 * u;
             if (k < total) {
                 if (write_slot) slot[k] = out[u];
-                const int ri = ii[u] - so, rj = jj[u] - so;
-                if (ri >= 0) root[tri_ix(2 * Q0, ri, rj)] = out[u];
+                if (k >= total - RT) rootb[k] = out[u];
             }
         }
         kb += 32 * NB;
@@ -498,7 +513,7 @@ __device__ __forceinline__ void elim_reg(const St<T, Q>& S, St<T, Q - 1>& out, c
 // the subtree below is emitted once (instruction-cache footprint grows with L, not
 // 2^L); lower levels stay fully unrolled for instruction-level parallelism.
 #ifndef TOR_LOOPQ
-#define TOR_LOOPQ 4
+#define TOR_LOOPQ 3
 #endif
 constexpr int kLoopQ = TOR_LOOPQ;
 
@@ -723,9 +738,8 @@ __device__ __forceinline__ void lane_tree_tmem(uint32_t row, const T& t, bool ne
 
 // --------------------------------------------------------- subtree kernel ----
 // Per-warp shared memory: the Q0-mode root (copy of the DFS leaf view), the
-// include buffers of the 5 fan-out levels, their t values, pivots, pivot-row
-// vectors and per-level parent descriptors.  Per block: (i,j) lookup tables of
-// the packed triangles the kernel walks (built once per block).
+// include buffers of the fan-out levels, their t values, the pivot-row vectors and
+// the DFS t values.  Per block: (i,j) tables of the fan-out child triangles.
 template <class T> struct WarpSmem {
     static constexpr int L = Cfg<T>::L;
     static constexpr int Q0 = L + FAN;
@@ -736,176 +750,169 @@ template <class T> struct WarpSmem {
     }
     // with TMEM the last level's include states never touch shared memory
     static constexpr int kBufEntries = Cfg<T>::TMEM ? lvl_off(FAN) : lvl_off(FAN + 1);
-    static constexpr int kTOff = kBufEntries;   // t of level buffers at 2^(e-1)-1+p, root t at 31
-    static constexpr int kPivOff = kTOff + 32;  // r1 / u1 / r2 of up to 16 eliminations
+    static constexpr int kTOff = kBufEntries;  // t of level buffers at 2^(e-1)-1+p, root t at 31
     __host__ __device__ static constexpr int uw_need() {
         int mx = 4 * kMaxJobModes;  // DFS eliminations: 4q entries
         for (int e = 1; e <= FAN; ++e) {
-            const int need = (1 << (e - 1)) * 2 * 2 * (Q0 - e + 1);
+            const int need = (1 << (e - 1)) * (4 * (Q0 - e + 1) + 1);  // stride 2m+1 per parent
             if (need > mx) mx = need;
         }
         return mx;
     }
-    static constexpr int kUwOff = kPivOff + 48;
+    static constexpr int kUwOff = kTOff + 32;
     static constexpr int kUwEntries = uw_need();
     static constexpr int kDfsT = kUwOff + kUwEntries;  // DFS slot t values (<= 32)
     static constexpr int kEntries = kDfsT + 32;
-    static constexpr int kDescInts = 16 * 4;           // per-level parent descriptors
-    static constexpr size_t kWarpBytes = kEntries * sizeof(T) + kDescInts * sizeof(int);
-    // (i,j) tables for triangle dims 2*(Q0-e), e = 0..FAN  (u16: i << 8 | j)
-    __host__ __device__ static constexpr int tab_off(int e) {
+    static constexpr size_t kWarpBytes = kEntries * sizeof(T);
+    // Block-wide item tables of the fan-out trailing updates: level e has E*tn items
+    // (it = x*tn + k: child x, entry k); word = src | ui << 11 | uj << 20 with src the
+    // parent entry (index into the warp area; the smem layout is static, so this is a
+    // constant per item), ui/uj the uw indices of u_i/u_j (w_i/w_j at +m).
+    // Levels 1..kItemLevels use item tables; with TMEM the last level uses the (i,j)
+    // table (ij_word) of its child triangle instead.
+    static constexpr int kItemLevels = Cfg<T>::TMEM ? FAN - 1 : FAN;
+    __host__ __device__ static constexpr int item_off(int e) {
         int o = 0;
-        for (int x = 0; x < e; ++x) o += tri_sz(2 * (Q0 - x));
+        for (int x = 1; x < e; ++x) o += (1 << (x - 1)) * tri_sz(2 * (Q0 - x));
         return o;
     }
-    static constexpr int kTabEntries = tab_off(FAN + 1);
-    static constexpr size_t kTabBytes = ((kTabEntries * 2 + 15) / 16) * 16;
+    static constexpr int kLastTabOff = item_off(kItemLevels + 1);
+    // node offsets: node (e, c), e = 0..FAN, at kNodeOff + 2^e - 1 + c
+    static constexpr int kNodeOff = kLastTabOff + (Cfg<T>::TMEM ? tri_sz(2 * (Q0 - FAN)) : 0);
+    static constexpr int kTabEntries = kNodeOff + (2 << FAN) - 1;
+    static constexpr size_t kTabBytes = ((kTabEntries * 4 + 15) / 16) * 16;
+    static_assert(kBufEntries < 2048 && uw_need() <= 512, "item word fields");
 };
 
-template <class T, int Q0>
-__device__ __forceinline__ void lane_view(const T* sm, int c, const T*& base, int& dim, int& skip, T& t,
-                                          const T* tvals, int e) {
-    // node (e, c) of the breadth-first fan-out rooted at the copied root (level 0)
-    if (c == 0) {
-        base = sm;
-        dim = 2 * Q0;
-        skip = e;
-        t = tvals[31];
-        return;
-    }
+// Node (e, c) of the breadth-first fan-out rooted at the copied root (level 0): its
+// state is a contiguous packed 2(Q0-e)-row triangle (an include buffer, or a view of
+// an ancestor's trailing block for exclude chains) and its term factor t.
+template <class T>
+__device__ __forceinline__ int node_off(int e, int c) {
+    constexpr int Q0 = WarpSmem<T>::Q0;
+    if (c == 0) return tri_ix(2 * Q0, 2 * e, 2 * e);
     const int tz = __ffs(c) - 1;
     const int lvl = e - tz;
     const int p = (c >> tz) >> 1;
-    dim = 2 * (Q0 - lvl);
-    int off = tri_sz(2 * Q0);
-#pragma unroll
-    for (int x = 1; x < FAN; ++x)
-        if (x < lvl) off += (1 << (x - 1)) * tri_sz(2 * (Q0 - x));
-    base = sm + off + p * tri_sz(dim);
-    skip = tz;
-    t = tvals[(1 << (lvl - 1)) - 1 + p];
+    const int dim = 2 * (Q0 - lvl);
+    return WarpSmem<T>::lvl_off(lvl) + p * tri_sz(dim) + tri_ix(dim, 2 * tz, 2 * tz);
+}
+__device__ __forceinline__ int node_tix(int e, int c) {
+    if (c == 0) return 31;
+    const int tz = __ffs(c) - 1;
+    const int lvl = e - tz;
+    return (1 << (lvl - 1)) - 1 + ((c >> tz) >> 1);
+}
+// node (e, c) from the per-block node table: word = node_off | node_tix << 16
+struct NodeRef {
+    int off, tix;
+};
+template <class T>
+__device__ __forceinline__ NodeRef node_ref(const uint32_t* tabs, int e, int c) {
+    const uint32_t w = tabs[WarpSmem<T>::kNodeOff + (1 << e) - 1 + c];
+    return NodeRef{static_cast<int>(w & 0xffffu), static_cast<int>(w >> 16)};
 }
 
 // One breadth-first level: the E = 2^(e-1) include nodes of level e each eliminate
-// the first mode of their parent (level e-1 node x) into level-e buffer x.
+// the first mode of their parent (level e-1 node x) into level-e buffer x.  Lane
+// (x, g) = (lane % E, lane / E) works on parent x throughout (pivots redundantly in
+// registers, pivot-row vectors j = 2+g+sG, trailing entries k = g+sG, G = 32/E), so
+// every source, table and destination address is a per-lane base plus a constant.
+#ifndef TOR_UB
+#define TOR_UB 8
+#endif
 template <class T, int E_LVL> struct FanLevel {
     static constexpr int Q0 = WarpSmem<T>::Q0;
     static constexpr int E = 1 << (E_LVL - 1);
+    static constexpr int G = 32 / E;
     static constexpr int q = Q0 - E_LVL + 1;  // parent modes
     static constexpr int m = 2 * q;
     static constexpr int dn = m - 2;
     static constexpr int tn = tri_sz(dn);
-    __device__ __forceinline__ static void run(T* sm, T* tvals, T* piv, T* uwv, int* desc, const uint16_t* tabs,
-                                               uint64_t leaf_mask, int leaf_sel, unsigned long long* err,
-                                               uint32_t tm_row) {
+    __device__ __forceinline__ static void run(T* sm, T* tvals, T* uwv, const uint32_t* tabs, uint64_t leaf_mask,
+                                               int leaf_sel, unsigned long long* err, uint32_t tm_row) {
         using A = Arith<T>;
         const int lane = threadIdx.x & 31;
+        const int x = lane & (E - 1), g = lane / E;
         PHASE_T0();
-        {
-            const int x = lane & (E - 1);
-            const T* pb;
-            int pd, psk;
-            T pt;
-            lane_view<T, Q0>(sm, x, pb, pd, psk, pt, tvals, E_LVL - 1);
-            const int sr = 2 * psk;
-            const Piv<T> pv = pivot2<T>(pb[tri_ix(pd, sr, sr)], pb[tri_ix(pd, sr, sr + 1)], pb[tri_ix(pd, sr + 1, sr + 1)], pt);
-            if (lane < E) {
-                const uint64_t nm = leaf_mask | (static_cast<uint64_t>((x << 1) | 1) << (Q0 - E_LVL));
-                if (pv.bad0 || pv.bad1) report_breakdown(err, nm, 2 * (leaf_sel + __popc(x)) + (pv.bad0 ? 0 : 1));
-                piv[x] = pv.r1;
-                piv[16 + x] = pv.u1;
-                piv[32 + x] = pv.r2;
-                tvals[E - 1 + x] = pv.tn;
-                desc[4 * x + 0] = static_cast<int>(pb - sm);
-                desc[4 * x + 1] = pd;
-                desc[4 * x + 2] = sr;
-            }
+        const NodeRef nr = node_ref<T>(tabs, E_LVL - 1, x);
+        const T* P = sm + nr.off;
+        const Piv<T> pv = pivot2<T>(P[0], P[1], P[m], tvals[nr.tix]);
+        if (g == 0) {
+            const uint64_t nm = leaf_mask | (static_cast<uint64_t>((x << 1) | 1) << (Q0 - E_LVL));
+            if (pv.bad0 || pv.bad1) report_breakdown(err, nm, 2 * (leaf_sel + __popc(x)) + (pv.bad0 ? 0 : 1));
+            tvals[E - 1 + x] = pv.tn;  // level e-1 t values live below index E-1: no hazard
         }
-        __syncwarp();
         PHASE_MARK(5 + 3 * (E_LVL - 1));
-        // pivot-row vectors u_j, w_j (j = 2..m-1) of every elimination.  Loops are
-        // branch-free (clamped item, predicated store) so unrolled iterations overlap.
-        constexpr int NV = E * (m - 2);
-        constexpr int NVI = (NV + 31) / 32;
+        // pivot-row vectors u_j, w_j (j = 2..m-1) of parent x
+        T* uwx = uwv + x * (2 * m + 1);  // odd stride: parents spread over the banks
         {
-            T s0v[NVI], s1v[NVI], r1v[NVI], u1v[NVI], r2v[NVI];
-            int xo[NVI];
+            constexpr int NVS = (m - 2 + G - 1) / G;
+            T a[NVS], b[NVS];
 #pragma unroll
-            for (int u = 0; u < NVI; ++u) {
-                const int it0 = lane + 32 * u;
-                const int it = it0 < NV ? it0 : NV - 1;
-                const int x = it / (m - 2);
-                const int j = 2 + it - x * (m - 2);
-                const T* pb = sm + desc[4 * x];
-                const int pd = desc[4 * x + 1], sr = desc[4 * x + 2];
-                s0v[u] = pb[tri_ix(pd, sr, sr + j)];
-                s1v[u] = pb[tri_ix(pd, sr + 1, sr + j)];
-                r1v[u] = piv[x];
-                u1v[u] = piv[16 + x];
-                r2v[u] = piv[32 + x];
-                xo[u] = x * 2 * m + j;
+            for (int s = 0; s < NVS; ++s) {
+                const int j = 2 + g + s * G;  // reads past row end stay inside the warp area
+                a[s] = P[j];
+                b[s] = P[m - 1 + j];
             }
 #pragma unroll
-            for (int u = 0; u < NVI; ++u) {
-                s0v[u] = A::mul(s0v[u], r1v[u]);
-                s1v[u] = A::mul(A::rank1s(s1v[u], u1v[u], s0v[u]), r2v[u]);
+            for (int s = 0; s < NVS; ++s) {
+                a[s] = A::mul(a[s], pv.r1);
+                b[s] = A::mul(A::rank1s(b[s], pv.u1, a[s]), pv.r2);
             }
 #pragma unroll
-            for (int u = 0; u < NVI; ++u)
-                if (lane + 32 * u < NV) {
-                    uwv[xo[u]] = s0v[u];
-                    uwv[xo[u] + m] = s1v[u];
+            for (int s = 0; s < NVS; ++s)
+                if (g + s * G < m - 2) {
+                    uwx[2 + g + s * G] = a[s];
+                    uwx[m + 2 + g + s * G] = b[s];
                 }
         }
         __syncwarp();
         PHASE_MARK(6 + 3 * (E_LVL - 1));
         if constexpr (Cfg<T>::TMEM && E_LVL == FAN) {
-            // last level -> TMEM: lane 2x+1 owns include child x, lane 2x the exclude child.
-            // The pair splits the include child's tn entries (2 each per chunk of 4); the
-            // even lane's results cross over by shuffle; every lane then stores its own
-            // node's chunk into its TMEM row.  The even lane's exclude state is the
-            // parent's trailing block, i.e. exactly the rank-2 inputs.
-            static_assert(tn % 4 == 0, "chunking");
-            const int x = lane >> 1, h = lane & 1;
-            const T* pb = sm + desc[4 * x];
-            const int pd = desc[4 * x + 1], sr = desc[4 * x + 2];
-            const T* uw = uwv + x * 2 * m;
-            const uint16_t* tab = tabs + WarpSmem<T>::tab_off(E_LVL);
+            // last level -> TMEM: lane 2x+1 owns include child x, lane 2x the exclude
+            // child (= parent x's trailing block Pt).  The pair splits the include
+            // child's entries (chunk c of 4: entries 4c+2h, 4c+2h+1 computed by lane
+            // h); the even lane's results cross over by shuffle.  Each lane stores its
+            // node's chunk to its TMEM row.
+            static_assert(tn % 4 == 0 && E == 16, "chunking");
+            const int xe = lane >> 1, h = lane & 1;
+            const T* Pt = sm + node_ref<T>(tabs, E_LVL - 1, xe).off + 2 * m - 1;
+            const T* sown = Pt + 2 * h;
+            const T* soth = Pt + 2 - 2 * h;
+            const T* uwe = uwv + xe * (2 * m + 1);
+            const uint32_t* tb = tabs + WarpSmem<T>::kLastTabOff + 2 * h;
             constexpr int NC = tn / 4;  // chunks of 4 entries (16 TMEM columns)
             constexpr int CB = 3;       // chunks per batch (loads of a batch issued together)
+            static_assert(NC % CB == 0, "batching");
 #pragma unroll 1
             for (int c0 = 0; c0 < NC; c0 += CB) {
-                T sv[CB][2], vv[CB][2];
+                T sv[CB][2], so[CB][2], vv[CB][2];
 #pragma unroll
                 for (int cc = 0; cc < CB; ++cc)
 #pragma unroll
                     for (int u = 0; u < 2; ++u) {
-                        const int c = c0 + cc < NC ? c0 + cc : NC - 1;
-                        const int ij = tab[4 * c + 2 * h + u];
-                        const int i = ij >> 8, j = ij & 0xff;
-                        sv[cc][u] = pb[tri_ix(pd, sr + 2 + i, sr + 2 + j)];
-                        vv[cc][u] = A::rank2(sv[cc][u], uw[2 + i], uw[2 + j], uw[m + 2 + i], uw[m + 2 + j]);
+                        const int k = 4 * (c0 + cc) + u;
+                        const uint32_t w = tb[k];
+                        const int i = static_cast<int>(w & 0xffffu), j = static_cast<int>(w >> 16);
+                        sv[cc][u] = sown[k];
+                        so[cc][u] = soth[k];
+                        vv[cc][u] = A::rank2(sv[cc][u], uwe[i], uwe[j], uwe[m + i], uwe[m + j]);
                     }
 #pragma unroll
                 for (int cc = 0; cc < CB; ++cc) {
-                    if (c0 + cc < NC) {
-                        T pv[2], ps[2];
+                    T y[2];
 #pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            pv[u] = shfl_xor_t(vv[cc][u], 1);
-                            ps[u] = shfl_xor_t(sv[cc][u], 1);
-                        }
-                        uint32_t r[16];
-                        if constexpr (sizeof(T) == sizeof(dd)) {
-                            // even lane: its exclude state's entries 4c..4c+3 (own inputs + partner's)
-                            // odd lane: its include state's entries (partner's results + own)
-                            dd_to_u32(h ? pv[0] : sv[cc][0], r + 0);
-                            dd_to_u32(h ? pv[1] : sv[cc][1], r + 4);
-                            dd_to_u32(h ? vv[cc][0] : ps[0], r + 8);
-                            dd_to_u32(h ? vv[cc][1] : ps[1], r + 12);
-                        }
-                        tm_st16(tm_row + 16 * (c0 + cc), r);
+                    for (int u = 0; u < 2; ++u) y[u] = shfl_xor_t(vv[cc][u], 1);
+                    uint32_t r[16];
+                    if constexpr (sizeof(T) == sizeof(dd)) {
+                        // even lane: exclude state entries 4c..4c+3 (own loads); odd: include
+                        dd_to_u32(h ? y[0] : sv[cc][0], r + 0);
+                        dd_to_u32(h ? y[1] : sv[cc][1], r + 4);
+                        dd_to_u32(h ? vv[cc][0] : so[cc][0], r + 8);
+                        dd_to_u32(h ? vv[cc][1] : so[cc][1], r + 12);
                     }
+                    tm_st16(tm_row + 16 * (c0 + cc), r);
                 }
             }
             tm_wait_st();
@@ -913,46 +920,38 @@ template <class T, int E_LVL> struct FanLevel {
             PHASE_MARK(7 + 3 * (E_LVL - 1));
             return;
         }
-        // trailing updates into the level-e buffers
-        T* lvl = sm + WarpSmem<T>::lvl_off(E_LVL);
-        const uint16_t* tab = tabs + WarpSmem<T>::tab_off(E_LVL);
+        // trailing updates into the level-e buffers: item it = lane + 32 s (x-major)
         constexpr int NE = E * tn;
         constexpr int NIT = (NE + 31) / 32;
-#ifndef TOR_UB
-#define TOR_UB 8
-#endif
         constexpr int UB = TOR_UB;  // items per batch: all loads of a batch precede its stores
+        const uint32_t* itb = tabs + WarpSmem<T>::item_off(E_LVL) + lane;
+        T* out = sm + WarpSmem<T>::lvl_off(E_LVL) + lane;
 #pragma unroll 1
         for (int s0 = 0; s0 < NIT; s0 += UB) {
             T sv[UB], ui[UB], uj[UB], wi[UB], wj[UB];
 #pragma unroll
             for (int u = 0; u < UB; ++u) {
-                const int it0 = lane + 32 * (s0 + u);
-                const int it = it0 < NE ? it0 : NE - 1;
-                const int x = it / tn;
-                const int k = it - x * tn;
-                const int ij = tab[k];
-                const int i = ij >> 8, j = ij & 0xff;
-                const T* pb = sm + desc[4 * x];
-                const int pd = desc[4 * x + 1], sr = desc[4 * x + 2];
-                const T* uw = uwv + x * 2 * m;
-                sv[u] = pb[tri_ix(pd, sr + 2 + i, sr + 2 + j)];
-                ui[u] = uw[2 + i];
-                uj[u] = uw[2 + j];
-                wi[u] = uw[m + 2 + i];
-                wj[u] = uw[m + 2 + j];
+                const int s = s0 + u;
+                const bool ok = s < NIT && (s < NIT - 1 || lane + 32 * s < NE);
+                const uint32_t w = ok ? itb[32 * s] : 0u;
+                const int src = static_cast<int>(w & 0x7ffu);
+                const int a = static_cast<int>((w >> 11) & 0x1ffu), b = static_cast<int>(w >> 20);
+                sv[u] = sm[src];
+                ui[u] = uwv[a];
+                uj[u] = uwv[b];
+                wi[u] = uwv[a + m];
+                wj[u] = uwv[b + m];
             }
 #pragma unroll
             for (int u = 0; u < UB; ++u) sv[u] = A::rank2(sv[u], ui[u], uj[u], wi[u], wj[u]);
 #pragma unroll
             for (int u = 0; u < UB; ++u) {
-                const int it0 = lane + 32 * (s0 + u);
-                if (it0 < NE && s0 + u < NIT) lvl[it0] = sv[u];
+                const int s = s0 + u;
+                if (s < NIT && (s < NIT - 1 || lane + 32 * s < NE)) out[32 * s] = sv[u];
             }
         }
         __syncwarp();
         PHASE_MARK(7 + 3 * (E_LVL - 1));
-        __syncwarp();
     }
 };
 
@@ -966,33 +965,53 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
     constexpr int Q0 = SM::Q0;
     constexpr int WPB = Cfg<T>::WPB;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint16_t* tabs = reinterpret_cast<uint16_t*>(smem_raw);
-    // block-wide (i,j) tables
-    for (int e = 0; e <= FAN; ++e) {
-        const int D = 2 * (Q0 - e);
+    uint32_t* tabs = reinterpret_cast<uint32_t*>(smem_raw);
+    // block-wide item tables of the fan-out levels (see WarpSmem)
+    for (int e = 1; e <= SM::kItemLevels; ++e) {
+        const int m = 2 * (Q0 - e + 1), D = m - 2, tn = tri_sz(D);
+        for (int it = threadIdx.x; it < (tn << (e - 1)); it += blockDim.x) {
+            const int x = it / tn;
+            int i = 0, r = it - x * tn;
+            while (r >= D - i) {
+                r -= D - i;
+                ++i;
+            }
+            const int src = node_off<T>(e - 1, x) + 2 * m - 1 + (it - x * tn);
+            const int ui = x * (2 * m + 1) + 2 + i, uj = x * (2 * m + 1) + 2 + i + r;
+            tabs[SM::item_off(e) + it] = static_cast<uint32_t>(src) | (static_cast<uint32_t>(ui) << 11) |
+                                         (static_cast<uint32_t>(uj) << 20);
+        }
+    }
+    for (int e = 0; e <= FAN; ++e)
+        for (int c = threadIdx.x; c < (1 << e); c += blockDim.x) tabs[SM::kNodeOff + (1 << e) - 1 + c] =
+                static_cast<uint32_t>(node_off<T>(e, c)) | (static_cast<uint32_t>(node_tix(e, c)) << 16);
+    if constexpr (Cfg<T>::TMEM) {
+        const int D = 2 * (Q0 - FAN);
         for (int k = threadIdx.x; k < tri_sz(D); k += blockDim.x) {
             int i = 0, r = k;
             while (r >= D - i) {
                 r -= D - i;
                 ++i;
             }
-            tabs[SM::tab_off(e) + k] = static_cast<uint16_t>((i << 8) | (i + r));
+            tabs[SM::kLastTabOff + k] = ij_word(i, i + r);
         }
     }
     __shared__ uint32_t tmem_base;
     uint32_t tm_row = 0;
     if constexpr (Cfg<T>::TMEM) {
-        static_assert(Cfg<T>::WPB == 4, "TMEM lane handoff needs one warp per TMEM lane quadrant");
+        // warp w uses TMEM lanes 32(w%4).. (its lane quadrant) and columns 256(w/4)..
+        static_assert(Cfg<T>::WPB == 4 || Cfg<T>::WPB == 8, "TMEM lane handoff: 4 or 8 warps per CTA");
+        constexpr uint32_t kCols = 64 * Cfg<T>::WPB;
         if ((threadIdx.x >> 5) == 0) {
             const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base));
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(dst), "r"(256)
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(dst), "r"(kCols)
                          : "memory");
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
         }
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        tm_row = tmem_base + (static_cast<uint32_t>(32 * ((threadIdx.x >> 5) & 3)) << 16);
+        tm_row = tmem_base + (static_cast<uint32_t>(32 * ((threadIdx.x >> 5) & 3)) << 16) + 256u * (threadIdx.x >> 7);
     } else {
         __syncthreads();
     }
@@ -1000,14 +1019,16 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
     const int lane = threadIdx.x & 31;
     unsigned char* wbase = smem_raw + SM::kTabBytes + wib * SM::kWarpBytes;
     T* sm = reinterpret_cast<T*>(wbase);
-    int* desc = reinterpret_cast<int*>(wbase + SM::kEntries * sizeof(T));
     T* tvals = sm + SM::kTOff;
-    T* piv = sm + SM::kPivOff;
     T* uwv = sm + SM::kUwOff;
     T* dfs_t = sm + SM::kDfsT;
     const int gw = blockIdx.x * WPB + wib;
     T* slots = scratch + static_cast<size_t>(gw) * scratch_stride;
     const int D = rjob - Q0;
+    // DFS slot s (state after the include at depth s-1, 2(rjob-s) rows) starts at entry
+    // sum_{x=1}^{s-1} tri(2(rjob-x)); lane s keeps that offset
+    int slot_off_l = 0;
+    for (int x = 1; x < lane && x <= D; ++x) slot_off_l += tri_sz(2 * (rjob - x));
 
     for (;;) {
         unsigned long long job = 0;
@@ -1026,78 +1047,67 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 const int kd = D - 1 - b;
                 const uint64_t above = leaf >> (b + 1);
                 const T* src;
-                int sd, ssk;
                 T st;
                 if (above == 0) {
-                    src = J.base;
-                    sd = J.dim;
-                    ssk = J.skip + kd;
+                    const int sk = 2 * (J.skip + kd);
+                    src = J.base + tri_ix(J.dim, sk, sk);
                     st = J.t;
                 } else {
                     const int tz = __ffsll(static_cast<long long>(above)) - 1;
                     const int s = kd - tz;  // slot index (depth after that include)
-                    size_t off = 0;
-                    for (int x = 1; x < s; ++x) off += tri_sz(2 * (rjob - x));
-                    src = slots + off;
-                    sd = 2 * (rjob - s);
-                    ssk = tz;
+                    src = slots + __shfl_sync(0xffffffffu, slot_off_l, s) + tri_ix(2 * (rjob - s), 2 * tz, 2 * tz);
                     st = dfs_t[s];
                 }
-                size_t doff = 0;
-                for (int x = 1; x < kd + 1; ++x) doff += tri_sz(2 * (rjob - x));
+                const int doff = __shfl_sync(0xffffffffu, slot_off_l, kd + 1);
                 const uint64_t lmask = J.mask | ((above << 1 | 1ull) << (rjob - kd - 1));
                 const int lsel = J.nsel + __popcll(above);
                 // the new slot kd+1 is re-read by later leaves only when b >= 1; its
                 // trailing Q0 modes are this leaf's root either way
-                dfs_elim<T, Q0>(src, sd, 2 * ssk, rjob - kd, slots + doff, b >= 1, sm, st, dfs_t + kd + 1, uwv,
-                                lmask, lsel, err);
+                dfs_elim<T, Q0>(src, rjob - kd, slots + doff, b >= 1, sm, st, dfs_t + kd + 1, uwv,
+                                g_ijtab + ijtab_off(rjob - kd - 1), lmask, lsel, err);
                 if (lane == 0) tvals[31] = dfs_t[kd + 1];
                 __syncwarp();
             }
             PHASE_MARK(0);
             if (leaf == 0) {
-                // first leaf: the root is the job state's trailing Q0 modes (HBM)
-                const T* lb = J.base;
-                const int ld = J.dim;
-                const int lsk = J.skip + D;
-                const T lt = J.t;
+                // first leaf: the root is the job state's trailing Q0 modes (HBM), a
+                // contiguous packed triangle
+                const int sk = 2 * (J.skip + D);
+                const T* lb = J.base + tri_ix(J.dim, sk, sk);
                 constexpr int RT = tri_sz(2 * Q0);
                 constexpr int RI = (RT + 31) / 32;
-                const int sr = 2 * lsk;
                 T rv[RI];
 #pragma unroll
                 for (int s = 0; s < RI; ++s) {
                     const int k0 = lane + 32 * s;
-                    const int ij = tabs[k0 < RT ? k0 : RT - 1];
-                    rv[s] = lb[tri_ix(ld, sr + (ij >> 8), sr + (ij & 0xff))];
+                    rv[s] = lb[k0 < RT ? k0 : RT - 1];
                 }
 #pragma unroll
                 for (int s = 0; s < RI; ++s)
                     if (lane + 32 * s < RT) sm[lane + 32 * s] = rv[s];
-                if (lane == 0) tvals[31] = lt;
+                if (lane == 0) tvals[31] = J.t;
             }
             __syncwarp();
             const uint64_t leaf_mask = J.mask | (leaf << Q0);
             const int leaf_sel = J.nsel + __popcll(leaf);
 
             PHASE_MARK(1);
-            FanLevel<T, 1>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err, tm_row);
-            FanLevel<T, 2>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err, tm_row);
-            FanLevel<T, 3>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err, tm_row);
-            FanLevel<T, 4>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err, tm_row);
-            FanLevel<T, 5>::run(sm, tvals, piv, uwv, desc, tabs, leaf_mask, leaf_sel, err, tm_row);
+            FanLevel<T, 1>::run(sm, tvals, uwv, tabs, leaf_mask, leaf_sel, err, tm_row);
+            FanLevel<T, 2>::run(sm, tvals, uwv, tabs, leaf_mask, leaf_sel, err, tm_row);
+            FanLevel<T, 3>::run(sm, tvals, uwv, tabs, leaf_mask, leaf_sel, err, tm_row);
+            FanLevel<T, 4>::run(sm, tvals, uwv, tabs, leaf_mask, leaf_sel, err, tm_row);
+            FanLevel<T, 5>::run(sm, tvals, uwv, tabs, leaf_mask, leaf_sel, err, tm_row);
 
             // lanes: node (FAN, lane)
             {
-                const T* vb;
-                int vd, vsk;
-                T vt;
-                lane_view<T, Q0>(sm, lane, vb, vd, vsk, vt, tvals, FAN);
-                const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(lane) << L);
-                const int lsel = leaf_sel + __popc(lane);
+                const int c = lane;
+                const NodeRef nr = node_ref<T>(tabs, FAN, c);
+                const T vt = tvals[nr.tix];
+                const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(c) << L);
+                const int lsel = leaf_sel + __popc(c);
                 const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
                 if constexpr (Cfg<T>::TMEM) lane_tree_tmem<T, L>(tm_row, vt, nodeneg, lmask, lsel, acc, err);
-                else lane_tree<T, L>(vb, vd, 2 * vsk, vt, nodeneg, lmask, lsel, acc, err);
+                else lane_tree<T, L>(sm + nr.off, 2 * L, 0, vt, nodeneg, lmask, lsel, acc, err);
                 acc.flush();
             }
             __syncwarp();
@@ -1120,7 +1130,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         __syncthreads();
         if ((threadIdx.x >> 5) == 0)
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(256)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(64 * Cfg<T>::WPB)
                          : "memory");
     }
 }
@@ -1223,6 +1233,24 @@ struct DevBuf {
     }
 };
 
+// (i,j) tables of the DFS eliminations, uploaded once per device
+int ensure_ijtab(int device, std::string& err) {
+    static std::mutex mu;
+    static bool done[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    if (device >= 0 && device < 64 && done[device]) return 0;
+    std::vector<uint32_t> h(kIjTabEntries);
+    for (int a = 1; a < kMaxJobModes; ++a) {
+        const int D = 2 * a;
+        int k = ijtab_off(a);
+        for (int i = 0; i < D; ++i)
+            for (int j = i; j < D; ++j) h[k++] = ij_word(i, j);
+    }
+    CK(cudaMemcpyToSymbol(g_ijtab, h.data(), sizeof(uint32_t) * h.size()));
+    if (device >= 0 && device < 64) done[device] = true;
+    return 0;
+}
+
 // A prepared evaluation: geometry chosen, device buffers allocated, the exact R of
 // every instance resident in HBM.  execute() runs the whole device pipeline
 // (prefix levels -> jobs -> subtree kernel -> fixed-order fold) and reads back
@@ -1244,6 +1272,7 @@ class PlanImpl final : public Plan {
         CK(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device));
         CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
         for (auto& e : ev_) CK(cudaEventCreate(&e));
+        if (const int st = ensure_ijtab(device, err)) return st;
 
         // prefix depth: enough jobs to fill the GPU, job states <= kMaxJobModes modes
         const uint64_t want_jobs = 16384;
@@ -1299,7 +1328,7 @@ class PlanImpl final : public Plan {
             // The occupancy API reports 1 CTA/SM for kernels that allocate TMEM; two 4-warp
             // CTAs (256 TMEM columns each = the SM's 512) fit by registers and shared memory
             // and do run concurrently (measured: 264 -> 173 ms at n=32 DD).
-            if (Cfg<T>::TMEM && 2 * (smem_ + 1024) <= 233472) bps = std::max(bps, 2);
+            if (Cfg<T>::TMEM && Cfg<T>::WPB == 4 && 2 * (smem_ + 1024) <= 233472) bps = std::max(bps, 2);
             if (const char* ov = std::getenv("TOR_BLOCKS_PER_SM")) bps = std::max(1, std::atoi(ov));
             if (std::getenv("TOR_DEBUG_TIMING")) {
                 cudaFuncAttributes fa;
