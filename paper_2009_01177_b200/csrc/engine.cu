@@ -616,8 +616,7 @@ __device__ __forceinline__ void tm_st16(uint32_t taddr, const uint32_t (&r)[16])
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
         "%14, %15, %16};\n" ::"r"(taddr),
         "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-        : "memory");
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
 }
 __device__ __forceinline__ void tm_ld4(uint32_t taddr, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
@@ -638,12 +637,6 @@ __device__ __forceinline__ dd u32_to_dd(uint32_t a, uint32_t b, uint32_t c, uint
     return dd{__hiloint2double(static_cast<int>(b), static_cast<int>(a)),
               __hiloint2double(static_cast<int>(d), static_cast<int>(c))};
 }
-// Loads entries [k0, k0+N) of this lane's TMEM state (issue only; tm_wait_ld before use).
-template <int N>
-__device__ __forceinline__ void tm_ld_entries(uint32_t row, int k0, uint32_t (&r)[4 * N]) {
-#pragma unroll
-    for (int u = 0; u < N; ++u) tm_ld4(row + 4 * (k0 + u), r[4 * u], r[4 * u + 1], r[4 * u + 2], r[4 * u + 3]);
-}
 
 // (row, col) of flat index k in a packed D-row upper triangle (compile-time)
 __host__ __device__ constexpr int tri_row(int D, int k) {
@@ -662,6 +655,48 @@ __host__ __device__ constexpr int tri_col(int D, int k) {
     }
     return i + k;
 }
+// TMEM column layout of a lane's level-FAN state (packed D = 2L row triangle, D = 8).
+// The level-FAN include child is formed by a lane pair (see FanLevel): entries with
+// i + j < D-1 ("A" set, 16 entries, row-major order A[0..15]) by the even lane,
+// their mirrors (D-1-j, D-1-i) by the odd lane, the 4 anti-diagonal entries
+// (n, D-1-n) by both.  TMEM slot 4c+p holds A[2c+p], slot 4c+2+p its mirror
+// (c < 8), slot 32+n anti-diagonal entry n.  Column of entry k = 4 * slot(k).
+constexpr int kMirD = 8;
+__host__ __device__ constexpr int mir_a_index(int i, int j) {  // index of (i,j) in A
+    int n = 0;
+    for (int a = 0; a < kMirD; ++a)
+        for (int b = a; b < kMirD; ++b)
+            if (a + b < kMirD - 1) {
+                if (a == i && b == j) return n;
+                ++n;
+            }
+    return -1;
+}
+__host__ __device__ constexpr int mir_a_row(int n) {
+    for (int a = 0; a < kMirD; ++a)
+        for (int b = a; b < kMirD; ++b)
+            if (a + b < kMirD - 1 && n-- == 0) return a;
+    return -1;
+}
+__host__ __device__ constexpr int mir_a_col(int n) {
+    for (int a = 0; a < kMirD; ++a)
+        for (int b = a; b < kMirD; ++b)
+            if (a + b < kMirD - 1 && n-- == 0) return b;
+    return -1;
+}
+__host__ __device__ constexpr int mir_slot(int k) {
+    const int i = tri_row(kMirD, k), j = tri_col(kMirD, k);
+    if (i + j == kMirD - 1) return 32 + i;
+    const int n = i + j < kMirD - 1 ? mir_a_index(i, j) : mir_a_index(kMirD - 1 - j, kMirD - 1 - i);
+    return 4 * (n >> 1) + (i + j < kMirD - 1 ? 0 : 2) + (n & 1);
+}
+// TMEM column of entry k of a D-row lane state
+template <int D>
+__host__ __device__ constexpr int tm_col(int k) {
+    if constexpr (D == kMirD) return 4 * mir_slot(k);
+    else return 4 * k;
+}
+
 // Rank-2 update of trailing entries [KB, KB+CNT) whose sources are in TMEM; the (i,j)
 // of every entry is a template constant so u/w/Sn stay in registers.
 template <class T, int M, int K, int END> struct LtUpd {
@@ -675,17 +710,31 @@ template <class T, int M, int K, int END> struct LtUpd {
         }
     }
 };
+// Loads entries [K0, K0+N) of this lane's D-row TMEM state (issue only; tm_wait_ld
+// before use).
+template <int D, int K, int N> struct TmLd {
+    __device__ __forceinline__ static void run(uint32_t row, uint32_t* r) {
+        if constexpr (N > 0) {
+            constexpr int col = tm_col<D>(K);
+            tm_ld4(row + col, r[0], r[1], r[2], r[3]);
+            TmLd<D, K + 1, N - 1>::run(row, r + 4);
+        }
+    }
+};
+template <int D, int K0, int N>
+__device__ __forceinline__ void tm_ld_entries(uint32_t row, uint32_t (&r)[4 * N]) {
+    TmLd<D, K0, N>::run(row, r);
+}
 template <class T, int M, int KB, int CNT>
-__device__ __forceinline__ void lt_wave(uint32_t base, const T (&u)[M], const T (&w)[M], St<T, M / 2 - 1>& Sn) {
+__device__ __forceinline__ void lt_wave(uint32_t row, const T (&u)[M], const T (&w)[M], St<T, M / 2 - 1>& Sn) {
     uint32_t rt[4 * CNT];
-#pragma unroll
-    for (int q = 0; q < CNT; ++q) tm_ld4(base + 4 * (KB + q), rt[4 * q], rt[4 * q + 1], rt[4 * q + 2], rt[4 * q + 3]);
+    tm_ld_entries<M, 2 * M - 1 + KB, CNT>(row, rt);
     tm_wait_ld();
     LtUpd<T, M, KB, KB + CNT>::run(rt, u, w, Sn);
 }
 
 // Lane subtree whose L-mode root state sits in this lane's TMEM row (entry k of the
-// packed 2L-row triangle at columns 4k..4k+3, DD words).  Same arithmetic as
+// packed 2L-row triangle at columns tm_col(k)..+3, DD words).  Same arithmetic as
 // lane_tree; only the source of the root entries differs.
 template <class T, int L>
 __device__ __forceinline__ void lane_tree_tmem(uint32_t row, const T& t, bool neg, uint64_t mask, int nsel,
@@ -701,7 +750,7 @@ __device__ __forceinline__ void lane_tree_tmem(uint32_t row, const T& t, bool ne
         T tn;
         if (br == 0) {
             uint32_t r0[4 * K01];
-            tm_ld_entries<K01>(row, 0, r0);
+            tm_ld_entries<M, 0, K01>(row, r0);
             tm_wait_ld();
             T e0[K01];
 #pragma unroll
@@ -719,13 +768,13 @@ __device__ __forceinline__ void lane_tree_tmem(uint32_t row, const T& t, bool ne
             // trailing block in two waves to bound live registers
             constexpr int NT = tri_sz(M - 2);
             constexpr int H = NT / 2;
-            lt_wave<T, M, 0, H>(row + 4 * K01, u, w, Sn);
-            lt_wave<T, M, H, NT - H>(row + 4 * K01, u, w, Sn);
+            lt_wave<T, M, 0, H>(row, u, w, Sn);
+            lt_wave<T, M, H, NT - H>(row, u, w, Sn);
             acc.add(tn, !neg, nsel + 1);
         } else {
             constexpr int NT = tri_sz(M - 2);
             uint32_t rt[4 * NT];
-            tm_ld_entries<NT>(row, K01, rt);
+            tm_ld_entries<M, K01, NT>(row, rt);
             tm_wait_ld();
 #pragma unroll
             for (int kk = 0; kk < NT; ++kk) Sn.e[kk] = u32_to_dd(rt[4 * kk], rt[4 * kk + 1], rt[4 * kk + 2], rt[4 * kk + 3]);
@@ -818,6 +867,36 @@ __device__ __forceinline__ NodeRef node_ref(const uint32_t* tabs, int e, int c) 
 // (x, g) = (lane % E, lane / E) works on parent x throughout (pivots redundantly in
 // registers, pivot-row vectors j = 2+g+sG, trailing entries k = g+sG, G = 32/E), so
 // every source, table and destination address is a per-lane base plus a constant.
+// Chunk C (< 8) of the mirror-split level-FAN update (see FanLevel): A entries
+// 2C, 2C+1 and their mirrors, all indices compile-time.
+template <class T, int M, int C> struct MirChunk {
+    __device__ __forceinline__ static void run(const T* Pt, const T (&u)[kMirD], const T (&w)[kMirD], int h,
+                                               uint32_t tm_row) {
+        if constexpr (C < 8) {
+            using A = Arith<T>;
+            constexpr int D = kMirD;
+            constexpr int i0 = mir_a_row(2 * C), j0 = mir_a_col(2 * C);
+            constexpr int i1 = mir_a_row(2 * C + 1), j1 = mir_a_col(2 * C + 1);
+            constexpr int kA0 = cix<D>(i0, j0), kB0 = cix<D>(D - 1 - j0, D - 1 - i0);
+            constexpr int kA1 = cix<D>(i1, j1), kB1 = cix<D>(D - 1 - j1, D - 1 - i1);
+            const T in0 = Pt[h ? kB0 : kA0], in1 = Pt[h ? kB1 : kA1];
+            const T sb0 = Pt[kB0], sb1 = Pt[kB1];
+            const T v0 = A::rank2(in0, u[i0], u[j0], w[i0], w[j0]);
+            const T v1 = A::rank2(in1, u[i1], u[j1], w[i1], w[j1]);
+            const T y0 = shfl_xor_t(v0, 1), y1 = shfl_xor_t(v1, 1);
+            uint32_t r[16];
+            if constexpr (sizeof(T) == sizeof(dd)) {
+                dd_to_u32(h ? y0 : in0, r + 0);
+                dd_to_u32(h ? y1 : in1, r + 4);
+                dd_to_u32(h ? v0 : sb0, r + 8);
+                dd_to_u32(h ? v1 : sb1, r + 12);
+            }
+            tm_st16(tm_row + 16 * C, r);
+            MirChunk<T, M, C + 1>::run(Pt, u, w, h, tm_row);
+        }
+    }
+};
+
 #ifndef TOR_UB
 #define TOR_UB 8
 #endif
@@ -872,48 +951,33 @@ template <class T, int E_LVL> struct FanLevel {
         if constexpr (Cfg<T>::TMEM && E_LVL == FAN) {
             // last level -> TMEM: lane 2x+1 owns include child x, lane 2x the exclude
             // child (= parent x's trailing block Pt).  The pair splits the include
-            // child's entries (chunk c of 4: entries 4c+2h, 4c+2h+1 computed by lane
-            // h); the even lane's results cross over by shuffle.  Each lane stores its
-            // node's chunk to its TMEM row.
-            static_assert(tn % 4 == 0 && E == 16, "chunking");
+            // child's entries by the mirror (i,j) -> (7-j,7-i): the even lane forms the
+            // "A" entries (i+j < 7) with u, w in registers, the odd lane the mirrors
+            // with the vectors held reversed -- the same register indices, so (i,j) are
+            // compile-time for both.  The 4 self-mirror entries are formed by both (the
+            // odd lane keeps them).  Even-lane results cross over by shuffle; each lane
+            // stores its node's state to its TMEM row in mir_slot order.
+            static_assert(dn == kMirD && tn == 36 && E == 16, "mirror split layout");
             const int xe = lane >> 1, h = lane & 1;
             const T* Pt = sm + node_ref<T>(tabs, E_LVL - 1, xe).off + 2 * m - 1;
-            const T* sown = Pt + 2 * h;
-            const T* soth = Pt + 2 - 2 * h;
             const T* uwe = uwv + xe * (2 * m + 1);
-            const uint32_t* tb = tabs + WarpSmem<T>::kLastTabOff + 2 * h;
-            constexpr int NC = tn / 4;  // chunks of 4 entries (16 TMEM columns)
-            constexpr int CB = 3;       // chunks per batch (loads of a batch issued together)
-            static_assert(NC % CB == 0, "batching");
-#pragma unroll 1
-            for (int c0 = 0; c0 < NC; c0 += CB) {
-                T sv[CB][2], so[CB][2], vv[CB][2];
+            T u[dn], w[dn];
 #pragma unroll
-                for (int cc = 0; cc < CB; ++cc)
+            for (int k = 0; k < dn; ++k) {
+                const int kk = 2 + (h ? dn - 1 - k : k);
+                u[k] = uwe[kk];
+                w[k] = uwe[m + kk];
+            }
+            MirChunk<T, m, 0>::run(Pt, u, w, h, tm_row);
+            {
+                uint32_t r[16];
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int k = 4 * (c0 + cc) + u;
-                        const uint32_t w = tb[k];
-                        const int i = static_cast<int>(w & 0xffffu), j = static_cast<int>(w >> 16);
-                        sv[cc][u] = sown[k];
-                        so[cc][u] = soth[k];
-                        vv[cc][u] = A::rank2(sv[cc][u], uwe[i], uwe[j], uwe[m + i], uwe[m + j]);
-                    }
-#pragma unroll
-                for (int cc = 0; cc < CB; ++cc) {
-                    T y[2];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) y[u] = shfl_xor_t(vv[cc][u], 1);
-                    uint32_t r[16];
-                    if constexpr (sizeof(T) == sizeof(dd)) {
-                        // even lane: exclude state entries 4c..4c+3 (own loads); odd: include
-                        dd_to_u32(h ? y[0] : sv[cc][0], r + 0);
-                        dd_to_u32(h ? y[1] : sv[cc][1], r + 4);
-                        dd_to_u32(h ? vv[cc][0] : so[cc][0], r + 8);
-                        dd_to_u32(h ? vv[cc][1] : so[cc][1], r + 12);
-                    }
-                    tm_st16(tm_row + 16 * (c0 + cc), r);
+                for (int a = 0; a < 4; ++a) {
+                    const T sv = Pt[cix<dn>(a, dn - 1 - a)];
+                    const T v = A::rank2(sv, u[dn - 1 - a], u[a], w[dn - 1 - a], w[a]);
+                    if constexpr (sizeof(T) == sizeof(dd)) dd_to_u32(h ? v : sv, r + 4 * a);
                 }
+                tm_st16(tm_row + 16 * 8, r);
             }
             tm_wait_st();
             __syncwarp();
