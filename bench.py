@@ -258,10 +258,13 @@ def main():
     e2e_step = statistics.median(e2e_ms)
 
     if rank == 0:
-        sass = json.load(open(os.path.join(ROOT, "profiles", "sass_counts.json"))) \
-            if os.path.exists(os.path.join(ROOT, "profiles", "sass_counts.json")) else {}
-        fpt = sass.get("flops_per_term", {}).get(dtype)
-        ipt = sass.get(dtype, {}).get("fp64_instr")
+        def _load(name):
+            path = os.path.join(ROOT, "profiles", name)
+            return json.load(open(path)) if os.path.exists(path) else {}
+        fmodel = _load("flops_model.json").get("per_term", {}).get(dtype, {}).get(str(n), {})
+        sass = _load("sass_counts.json")
+        fpt = fmodel.get("flops")          # algorithmic flops / term (SASS-pinned primitive model)
+        ipt = fmodel.get("fp64_instr")
         roof = None
         if fpt and peak:
             terms_rank = terms_total / world
@@ -269,13 +272,21 @@ def main():
             roof = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": sass.get("dram_bytes_per_launch", {}).get(dtype),
                     "kernel": "subtree_kernel", "flops_per_term": fpt,
-                    "flops_per_term_source": "profiles/sass_counts.json (ncu executed DFMA*2+DADD+DMUL / terms)",
+                    "flops_per_term_source": "profiles/flops_model.json: Schur-tree node counts x SASS-pinned "
+                                             "primitive costs (tools/flops_model.py), useful work only",
+                    "kappa": fmodel.get("kappa"), "rho": fmodel.get("rho_leaf_bundle_flops"),
                     "peak_source": peak_src}
             if ipt:
                 # FP64 pipe issue utilisation: DD arithmetic is DADD-heavy, so the flop
                 # fraction caps well below 1 even at a saturated pipe (peak = 2 flops/instr)
                 roof["fp64_instr_per_term"] = ipt
                 roof["fp64_pipe_frac"] = terms_rank * ipt / (kstep_ms * 1e-3) / (peak * 1e12 / 2)
+            ex = sass.get("flops_per_term", {}).get(dtype)
+            if ex:
+                # cross-check: ncu executed (includes lanes that compute warp-uniform pivots
+                # redundantly and padding items)
+                roof["executed_flops_per_term_ncu"] = ex
+                roof["executed_over_algorithmic"] = ex / fpt
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             try:

@@ -169,30 +169,6 @@ template <> __device__ __forceinline__ void warp_fold<double>(Acc<double>& a) {
     }
 }
 
-// Pivot chain of one mode elimination (rows 0,1 of the view): Cholesky pivots
-// rho1 = 1/sqrt(s00) and rho2 = 1/sqrt(s11 - s01^2/s00), computed as
-// rho2 = sqrt(s00) * rhod with rhod = 1/sqrt(det2), det2 = s00 s11 - s01^2, so the
-// two reciprocal square roots are independent (half the dependent latency of the
-// textbook chain); the child's term factor is t * rhod.
-template <class T> struct Piv {
-    T r1, u1, r2, tn;
-    bool bad0, bad1;
-};
-template <class T>
-__device__ __forceinline__ Piv<T> pivot2(const T& s00, const T& s01, const T& s11, const T& t) {
-    using A = Arith<T>;
-    Piv<T> p;
-    const T a = A::norm(s00);
-    p.bad0 = nonpositive(A::hi(a));
-    p.r1 = A::rsqrt(a);
-    const T det = A::norm(A::rank1(A::mul(a, s11), s01, s01));
-    p.bad1 = nonpositive(A::hi(det));
-    const T rd = A::rsqrt(det);
-    p.u1 = A::mul(s01, p.r1);
-    p.r2 = A::mul(A::mul(a, p.r1), rd);
-    p.tn = A::mul(t, rd);
-    return p;
-}
 
 
 // ------------------------------------------------ warp-cooperative elimination --
