@@ -203,6 +203,10 @@ void tor_plan_destroy(tor_plan* plan);
 /* Number of CUDA devices visible (0 without a GPU). */
 int tor_device_count(void);
 
+/* Frees the device memory the library keeps pooled between calls (plans reuse the
+ * prefix pools / DFS scratch of finished calls; no reference counterpart). */
+void tor_release_device_cache(void);
+
 #ifdef __cplusplus
 }
 #endif

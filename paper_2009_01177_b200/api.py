@@ -62,7 +62,8 @@ class TorPartial(C.Structure):
 EXPORTS = ("tor_abi_version", "tor_check_symmetries", "tor_check_dense", "tor_det_i_minus_a",
            "tor_select_precision", "tor_force_width", "tor_torontonian", "tor_torontonian_reference",
            "tor_torontonian_batch", "tor_torontonian_slice", "tor_torontonian_shard", "tor_fold_partials",
-           "tor_probability", "tor_device_count", "tor_plan_create", "tor_plan_execute", "tor_plan_destroy")
+           "tor_probability", "tor_device_count", "tor_plan_create", "tor_plan_execute", "tor_plan_destroy",
+           "tor_release_device_cache")
 
 _lib = None
 
@@ -96,6 +97,8 @@ def lib():
         L.tor_plan_execute.argtypes = [C.c_void_p, P(TorResult), P(TorError)]
         L.tor_plan_destroy.argtypes = [C.c_void_p]
         L.tor_plan_destroy.restype = None
+        L.tor_release_device_cache.argtypes = []
+        L.tor_release_device_cache.restype = None
         _lib = L
     return _lib
 
@@ -326,3 +329,8 @@ class Plan:
 
 def device_count() -> int:
     return lib().tor_device_count()
+
+
+def release_device_cache() -> None:
+    """Free the device memory pooled between calls (tor_release_device_cache)."""
+    lib().tor_release_device_cache()

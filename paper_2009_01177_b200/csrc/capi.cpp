@@ -211,6 +211,8 @@ int tor_device_count(void) {
     return c;
 }
 
+void tor_release_device_cache(void) { release_device_cache(); }
+
 int tor_check_symmetries(const tor_input* in, double devs[3], int* pass, tor_error* err) {
     try {
         clear_err(err);

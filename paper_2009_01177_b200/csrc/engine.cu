@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -1263,13 +1264,64 @@ __global__ void fold_kernel(double* partials, uint64_t per) {
         }                                                                             \
     } while (0)
 
+// Process-wide cache of device allocations: plans are created per call (the C ABI
+// is stateless), and cudaMalloc/cudaFree of the tens of MB of prefix pools and DFS
+// scratch would otherwise cost milliseconds per call.  Blocks are reused when their
+// capacity is within 2x of the request; tor_release_device_cache() frees them.
+struct DevPool {
+    static constexpr size_t kMaxPooled = size_t(8) << 30;  // per device
+    std::mutex mu;
+    std::multimap<size_t, void*> free_blocks[64];
+    size_t pooled[64] = {};
+    static DevPool& get() {
+        static DevPool pool;
+        return pool;
+    }
+};
 struct DevBuf {
     void* p = nullptr;
+    size_t cap = 0;
+    int dev = -1;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
+    cudaError_t alloc(size_t bytes, int device) {
+        bytes = std::max<size_t>(bytes, 256);
+        if (device >= 0 && device < 64) {
+            DevPool& pl = DevPool::get();
+            std::lock_guard<std::mutex> lk(pl.mu);
+            auto& fb = pl.free_blocks[device];
+            auto it = fb.lower_bound(bytes);
+            if (it != fb.end() && it->first <= 2 * bytes) {
+                p = it->second;
+                cap = it->first;
+                dev = device;
+                pl.pooled[device] -= cap;
+                fb.erase(it);
+                return cudaSuccess;
+            }
+        }
+        const cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) {
+            cap = bytes;
+            dev = device;
+        } else {
+            p = nullptr;
+        }
+        return e;
+    }
     ~DevBuf() {
-        if (p) cudaFree(p);
+        if (!p) return;
+        if (dev >= 0 && dev < 64) {
+            DevPool& pl = DevPool::get();
+            std::lock_guard<std::mutex> lk(pl.mu);
+            if (pl.pooled[dev] + cap <= DevPool::kMaxPooled) {
+                pl.free_blocks[dev].emplace(cap, p);
+                pl.pooled[dev] += cap;
+                return;
+            }
+        }
+        cudaFree(p);
     }
 };
 
@@ -1342,15 +1394,15 @@ class PlanImpl final : public Plan {
         g_.inst_entries = o;
         g_.inst_ts = std::max<size_t>(to, 1);
 
-        CK(cudaMalloc(&pool_.p, sizeof(T) * g_.inst_entries * ninst_));
-        CK(cudaMalloc(&tpool_.p, sizeof(T) * g_.inst_ts * ninst_));
-        CK(cudaMalloc(&jobs_.p, sizeof(Job<T>) * njobs_));
-        CK(cudaMalloc(&parts_.p, sizeof(double) * 5 * njobs_));
-        CK(cudaMalloc(&errw_.p, sizeof(unsigned long long)));
-        CK(cudaMalloc(&ctr_.p, sizeof(unsigned long long)));
+        CK(pool_.alloc(sizeof(T) * g_.inst_entries * ninst_, device_));
+        CK(tpool_.alloc(sizeof(T) * g_.inst_ts * ninst_, device_));
+        CK(jobs_.alloc(sizeof(Job<T>) * njobs_, device_));
+        CK(parts_.alloc(sizeof(double) * 5 * njobs_, device_));
+        CK(errw_.alloc(sizeof(unsigned long long), device_));
+        CK(ctr_.alloc(sizeof(unsigned long long), device_));
         if (!use_levels_) {
             work_stride_ = 2 * static_cast<size_t>(tri_sz(2 * n_));
-            CK(cudaMalloc(&work_.p, sizeof(T) * work_stride_ * njobs_));
+            CK(work_.alloc(sizeof(T) * work_stride_ * njobs_, device_));
         }
         if (rjob_ >= Q0) {
             using SM = WarpSmem<T>;
@@ -1391,7 +1443,7 @@ class PlanImpl final : public Plan {
             size_t stride = 0;
             for (int x = 1; x <= D; ++x) stride += tri_sz(2 * (rjob_ - x));
             scr_stride_ = std::max<size_t>(stride, 1);
-            CK(cudaMalloc(&scr_.p, sizeof(T) * scr_stride_ * blocks_ * WPB));
+            CK(scr_.alloc(sizeof(T) * scr_stride_ * blocks_ * WPB, device_));
         }
         // resident inputs: the exact R of every instance
         std::vector<T> host(static_cast<size_t>(tri_sz(2 * n_)));
@@ -1551,6 +1603,21 @@ int make_plan(int device, const std::vector<PreparedInput>& inputs, const WorkRa
 
 }  // namespace
 
+void release_device_cache() {
+    DevPool& pl = DevPool::get();
+    std::lock_guard<std::mutex> lk(pl.mu);
+    for (int d = 0; d < 64; ++d) {
+        if (pl.free_blocks[d].empty()) continue;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(d);
+        for (auto& kv : pl.free_blocks[d]) cudaFree(kv.second);
+        pl.free_blocks[d].clear();
+        pl.pooled[d] = 0;
+        cudaSetDevice(cur);
+    }
+}
+
 int engine_tree_min_n(int mode) {
     return mode == MODE_QD ? Cfg<qd>::L + FAN : Cfg<dd>::L + FAN;
 }
@@ -1582,10 +1649,19 @@ int engine_run(int device, int mode, const std::vector<PreparedInput>& inputs, c
         return 0;
     }
     Plan* p = nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     const int st = plan_create(device, mode, inputs, range, &p, err);
     if (st != 0) return st;
+    const auto t1 = std::chrono::steady_clock::now();
     const int rs = p->execute(out, stats, err);
+    const auto t2 = std::chrono::steady_clock::now();
     delete p;
+    if (std::getenv("TOR_DEBUG_TIMING")) {
+        const auto t3 = std::chrono::steady_clock::now();
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "[tor] engine_run: plan_create %.3f ms, execute %.3f ms, destroy %.3f ms\n", ms(t0, t1),
+                     ms(t1, t2), ms(t2, t3));
+    }
     return rs;
 }
 

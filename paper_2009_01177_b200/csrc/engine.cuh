@@ -90,5 +90,6 @@ int fixed_run(int device, int width_bits, int n, const double* a00, const double
 
 // Minimum instance size handled by the tree kernel; smaller n uses the direct path.
 int engine_tree_min_n(int mode);
+void release_device_cache();  // frees the pooled device allocations of finished plans
 
 }  // namespace tor
