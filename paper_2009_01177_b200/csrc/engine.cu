@@ -73,6 +73,7 @@ template <> struct Cfg<double> {
     static constexpr int WPB = 4;
     static constexpr int MINB = 1;
     static constexpr bool TMEM = false;
+    static constexpr bool WS = false;
 };
 template <> struct Cfg<dd> {
     static constexpr int L = 4;
@@ -85,12 +86,19 @@ template <> struct Cfg<dd> {
 #endif
     static constexpr int MINB = (TOR_DD_TMEM && WPB == 4) ? 2 : 1;
     static constexpr bool TMEM = TOR_DD_TMEM;
+#ifndef TOR_DD_WS
+#define TOR_DD_WS 1
+#endif
+    // warp specialisation: warps 0-3 run the DFS + fan-out (producers), warps 4-7 the
+    // lane subtrees (consumers) of the same TMEM lane quadrant, double-buffered in TMEM
+    static constexpr bool WS = TOR_DD_TMEM && WPB == 8 && TOR_DD_WS;
 };
 template <> struct Cfg<qd> {
     static constexpr int L = 3;
     static constexpr int WPB = 1;
     static constexpr int MINB = 1;
     static constexpr bool TMEM = false;
+    static constexpr bool WS = false;
 };
 
 template <class T> constexpr int root_modes() { return Cfg<T>::L + FAN; }
@@ -1058,102 +1066,87 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
     }
     const int wib = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    unsigned char* wbase = smem_raw + SM::kTabBytes + wib * SM::kWarpBytes;
-    T* sm = reinterpret_cast<T*>(wbase);
-    T* tvals = sm + SM::kTOff;
-    T* uwv = sm + SM::kUwOff;
-    T* dfs_t = sm + SM::kDfsT;
-    const int gw = blockIdx.x * WPB + wib;
-    T* slots = scratch + static_cast<size_t>(gw) * scratch_stride;
     const int D = rjob - Q0;
     // DFS slot s (state after the include at depth s-1, 2(rjob-s) rows) starts at entry
     // sum_{x=1}^{s-1} tri(2(rjob-x)); lane s keeps that offset
     int slot_off_l = 0;
     for (int x = 1; x < lane && x <= D; ++x) slot_off_l += tri_sz(2 * (rjob - x));
+    // Warp areas.  Unspecialised: warp w owns area w.  Warp-specialised: the pair
+    // (producer p, consumer p+4) owns areas 2p and 2p+1; their fan-out buffers and t
+    // values alternate between leaves (slot = leaf parity), the pivot-row vectors of
+    // area 2p are the producer's, those of area 2p+1 the consumer's (level FAN).
+    const int pw = Cfg<T>::WS ? (wib & 3) : wib;
+    const int ppb = Cfg<T>::WS ? 4 : WPB;  // producers per block
+    auto area = [&](int a) { return reinterpret_cast<T*>(smem_raw + SM::kTabBytes + a * SM::kWarpBytes); };
+    T* sm = area(Cfg<T>::WS ? 2 * pw : pw);
+    T* tvals = sm + SM::kTOff;
+    T* uwv = sm + SM::kUwOff;
+    T* dfs_t = sm + SM::kDfsT;
+    T* slots = scratch + static_cast<size_t>(blockIdx.x * ppb + pw) * scratch_stride;
 
-    for (;;) {
-        unsigned long long job = 0;
-        if (lane == 0) job = atomicAdd(job_counter, 1ull);
-        job = __shfl_sync(0xffffffffu, job, 0);
-        if (job >= njobs) break;
-        const Job<T> J = jobs[job];
-        Acc<T> acc;
-        acc.sc = tsc;
-
-        for (uint64_t leaf = 0; leaf < (1ull << D); ++leaf) {
-            PHASE_T0();
-            if (leaf > 0) {
-                // flip exclude->include at depth kd (lowest set bit of leaf)
-                const int b = __ffsll(static_cast<long long>(leaf)) - 1;
-                const int kd = D - 1 - b;
-                const uint64_t above = leaf >> (b + 1);
-                const T* src;
-                T st;
-                if (above == 0) {
-                    const int sk = 2 * (J.skip + kd);
-                    src = J.base + tri_ix(J.dim, sk, sk);
-                    st = J.t;
-                } else {
-                    const int tz = __ffsll(static_cast<long long>(above)) - 1;
-                    const int s = kd - tz;  // slot index (depth after that include)
-                    src = slots + __shfl_sync(0xffffffffu, slot_off_l, s) + tri_ix(2 * (rjob - s), 2 * tz, 2 * tz);
-                    st = dfs_t[s];
-                }
-                const int doff = __shfl_sync(0xffffffffu, slot_off_l, kd + 1);
-                const uint64_t lmask = J.mask | ((above << 1 | 1ull) << (rjob - kd - 1));
-                const int lsel = J.nsel + __popcll(above);
-                // the new slot kd+1 is re-read by later leaves only when b >= 1; its
-                // trailing Q0 modes are this leaf's root either way
-                dfs_elim<T, Q0>(src, rjob - kd, slots + doff, b >= 1, sm, st, dfs_t + kd + 1, uwv,
-                                g_ijtab + ijtab_off(rjob - kd - 1), lmask, lsel, err);
-                if (lane == 0) tvals[31] = dfs_t[kd + 1];
-                __syncwarp();
+    // DFS step + root + fan-out of one leaf of job J into the fan area fsm (buffers +
+    // t values): all FAN levels, or (warp-specialised) levels 1..FAN-1 -- the level-FAN
+    // states in shared memory, or in TMEM at tm_slot for the TMEM types
+    auto produce_leaf = [&](const Job<T>& J, uint64_t leaf, uint32_t tm_slot, T* fsm) {
+        T* ftv = fsm + SM::kTOff;
+        PHASE_T0();
+        if (leaf > 0) {
+            // flip exclude->include at depth kd (lowest set bit of leaf)
+            const int b = __ffsll(static_cast<long long>(leaf)) - 1;
+            const int kd = D - 1 - b;
+            const uint64_t above = leaf >> (b + 1);
+            const T* src;
+            T st;
+            if (above == 0) {
+                const int sk = 2 * (J.skip + kd);
+                src = J.base + tri_ix(J.dim, sk, sk);
+                st = J.t;
+            } else {
+                const int tz = __ffsll(static_cast<long long>(above)) - 1;
+                const int s = kd - tz;  // slot index (depth after that include)
+                src = slots + __shfl_sync(0xffffffffu, slot_off_l, s) + tri_ix(2 * (rjob - s), 2 * tz, 2 * tz);
+                st = dfs_t[s];
             }
-            PHASE_MARK(0);
-            if (leaf == 0) {
-                // first leaf: the root is the job state's trailing Q0 modes (HBM), a
-                // contiguous packed triangle
-                const int sk = 2 * (J.skip + D);
-                const T* lb = J.base + tri_ix(J.dim, sk, sk);
-                constexpr int RT = tri_sz(2 * Q0);
-                constexpr int RI = (RT + 31) / 32;
-                T rv[RI];
-#pragma unroll
-                for (int s = 0; s < RI; ++s) {
-                    const int k0 = lane + 32 * s;
-                    rv[s] = lb[k0 < RT ? k0 : RT - 1];
-                }
-#pragma unroll
-                for (int s = 0; s < RI; ++s)
-                    if (lane + 32 * s < RT) sm[lane + 32 * s] = rv[s];
-                if (lane == 0) tvals[31] = J.t;
-            }
+            const int doff = __shfl_sync(0xffffffffu, slot_off_l, kd + 1);
+            const uint64_t lmask = J.mask | ((above << 1 | 1ull) << (rjob - kd - 1));
+            const int lsel = J.nsel + __popcll(above);
+            // the new slot kd+1 is re-read by later leaves only when b >= 1; its
+            // trailing Q0 modes are this leaf's root either way
+            dfs_elim<T, Q0>(src, rjob - kd, slots + doff, b >= 1, fsm, st, dfs_t + kd + 1, uwv,
+                            g_ijtab + ijtab_off(rjob - kd - 1), lmask, lsel, err);
+            if (lane == 0) ftv[31] = dfs_t[kd + 1];
             __syncwarp();
-            const uint64_t leaf_mask = J.mask | (leaf << Q0);
-            const int leaf_sel = J.nsel + __popcll(leaf);
-
-            PHASE_MARK(1);
-            FanLevel<T, 1>::run(sm, tvals, uwv, tabs, leaf_mask, leaf_sel, err, tm_row);
-            FanLevel<T, 2>::run(sm, tvals, uwv, tabs, leaf_mask, leaf_sel, err, tm_row);
-            FanLevel<T, 3>::run(sm, tvals, uwv, tabs, leaf_mask, leaf_sel, err, tm_row);
-            FanLevel<T, 4>::run(sm, tvals, uwv, tabs, leaf_mask, leaf_sel, err, tm_row);
-            FanLevel<T, 5>::run(sm, tvals, uwv, tabs, leaf_mask, leaf_sel, err, tm_row);
-
-            // lanes: node (FAN, lane)
-            {
-                const int c = lane;
-                const NodeRef nr = node_ref<T>(tabs, FAN, c);
-                const T vt = tvals[nr.tix];
-                const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(c) << L);
-                const int lsel = leaf_sel + __popc(c);
-                const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
-                if constexpr (Cfg<T>::TMEM) lane_tree_tmem<T, L>(tm_row, vt, nodeneg, lmask, lsel, acc, err);
-                else lane_tree<T, L>(sm + nr.off, 2 * L, 0, vt, nodeneg, lmask, lsel, acc, err);
-                acc.flush();
-            }
-            __syncwarp();
-            PHASE_MARK(4);
         }
+        PHASE_MARK(0);
+        if (leaf == 0) {
+            // first leaf: the root is the job state's trailing Q0 modes (HBM), a
+            // contiguous packed triangle
+            const int sk = 2 * (J.skip + D);
+            const T* lb = J.base + tri_ix(J.dim, sk, sk);
+            constexpr int RT = tri_sz(2 * Q0);
+            constexpr int RI = (RT + 31) / 32;
+            T rv[RI];
+#pragma unroll
+            for (int s = 0; s < RI; ++s) {
+                const int k0 = lane + 32 * s;
+                rv[s] = lb[k0 < RT ? k0 : RT - 1];
+            }
+#pragma unroll
+            for (int s = 0; s < RI; ++s)
+                if (lane + 32 * s < RT) fsm[lane + 32 * s] = rv[s];
+            if (lane == 0) ftv[31] = J.t;
+        }
+        __syncwarp();
+        const uint64_t leaf_mask = J.mask | (leaf << Q0);
+        const int leaf_sel = J.nsel + __popcll(leaf);
+        PHASE_MARK(1);
+        FanLevel<T, 1>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
+        FanLevel<T, 2>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
+        FanLevel<T, 3>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
+        FanLevel<T, 4>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
+        if constexpr (!Cfg<T>::WS) FanLevel<T, 5>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
+    };
+    auto write_partial = [&](Acc<T>& acc, unsigned long long job) {
         warp_fold<T>(acc);
         if (lane == 0) {
             double w[4];
@@ -1166,6 +1159,104 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
             o[4] = acc.abs_sum;
         }
         __syncwarp();
+    };
+
+    if constexpr (Cfg<T>::WS) {
+        // ---- warp-specialised: producer warp p (0-3) runs the DFS and fan-out levels
+        // 1..FAN-1 of leaf i into fan area 2p + (i & 1); consumer warp p+4 runs level FAN
+        // (into its TMEM lane quadrant) and the lane subtrees from that area.  One named
+        // barrier per leaf hands area i to the consumer and area i-1 back to the producer.
+        struct WsMeta {
+            unsigned long long mask;
+            unsigned long long job;
+            int sel, flags;  // 1: last leaf of the job, 2: no more leaves
+        };
+        __shared__ WsMeta meta[4][2];
+        const int pair = wib & 3;
+        auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;\n" ::"r"(1 + pair) : "memory"); };
+        int slot = 0;
+        if (wib < 4) {
+            for (;;) {
+                unsigned long long job = 0;
+                if (lane == 0) job = atomicAdd(job_counter, 1ull);
+                job = __shfl_sync(0xffffffffu, job, 0);
+                if (job >= njobs) break;
+                const Job<T> J = jobs[job];
+                for (uint64_t leaf = 0; leaf < (1ull << D); ++leaf) {
+                    produce_leaf(J, leaf, 0u, area(2 * pair + slot));
+                    if (lane == 0) {
+                        meta[pair][slot].mask = J.mask | (leaf << Q0);
+                        meta[pair][slot].job = job;
+                        meta[pair][slot].sel = J.nsel + __popcll(leaf);
+                        meta[pair][slot].flags = leaf + 1 == (1ull << D) ? 1 : 0;
+                    }
+                    __syncwarp();
+                    pair_sync();
+                    slot ^= 1;
+                }
+            }
+            if (lane == 0) meta[pair][slot].flags = 2;
+            __syncwarp();
+            pair_sync();
+        } else {
+            const uint32_t crow = tmem_base + ((32u * pair) << 16);
+            T* cuw = area(2 * pair + 1) + SM::kUwOff;  // the consumer's pivot-row vectors
+            Acc<T> acc;
+            acc.sc = tsc;
+            for (;;) {
+                pair_sync();
+                const unsigned long long leaf_mask = meta[pair][slot].mask;
+                const unsigned long long job = meta[pair][slot].job;
+                const int leaf_sel = meta[pair][slot].sel, flags = meta[pair][slot].flags;
+                if (flags & 2) break;
+                T* fsm = area(2 * pair + slot);
+                T* ftv = fsm + SM::kTOff;
+                FanLevel<T, FAN>::run(fsm, ftv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
+                const int c = lane;
+                const T vt = ftv[node_ref<T>(tabs, FAN, c).tix];
+                const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(c) << L);
+                const int lsel = leaf_sel + __popc(c);
+                const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
+                lane_tree_tmem<T, L>(crow, vt, nodeneg, lmask, lsel, acc, err);
+                acc.flush();
+                if (flags & 1) {
+                    write_partial(acc, job);
+                    acc = Acc<T>();
+                    acc.sc = tsc;
+                }
+                __syncwarp();
+                slot ^= 1;
+            }
+        }
+    } else {
+        for (;;) {
+            unsigned long long job = 0;
+            if (lane == 0) job = atomicAdd(job_counter, 1ull);
+            job = __shfl_sync(0xffffffffu, job, 0);
+            if (job >= njobs) break;
+            const Job<T> J = jobs[job];
+            Acc<T> acc;
+            acc.sc = tsc;
+            for (uint64_t leaf = 0; leaf < (1ull << D); ++leaf) {
+                produce_leaf(J, leaf, tm_row, sm);
+                PHASE_T0();
+                // lanes: node (FAN, lane)
+                const uint64_t leaf_mask = J.mask | (leaf << Q0);
+                const int leaf_sel = J.nsel + __popcll(leaf);
+                const int c = lane;
+                const NodeRef nr = node_ref<T>(tabs, FAN, c);
+                const T vt = tvals[nr.tix];
+                const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(c) << L);
+                const int lsel = leaf_sel + __popc(c);
+                const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
+                if constexpr (Cfg<T>::TMEM) lane_tree_tmem<T, L>(tm_row, vt, nodeneg, lmask, lsel, acc, err);
+                else lane_tree<T, L>(sm + nr.off, 2 * L, 0, vt, nodeneg, lmask, lsel, acc, err);
+                acc.flush();
+                __syncwarp();
+                PHASE_MARK(4);
+            }
+            write_partial(acc, job);
+        }
     }
     if constexpr (Cfg<T>::TMEM) {
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
