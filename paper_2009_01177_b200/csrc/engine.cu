@@ -74,24 +74,30 @@ template <> struct Cfg<double> {
     static constexpr int MINB = 1;
     static constexpr bool TMEM = false;
     static constexpr bool WS = false;
+    static constexpr int WS_MODE = 0;
 };
 template <> struct Cfg<dd> {
     static constexpr int L = 4;
+#ifndef TOR_DD_WS
+#define TOR_DD_WS 2
+#endif
+    // Warp specialisation (TMEM only).  0: none, every warp runs whole leaves.
+    // 1: 4 producer warps (DFS + fan-out levels 1-4) + 4 consumer warps (level 5 +
+    //    lane subtrees), double-buffered fan areas per pair.
+    // 2: 4 producers (DFS + levels 1-3) + 8 consumers (levels 4, 5 + lane subtrees),
+    //    each producer alternating between two jobs / two consumers; 12 warps at 168
+    //    registers (3 per SM sub-partition).
+    static constexpr int WS_MODE = TOR_DD_TMEM ? TOR_DD_WS : 0;
+    static constexpr bool WS = WS_MODE >= 1;
 #ifdef TOR_DD_WPB
     static constexpr int WPB = TOR_DD_WPB;
 #else
     // one 8-warp CTA per SM (two warps per TMEM lane quadrant, 256 columns each):
     // measured 123 ms vs 138 ms for two 4-warp CTAs at n=32
-    static constexpr int WPB = TOR_DD_TMEM ? 8 : 2;
+    static constexpr int WPB = TOR_DD_TMEM ? (WS_MODE == 2 ? 12 : 8) : 2;
 #endif
     static constexpr int MINB = (TOR_DD_TMEM && WPB == 4) ? 2 : 1;
     static constexpr bool TMEM = TOR_DD_TMEM;
-#ifndef TOR_DD_WS
-#define TOR_DD_WS 1
-#endif
-    // warp specialisation: warps 0-3 run the DFS + fan-out (producers), warps 4-7 the
-    // lane subtrees (consumers) of the same TMEM lane quadrant, double-buffered in TMEM
-    static constexpr bool WS = TOR_DD_TMEM && WPB == 8 && TOR_DD_WS;
 };
 template <> struct Cfg<qd> {
     static constexpr int L = 3;
@@ -99,6 +105,7 @@ template <> struct Cfg<qd> {
     static constexpr int MINB = 1;
     static constexpr bool TMEM = false;
     static constexpr bool WS = false;
+    static constexpr int WS_MODE = 0;
 };
 
 template <class T> constexpr int root_modes() { return Cfg<T>::L + FAN; }
@@ -263,7 +270,10 @@ template <class T, int Q0>
 __device__ void dfs_elim(const T* P, int q, T* slot, bool write_slot, T* root, const T& t_in, T* t_out, T* uw,
                          const uint32_t* tb, uint64_t mask, int nsel, unsigned long long* err) {
     using A = Arith<T>;
-    constexpr int NB = 8;  // entries per lane per batch
+#ifndef TOR_NB
+#define TOR_NB 8
+#endif
+    constexpr int NB = TOR_NB;  // entries per lane per batch
     constexpr int RT = tri_sz(2 * Q0);
     const int lane = threadIdx.x & 31;
     PHASE_T0();
@@ -770,6 +780,136 @@ __device__ __forceinline__ void lane_tree_tmem(uint32_t row, const T& t, bool ne
     }
 }
 
+// TMEM-streamed lane subtree: emits the 2^L - 1 extension terms of the L-mode node in
+// this lane's TMEM row (its own term is emitted by the caller).  For L >= 4 the child
+// states (L-1 modes) are not kept in registers: the include child is streamed entry
+// by entry into the scratch columns scr (natural layout), the exclude child (the
+// parent's trailing block) is copied there, and one copy of the (L-1)-mode code runs
+// for both; the 3-mode level keeps its children (2 modes) in registers.
+template <class T, int M, int K, int END> struct LtUpdTm {
+    __device__ __forceinline__ static void run(const uint32_t* rt, const T (&u)[M], const T (&w)[M], uint32_t dst) {
+        if constexpr (K < END) {
+            constexpr int D = M - 2;
+            constexpr int i = tri_row(D, K), j = tri_col(D, K);
+            const T v =
+                Arith<T>::rank2(u32_to_dd(rt[0], rt[1], rt[2], rt[3]), u[2 + i], u[2 + j], w[2 + i], w[2 + j]);
+            uint32_t r[4];
+            dd_to_u32(v, r);
+            tm_st4(dst + tm_col<D>(K), r[0], r[1], r[2], r[3]);
+            LtUpdTm<T, M, K + 1, END>::run(rt + 4, u, w, dst);
+        }
+    }
+};
+template <int D, int K, int END> struct TmCopy {
+    __device__ __forceinline__ static void run(const uint32_t* rt, uint32_t dst) {
+        if constexpr (K < END) {
+            tm_st4(dst + tm_col<D - 2>(K), rt[0], rt[1], rt[2], rt[3]);
+            TmCopy<D, K + 1, END>::run(rt + 4, dst);
+        }
+    }
+};
+template <class T, int L>
+__device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t, bool neg, uint64_t mask, int nsel,
+                                         Acc<T>& acc, unsigned long long* err) {
+    using A = Arith<T>;
+    constexpr int M = 2 * L;
+    constexpr int K01 = 2 * M - 1;  // entries of rows 0 and 1
+    constexpr int NT = tri_sz(M - 2);
+    const uint64_t bit = 1ull << (L - 1);
+#pragma unroll 1
+    for (int br = 0; br < 2; ++br) {
+        T tn;
+        if constexpr (L >= 4) {
+            if (br == 0) {
+                uint32_t r0[4 * K01];
+                tm_ld_entries<M, 0, K01>(row, r0);
+                tm_wait_ld();
+                T e0[K01];
+#pragma unroll
+                for (int k = 0; k < K01; ++k) e0[k] = u32_to_dd(r0[4 * k], r0[4 * k + 1], r0[4 * k + 2], r0[4 * k + 3]);
+                const Piv<T> pv = pivot2<T>(e0[0], e0[1], e0[M], t);
+                if (pv.bad0 || pv.bad1) report_breakdown(err, mask | bit, 2 * nsel + (pv.bad0 ? 0 : 1));
+                tn = pv.tn;
+                T u[M], w[M];
+#pragma unroll
+                for (int j = 2; j < M; ++j) {
+                    u[j] = A::mul(e0[j], pv.r1);
+                    w[j] = A::mul(A::rank1s(e0[M + j - 1], pv.u1, u[j]), pv.r2);
+                }
+                constexpr int H = (NT + 2) / 3;
+                {
+                    uint32_t rt[4 * H];
+                    tm_ld_entries<M, K01, H>(row, rt);
+                    tm_wait_ld();
+                    LtUpdTm<T, M, 0, H>::run(rt, u, w, scr);
+                }
+                {
+                    uint32_t rt[4 * H];
+                    tm_ld_entries<M, K01 + H, H>(row, rt);
+                    tm_wait_ld();
+                    LtUpdTm<T, M, H, 2 * H>::run(rt, u, w, scr);
+                }
+                {
+                    uint32_t rt[4 * (NT - 2 * H)];
+                    tm_ld_entries<M, K01 + 2 * H, NT - 2 * H>(row, rt);
+                    tm_wait_ld();
+                    LtUpdTm<T, M, 2 * H, NT>::run(rt, u, w, scr);
+                }
+                acc.add(tn, !neg, nsel + 1);
+            } else {
+                constexpr int H = (NT + 1) / 2;
+                {
+                    uint32_t rt[4 * H];
+                    tm_ld_entries<M, K01, H>(row, rt);
+                    tm_wait_ld();
+                    TmCopy<M, 0, H>::run(rt, scr);
+                }
+                {
+                    uint32_t rt[4 * (NT - H)];
+                    tm_ld_entries<M, K01 + H, NT - H>(row, rt);
+                    tm_wait_ld();
+                    TmCopy<M, H, NT>::run(rt, scr);
+                }
+                tn = t;
+            }
+            tm_wait_st();
+            tmem_ext<T, L - 1>(scr, scr, tn, br == 0 ? !neg : neg, br == 0 ? (mask | bit) : mask, nsel + (br == 0),
+                               acc, err);
+        } else {
+            St<T, L - 1> Sn;
+            if (br == 0) {
+                uint32_t r0[4 * K01];
+                tm_ld_entries<M, 0, K01>(row, r0);
+                tm_wait_ld();
+                T e0[K01];
+#pragma unroll
+                for (int k = 0; k < K01; ++k) e0[k] = u32_to_dd(r0[4 * k], r0[4 * k + 1], r0[4 * k + 2], r0[4 * k + 3]);
+                const Piv<T> pv = pivot2<T>(e0[0], e0[1], e0[M], t);
+                if (pv.bad0 || pv.bad1) report_breakdown(err, mask | bit, 2 * nsel + (pv.bad0 ? 0 : 1));
+                tn = pv.tn;
+                T u[M], w[M];
+#pragma unroll
+                for (int j = 2; j < M; ++j) {
+                    u[j] = A::mul(e0[j], pv.r1);
+                    w[j] = A::mul(A::rank1s(e0[M + j - 1], pv.u1, u[j]), pv.r2);
+                }
+                lt_wave<T, M, 0, NT>(row, u, w, Sn);
+                acc.add(tn, !neg, nsel + 1);
+            } else {
+                uint32_t rt[4 * NT];
+                tm_ld_entries<M, K01, NT>(row, rt);
+                tm_wait_ld();
+#pragma unroll
+                for (int kk = 0; kk < NT; ++kk)
+                    Sn.e[kk] = u32_to_dd(rt[4 * kk], rt[4 * kk + 1], rt[4 * kk + 2], rt[4 * kk + 3]);
+                tn = t;
+            }
+            SubReg<T, L - 1>::run(Sn, tn, br == 0 ? !neg : neg, br == 0 ? (mask | bit) : mask, nsel + (br == 0), acc,
+                                  err);
+        }
+    }
+}
+
 // --------------------------------------------------------- subtree kernel ----
 // Per-warp shared memory: the Q0-mode root (copy of the DFS leaf view), the
 // include buffers of the fan-out levels, their t values, the pivot-row vectors and
@@ -797,6 +937,18 @@ template <class T> struct WarpSmem {
     static constexpr int kUwEntries = uw_need();
     static constexpr int kDfsT = kUwOff + kUwEntries;  // DFS slot t values (<= 32)
     static constexpr int kEntries = kDfsT + 32;
+    // WS mode 2 producer-private: pivot-row vectors of the DFS and levels 1..3, DFS t
+    // values of its two job contexts
+    __host__ __device__ static constexpr int prod_uw() {
+        int mx = 4 * kMaxJobModes;
+        for (int e = 1; e <= 3; ++e) {
+            const int need = (1 << (e - 1)) * (4 * (Q0 - e + 1) + 1);
+            if (need > mx) mx = need;
+        }
+        return mx;
+    }
+    static constexpr int kProdUw = prod_uw();
+    static constexpr int kProdEntries = kProdUw + 64;
     static constexpr size_t kWarpBytes = kEntries * sizeof(T);
     // Block-wide item tables of the fan-out trailing updates: level e has E*tn items
     // (it = x*tn + k: child x, entry k); word = src | ui << 11 | uj << 20 with src the
@@ -1049,8 +1201,8 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
     uint32_t tm_row = 0;
     if constexpr (Cfg<T>::TMEM) {
         // warp w uses TMEM lanes 32(w%4).. (its lane quadrant) and columns 256(w/4)..
-        static_assert(Cfg<T>::WPB == 4 || Cfg<T>::WPB == 8, "TMEM lane handoff: 4 or 8 warps per CTA");
-        constexpr uint32_t kCols = 64 * Cfg<T>::WPB;
+        static_assert(Cfg<T>::WPB == 4 || Cfg<T>::WPB == 8 || Cfg<T>::WPB == 12, "TMEM lane handoff: 4, 8, 12 warps");
+        constexpr uint32_t kCols = Cfg<T>::WPB >= 8 ? 512 : 256;
         if ((threadIdx.x >> 5) == 0) {
             const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base));
             asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(dst), "r"(kCols)
@@ -1075,19 +1227,21 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
     // (producer p, consumer p+4) owns areas 2p and 2p+1; their fan-out buffers and t
     // values alternate between leaves (slot = leaf parity), the pivot-row vectors of
     // area 2p are the producer's, those of area 2p+1 the consumer's (level FAN).
+    // WS mode 2: areas 0..7 belong to the consumers (producer p fills areas p, p+4);
+    // producer p's private pivot-row vectors and DFS t values follow the areas.
     const int pw = Cfg<T>::WS ? (wib & 3) : wib;
     const int ppb = Cfg<T>::WS ? 4 : WPB;  // producers per block
     auto area = [&](int a) { return reinterpret_cast<T*>(smem_raw + SM::kTabBytes + a * SM::kWarpBytes); };
-    T* sm = area(Cfg<T>::WS ? 2 * pw : pw);
+    T* sm = area(Cfg<T>::WS_MODE == 2 ? pw : (Cfg<T>::WS ? 2 * pw : pw));
     T* tvals = sm + SM::kTOff;
-    T* uwv = sm + SM::kUwOff;
-    T* dfs_t = sm + SM::kDfsT;
+    T* uwv = Cfg<T>::WS_MODE == 2 ? area(8) + pw * SM::kProdEntries : sm + SM::kUwOff;
+    T* dfs_t = Cfg<T>::WS_MODE == 2 ? uwv + SM::kProdUw : sm + SM::kDfsT;
     T* slots = scratch + static_cast<size_t>(blockIdx.x * ppb + pw) * scratch_stride;
 
     // DFS step + root + fan-out of one leaf of job J into the fan area fsm (buffers +
     // t values): all FAN levels, or (warp-specialised) levels 1..FAN-1 -- the level-FAN
     // states in shared memory, or in TMEM at tm_slot for the TMEM types
-    auto produce_leaf = [&](const Job<T>& J, uint64_t leaf, uint32_t tm_slot, T* fsm) {
+    auto produce_leaf = [&](const Job<T>& J, uint64_t leaf, uint32_t tm_slot, T* fsm, T* dfs_t, T* slots) {
         T* ftv = fsm + SM::kTOff;
         PHASE_T0();
         if (leaf > 0) {
@@ -1143,7 +1297,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         FanLevel<T, 1>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
         FanLevel<T, 2>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
         FanLevel<T, 3>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
-        FanLevel<T, 4>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
+        if constexpr (Cfg<T>::WS_MODE != 2) FanLevel<T, 4>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
         if constexpr (!Cfg<T>::WS) FanLevel<T, 5>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
     };
     auto write_partial = [&](Acc<T>& acc, unsigned long long job) {
@@ -1161,7 +1315,121 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         __syncwarp();
     };
 
-    if constexpr (Cfg<T>::WS) {
+    if constexpr (Cfg<T>::WS_MODE == 2) {
+        // ---- warp-specialised, 4 producers + 8 consumers.  Producer p keeps two job
+        // contexts s = 0, 1; leaf after leaf it alternates between them, running the DFS
+        // and fan-out levels 1..3 of context s into consumer (p + 4s)'s area.  Consumer c
+        // runs levels 4 and 5 (TMEM, its lane quadrant c % 4, columns 256 (c / 4)) and
+        // the lane subtrees, accumulating whole jobs (same per-job arithmetic and order
+        // as the unspecialised kernel).  Areas are handed over by mbarriers: full[c]
+        // (producer -> consumer), empty[c] (consumer -> producer, arrived as soon as the
+        // consumer no longer reads the producer's part of the area).
+        struct WsMeta {
+            unsigned long long mask;
+            unsigned long long job;
+            int sel, flags;  // 1: last leaf of the job, 2: no more leaves
+        };
+        __shared__ WsMeta meta[8];
+        __shared__ __align__(8) unsigned long long mbar[16];  // full[0..7], empty[8..15]
+        if (threadIdx.x < 16) {
+            const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[threadIdx.x]));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(32) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        __syncthreads();
+        auto mb_arrive = [&](int i) {
+            const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[i]));
+            asm volatile("{.reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0];}\n" ::"r"(a) : "memory");
+        };
+        auto mb_wait = [&](int i, uint32_t parity) {
+            const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[i]));
+            uint32_t ok = 0;
+            while (!ok)
+                asm volatile(
+                    "{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p;}\n"
+                    : "=r"(ok)
+                    : "r"(a), "r"(parity), "r"(1000000u)
+                    : "memory");
+        };
+        if (wib < 4) {
+            const int p = wib;
+            Job<T> J[2];
+            unsigned long long jid[2];
+            uint64_t leaf[2] = {0, 0};
+            bool act[2];
+            uint32_t uses[2] = {0, 0};
+            auto fetch = [&](int s) {
+                unsigned long long j = 0;
+                if (lane == 0) j = atomicAdd(job_counter, 1ull);
+                j = __shfl_sync(0xffffffffu, j, 0);
+                act[s] = j < njobs;
+                jid[s] = j;
+                if (act[s]) J[s] = jobs[j];
+                leaf[s] = 0;
+            };
+            fetch(0);
+            fetch(1);
+            while (act[0] || act[1]) {
+#pragma unroll 1
+                for (int s = 0; s < 2; ++s) {
+                    if (!act[s]) continue;
+                    const int c = p + 4 * s;
+                    mb_wait(8 + c, (uses[s] & 1) ^ 1);
+                    T* cslots = scratch + (static_cast<size_t>(blockIdx.x * 4 + p) * 2 + s) * scratch_stride;
+                    produce_leaf(J[s], leaf[s], 0u, area(c), dfs_t + 32 * s, cslots);
+                    if (lane == 0) {
+                        meta[c].mask = J[s].mask | (leaf[s] << Q0);
+                        meta[c].job = jid[s];
+                        meta[c].sel = J[s].nsel + __popcll(leaf[s]);
+                        meta[c].flags = leaf[s] + 1 == (1ull << D) ? 1 : 0;
+                    }
+                    __syncwarp();
+                    mb_arrive(c);
+                    ++uses[s];
+                    if (++leaf[s] == (1ull << D)) fetch(s);
+                }
+            }
+#pragma unroll 1
+            for (int s = 0; s < 2; ++s) {
+                const int c = p + 4 * s;
+                mb_wait(8 + c, (uses[s] & 1) ^ 1);
+                if (lane == 0) meta[c].flags = 2;
+                __syncwarp();
+                mb_arrive(c);
+            }
+        } else {
+            const int c = wib - 4;
+            const uint32_t crow = tmem_base + ((32u * (c & 3)) << 16) + 256u * (c >> 2);
+            T* csm = area(c);
+            T* ctv = csm + SM::kTOff;
+            T* cuw = csm + SM::kUwOff;
+            Acc<T> acc;
+            acc.sc = tsc;
+            for (uint32_t k = 0;; ++k) {
+                mb_wait(c, k & 1);
+                const unsigned long long leaf_mask = meta[c].mask;
+                const unsigned long long job = meta[c].job;
+                const int leaf_sel = meta[c].sel, flags = meta[c].flags;
+                if (flags & 2) break;
+                FanLevel<T, 4>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
+                FanLevel<T, FAN>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
+                const T vt = ctv[node_ref<T>(tabs, FAN, lane).tix];
+                __syncwarp();
+                mb_arrive(8 + c);  // the producer may refill root..L3 and t values 0..6, 31
+                const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(lane) << L);
+                const int lsel = leaf_sel + __popc(lane);
+                const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
+                acc.add(vt, nodeneg, lsel);
+                tmem_ext<T, L>(crow, crow + 4 * tri_sz(2 * L), vt, nodeneg, lmask, lsel, acc, err);
+                acc.flush();
+                if (flags & 1) {
+                    write_partial(acc, job);
+                    acc = Acc<T>();
+                    acc.sc = tsc;
+                }
+            }
+        }
+    } else if constexpr (Cfg<T>::WS) {
         // ---- warp-specialised: producer warp p (0-3) runs the DFS and fan-out levels
         // 1..FAN-1 of leaf i into fan area 2p + (i & 1); consumer warp p+4 runs level FAN
         // (into its TMEM lane quadrant) and the lane subtrees from that area.  One named
@@ -1183,7 +1451,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 if (job >= njobs) break;
                 const Job<T> J = jobs[job];
                 for (uint64_t leaf = 0; leaf < (1ull << D); ++leaf) {
-                    produce_leaf(J, leaf, 0u, area(2 * pair + slot));
+                    produce_leaf(J, leaf, 0u, area(2 * pair + slot), dfs_t, slots);
                     if (lane == 0) {
                         meta[pair][slot].mask = J.mask | (leaf << Q0);
                         meta[pair][slot].job = job;
@@ -1217,7 +1485,12 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(c) << L);
                 const int lsel = leaf_sel + __popc(c);
                 const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
+#ifdef TOR_LT_REGS
                 lane_tree_tmem<T, L>(crow, vt, nodeneg, lmask, lsel, acc, err);
+#else
+                acc.add(vt, nodeneg, lsel);
+                tmem_ext<T, L>(crow, crow + 4 * tri_sz(2 * L), vt, nodeneg, lmask, lsel, acc, err);
+#endif
                 acc.flush();
                 if (flags & 1) {
                     write_partial(acc, job);
@@ -1238,7 +1511,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
             Acc<T> acc;
             acc.sc = tsc;
             for (uint64_t leaf = 0; leaf < (1ull << D); ++leaf) {
-                produce_leaf(J, leaf, tm_row, sm);
+                produce_leaf(J, leaf, tm_row, sm, dfs_t, slots);
                 PHASE_T0();
                 // lanes: node (FAN, lane)
                 const uint64_t leaf_mask = J.mask | (leaf << Q0);
@@ -1262,7 +1535,8 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         __syncthreads();
         if ((threadIdx.x >> 5) == 0)
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(64 * Cfg<T>::WPB)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
+                         "r"(Cfg<T>::WPB >= 8 ? 512 : 256)
                          : "memory");
     }
 }
@@ -1498,7 +1772,8 @@ class PlanImpl final : public Plan {
         if (rjob_ >= Q0) {
             using SM = WarpSmem<T>;
             constexpr int WPB = Cfg<T>::WPB;
-            smem_ = SM::kTabBytes + SM::kWarpBytes * WPB;
+            smem_ = Cfg<T>::WS_MODE == 2 ? SM::kTabBytes + SM::kWarpBytes * 8 + sizeof(T) * SM::kProdEntries * 4
+                                         : SM::kTabBytes + SM::kWarpBytes * WPB;
             CK(cudaFuncSetAttribute(subtree_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem_)));
             CK(cudaFuncSetAttribute(subtree_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
