@@ -271,7 +271,7 @@ __device__ void dfs_elim(const T* P, int q, T* slot, bool write_slot, T* root, c
                          const uint32_t* tb, uint64_t mask, int nsel, unsigned long long* err) {
     using A = Arith<T>;
 #ifndef TOR_NB
-#define TOR_NB 8
+#define TOR_NB 6
 #endif
     constexpr int NB = TOR_NB;  // entries per lane per batch
     constexpr int RT = tri_sz(2 * Q0);
@@ -1035,7 +1035,7 @@ template <class T, int M, int C> struct MirChunk {
 };
 
 #ifndef TOR_UB
-#define TOR_UB 8
+#define TOR_UB 5
 #endif
 template <class T, int E_LVL> struct FanLevel {
     static constexpr int Q0 = WarpSmem<T>::Q0;
