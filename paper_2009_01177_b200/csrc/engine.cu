@@ -473,6 +473,20 @@ __global__ void direct_prefix_kernel(int n, int k, const T* R, int ninst, size_t
 
 // ------------------------------------------------ register-level subtrees ----
 // State of Q modes in registers: packed upper triangle of 2Q rows.
+// Pivot chain inside the lane subtrees: optionally one out-of-line copy (instruction
+// footprint) instead of one per call site.
+#ifdef TOR_PIVOT_NOINLINE
+template <class T>
+__device__ __noinline__ Piv<T> piv_lt(T s00, T s01, T s11, T t) {
+    return pivot2<T>(s00, s01, s11, t);
+}
+#else
+template <class T>
+__device__ __forceinline__ Piv<T> piv_lt(const T& s00, const T& s01, const T& s11, const T& t) {
+    return pivot2<T>(s00, s01, s11, t);
+}
+#endif
+
 template <class T, int Q> struct St {
     T e[tri_sz(2 * Q)];
 };
@@ -485,7 +499,7 @@ __device__ __forceinline__ void elim_reg(const St<T, Q>& S, St<T, Q - 1>& out, c
                                          int nsel, unsigned long long* err) {
     using A = Arith<T>;
     constexpr int M = 2 * Q;
-    const Piv<T> pv = pivot2<T>(S.e[cix<M>(0, 0)], S.e[cix<M>(0, 1)], S.e[cix<M>(1, 1)], t);
+    const Piv<T> pv = piv_lt<T>(S.e[cix<M>(0, 0)], S.e[cix<M>(0, 1)], S.e[cix<M>(1, 1)], t);
     const T r1 = pv.r1, u1 = pv.u1, r2 = pv.r2;
     if (pv.bad0 || pv.bad1) report_breakdown(err, mask, 2 * nsel + (pv.bad0 ? 0 : 1));
     tout = pv.tn;
@@ -827,7 +841,7 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
                 T e0[K01];
 #pragma unroll
                 for (int k = 0; k < K01; ++k) e0[k] = u32_to_dd(r0[4 * k], r0[4 * k + 1], r0[4 * k + 2], r0[4 * k + 3]);
-                const Piv<T> pv = pivot2<T>(e0[0], e0[1], e0[M], t);
+                const Piv<T> pv = piv_lt<T>(e0[0], e0[1], e0[M], t);
                 if (pv.bad0 || pv.bad1) report_breakdown(err, mask | bit, 2 * nsel + (pv.bad0 ? 0 : 1));
                 tn = pv.tn;
                 T u[M], w[M];
@@ -884,7 +898,7 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
                 T e0[K01];
 #pragma unroll
                 for (int k = 0; k < K01; ++k) e0[k] = u32_to_dd(r0[4 * k], r0[4 * k + 1], r0[4 * k + 2], r0[4 * k + 3]);
-                const Piv<T> pv = pivot2<T>(e0[0], e0[1], e0[M], t);
+                const Piv<T> pv = piv_lt<T>(e0[0], e0[1], e0[M], t);
                 if (pv.bad0 || pv.bad1) report_breakdown(err, mask | bit, 2 * nsel + (pv.bad0 ? 0 : 1));
                 tn = pv.tn;
                 T u[M], w[M];
