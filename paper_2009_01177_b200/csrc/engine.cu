@@ -273,7 +273,10 @@ __device__ void dfs_elim(const T* P, int q, T* slot, bool write_slot, T* root, c
 #ifndef TOR_NB
 #define TOR_NB 6
 #endif
-    constexpr int NB = TOR_NB;  // entries per lane per batch
+#ifndef TOR_QD_NB
+#define TOR_QD_NB 1
+#endif
+    constexpr int NB = sizeof(T) == sizeof(qd) ? TOR_QD_NB : TOR_NB;  // entries per lane per batch
     constexpr int RT = tri_sz(2 * Q0);
     const int lane = threadIdx.x & 31;
     PHASE_T0();
@@ -525,6 +528,10 @@ __device__ __forceinline__ void elim_reg(const St<T, Q>& S, St<T, Q - 1>& out, c
 #define TOR_LOOPQ 3
 #endif
 constexpr int kLoopQ = TOR_LOOPQ;
+#ifndef TOR_QD_LOOPQ
+#define TOR_QD_LOOPQ 3
+#endif
+constexpr int kLoopQQd = TOR_QD_LOOPQ;
 
 template <class T, int Q> struct SubReg {
     __device__ __forceinline__ static void branch(const St<T, Q>& S, int br, const T& t, bool neg, uint64_t mask,
@@ -548,7 +555,7 @@ template <class T, int Q> struct SubReg {
     }
     __device__ __forceinline__ static void run(const St<T, Q>& S, const T& t, bool neg, uint64_t mask, int nsel,
                                                Acc<T>& acc, unsigned long long* err) {
-        if constexpr (Q >= kLoopQ) {
+        if constexpr (Q >= (sizeof(T) == sizeof(qd) ? kLoopQQd : kLoopQ)) {
 #pragma unroll 1
             for (int br = 0; br < 2; ++br) branch(S, br, t, neg, mask, nsel, acc, err);
         } else {
@@ -1051,6 +1058,9 @@ template <class T, int M, int C> struct MirChunk {
 #ifndef TOR_UB
 #define TOR_UB 5
 #endif
+#ifndef TOR_QD_UB
+#define TOR_QD_UB 1
+#endif
 template <class T, int E_LVL> struct FanLevel {
     static constexpr int Q0 = WarpSmem<T>::Q0;
     static constexpr int E = 1 << (E_LVL - 1);
@@ -1138,7 +1148,7 @@ template <class T, int E_LVL> struct FanLevel {
         // trailing updates into the level-e buffers: item it = lane + 32 s (x-major)
         constexpr int NE = E * tn;
         constexpr int NIT = (NE + 31) / 32;
-        constexpr int UB = TOR_UB;  // items per batch: all loads of a batch precede its stores
+        constexpr int UB = sizeof(T) == sizeof(qd) ? TOR_QD_UB : TOR_UB;  // items per batch (loads before stores)
         const uint32_t* itb = tabs + WarpSmem<T>::item_off(E_LVL) + lane;
         T* out = sm + WarpSmem<T>::lvl_off(E_LVL) + lane;
 #pragma unroll 1
