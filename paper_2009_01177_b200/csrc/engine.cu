@@ -40,6 +40,7 @@ namespace {
 constexpr int FAN = 5;  // breadth-first fan-out levels -> 32 lane nodes
 constexpr int MAX_LEVELS = 48;
 constexpr int kMaxJobModes = 24;
+constexpr uint64_t kWantJobs = 262144;
 
 __host__ __device__ constexpr int tri_sz(int d) { return d * (d + 1) / 2; }
 __host__ __device__ __forceinline__ int tri_ix(int d, int i, int j) {
@@ -1755,8 +1756,13 @@ class PlanImpl final : public Plan {
         for (auto& e : ev_) CK(cudaEventCreate(&e));
         if (const int st = ensure_ijtab(device, err)) return st;
 
-        // prefix depth: enough jobs to fill the GPU, job states <= kMaxJobModes modes
-        const uint64_t want_jobs = 16384;
+        // Prefix depth c: a function of (n, instances) only -- not of this plan's class
+        // range -- so every shard count evaluates the same jobs and the fixed fold tree
+        // gives bit-identical results.  kWantJobs whole-problem jobs keep the dynamic
+        // schedule's tail short even for the 1/8 shard of an 8-GPU run; job states are
+        // <= kMaxJobModes modes.
+        uint64_t want_jobs = kWantJobs;
+        if (const char* wj = std::getenv("TOR_WANT_JOBS")) want_jobs = std::strtoull(wj, nullptr, 10);
         c_ = 0;
         if (n_ >= Q0) {
             int cw = 0;

@@ -184,6 +184,18 @@ def test_shards_fold_bit_identical(world):
         assert folded["sum_abs_terms"] == whole["sum_abs_terms"]
 
 
+def test_shards_fold_bit_identical_n32_dd():
+    # the headline configuration: 1/2/4/8 shards of the n=32 DD Torontonian fold to the
+    # identical words (the prefix depth does not depend on the shard's class range)
+    m = W.load_config_instance(4)
+    whole = T.torontonian(m, "128")
+    for world in (2, 4, 8):
+        parts = [T.torontonian_shard(m, "128", r, world) for r in range(world)]
+        folded = T.fold_partials(parts, m)
+        assert folded["words"] == whole["words"], world
+        assert folded["sum_abs_terms"] == whole["sum_abs_terms"], world
+
+
 def test_determinism_reruns():
     m = W.load_config_instance(1)
     a = T.torontonian(m, "128")
