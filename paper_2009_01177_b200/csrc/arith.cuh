@@ -159,52 +159,57 @@ TOR_HD dd dd_rank1(dd s, dd a, dd b) {
     return dd{s1, lo};
 }
 
-// ---- fixed-exponent DD for Schur-complement states ------------------------------
+// ---- fixed-exponent (biased grid) DD for Schur-complement states -----------------
 // Every entry of every Schur complement of the (scaled) R satisfies |S_ij| <= max_k R_kk
-// (SPD: Schur complements only shrink the diagonal, |S_ij| <= sqrt(S_ii S_jj)), and the
-// Cholesky row vectors satisfy |u_i u_j| <= max_k R_kk too.  With max_k R_kk < 3.75 the
-// leading word of a state entry is kept on the grid 2^-kGridG: products are rounded to
-// that grid by the add/subtract of C, and the leading-word updates s.hi - P1 - P2 are
-// then EXACT (no TwoSum); the rounding remainders go to the low word through the FMA.
-// A rank-2 entry update costs 16 FP64 instructions instead of 24, with the same
-// backward error shape (absolute, ~2^-103 of the O(1) state scale).
+// (SPD: Schur complements only shrink the diagonal, |S_ij| <= sqrt(S_ii S_jj)), and so do
+// the partial complements S - u u^T and the Cholesky products |u_i u_j|, |w_i w_j|.  With
+// max_k R_kk < 3.75 a state entry is stored BIASED: its leading word is b = s_hi + C with
+// C = 12, so b lies in [8.25, 15.75] where the double spacing is 2^-kGridG -- the leading
+// word sits on the grid 2^-49 by construction.  A rank-2 entry update is then
+//     z1 = fma(-u_i, u_j, b)      (= grid(s - u_i u_j) + C: the FMA rounds onto the grid)
+//     r1 = fma(u_i, u_j, z1 - b)  (the product's grid remainder; z1 - b exact)
+//     z2 = fma(-w_i, w_j, z1),  r2 = fma(w_i, w_j, z2 - z1)
+// and the low word collects s_lo - r1 - r2 and the four cross products: 12 FP64
+// instructions per entry (8 DFMA, 4 DADD) instead of 16 for an unbiased grid (DMUL +
+// two DADDs per grid rounding) or 24 with TwoSums.  Same backward error shape (absolute,
+// ~2^-103 of the O(1) state scale).  Values leave the biased form (unb(): one exact
+// DADD) only where they become pivots or pivot-row vectors.
 constexpr int kGridG = 49;
-constexpr double kGridC = 12.0;  // 1.5 * 2^(52 - kGridG): p + C lies in [8, 16) for |p| < 4
+constexpr double kGridC = 12.0;  // 1.5 * 2^(52 - kGridG): s + C lies in [8, 16) for |s| < 4
 
 TOR_HD double grid_round(double p) { return (p + kGridC) - kGridC; }
 
-// (x + y) as a grid state entry (host-side R construction)
+// (x + y) as a biased grid state entry (host-side R construction)
 TOR_HD dd dd_to_grid(double x, double y) {
     double sh, se;
     two_sum(x, y, sh, se);
-    const double H = grid_round(sh);
-    return dd{H, (sh - H) + se};
+    const double B = sh + kGridC;  // rounds sh onto the grid (exact in [8, 16))
+    return dd{B, (sh - (B - kGridC)) + se};
 }
+TOR_HD dd dd_unbias(const dd& s) { return dd{s.hi - kGridC, s.lo}; }
 
 TOR_HD dd dd_rank2_grid(dd s, dd a, dd b, dd c, dd d) {
-    const double p1 = a.hi * b.hi;
-    const double P1 = grid_round(p1);
-    const double r1 = fma_(a.hi, b.hi, -P1);
-    const double p2 = c.hi * d.hi;
-    const double P2 = grid_round(p2);
-    const double r2 = fma_(c.hi, d.hi, -P2);
-    const double hi = (s.hi - P1) - P2;
+    const double z1 = fma_(-a.hi, b.hi, s.hi);
+    const double r1 = fma_(a.hi, b.hi, z1 - s.hi);
+    const double z2 = fma_(-c.hi, d.hi, z1);
+    const double r2 = fma_(c.hi, d.hi, z2 - z1);
     double lo = s.lo - r1;
     lo = lo - r2;
     lo = fma_(-a.hi, b.lo, lo);
     lo = fma_(-a.lo, b.hi, lo);
     lo = fma_(-c.hi, d.lo, lo);
     lo = fma_(-c.lo, d.hi, lo);
-    return dd{hi, lo};
+    return dd{z2, lo};
 }
+// s - a*b for a biased state entry s (the partial complement of a pivot-row vector);
+// the result is UNBIASED (it feeds a product)
 TOR_HD dd dd_rank1_grid(dd s, dd a, dd b) {
-    const double p1 = a.hi * b.hi;
-    const double P1 = grid_round(p1);
-    const double r1 = fma_(a.hi, b.hi, -P1);
+    const double z1 = fma_(-a.hi, b.hi, s.hi);
+    const double r1 = fma_(a.hi, b.hi, z1 - s.hi);
     double lo = s.lo - r1;
     lo = fma_(-a.hi, b.lo, lo);
     lo = fma_(-a.lo, b.hi, lo);
-    return dd{s.hi - P1, lo};
+    return dd{z1 - kGridC, lo};
 }
 
 // 1/sqrt(x) for normalised x > 0: fp64 seed + one DD Newton step on the exact
@@ -357,6 +362,7 @@ template <> struct Arith<double> {
     TOR_HD static double rank1(double s, double a, double b) { return fma_(-a, b, s); }
     TOR_HD static double rank1s(double s, double a, double b) { return fma_(-a, b, s); }
     TOR_HD static double rsqrt(double a) { return rsqrt_d(a); }
+    TOR_HD static double unb(double a) { return a; }
     TOR_HD static double neg(double a) { return -a; }
     TOR_HD static void words(double a, double* w) { w[0] = a; }
 };
@@ -389,12 +395,15 @@ template <> struct Arith<dd> {
         return dd_rank2_grid(s, a, b, c, d);
     }
     TOR_HD static dd rank1s(const dd& s, const dd& a, const dd& b) { return dd_rank1_grid(s, a, b); }
+    // state entry -> value
+    TOR_HD static dd unb(const dd& a) { return dd_unbias(a); }
 #else
     static constexpr bool kGrid = false;
     TOR_HD static dd rank2(const dd& s, const dd& a, const dd& b, const dd& c, const dd& d) {
         return dd_rank2(s, a, b, c, d);
     }
     TOR_HD static dd rank1s(const dd& s, const dd& a, const dd& b) { return dd_rank1(s, a, b); }
+    TOR_HD static dd unb(const dd& a) { return a; }
 #endif
     // general (non-state) s - a*b
     TOR_HD static dd rank1(const dd& s, const dd& a, const dd& b) { return dd_rank1(s, a, b); }
@@ -420,6 +429,7 @@ template <> struct Arith<qd> {
     TOR_HD static qd rank1(const qd& s, const qd& a, const qd& b) { return qd_rank1(s, a, b); }
     TOR_HD static qd rank1s(const qd& s, const qd& a, const qd& b) { return qd_rank1(s, a, b); }
     TOR_HD static qd rsqrt(const qd& a) { return qd_rsqrt(a); }
+    TOR_HD static qd unb(const qd& a) { return a; }
     TOR_HD static qd neg(const qd& a) { return qd_neg(a); }
     TOR_HD static void words(const qd& a, double* w) {
         for (int i = 0; i < 4; ++i) w[i] = a.x[i];
@@ -431,7 +441,8 @@ template <> struct Arith<qd> {
 // rho1 = 1/sqrt(s00) and rho2 = 1/sqrt(s11 - s01^2/s00), computed as
 // rho2 = sqrt(s00) * rhod with rhod = 1/sqrt(det2), det2 = s00 s11 - s01^2, so the
 // two reciprocal square roots are independent (half the dependent latency of the
-// textbook chain); the child's term factor is t * rhod.
+// textbook chain); the child's term factor is t * rhod.  s00, s01, s11 are state
+// entries (biased in grid DD).
 template <class T> struct Piv {
     T r1, u1, r2, tn;
     bool bad0, bad1;
@@ -440,13 +451,14 @@ template <class T>
 TOR_HD Piv<T> pivot2(const T& s00, const T& s01, const T& s11, const T& t) {
     using A = Arith<T>;
     Piv<T> p;
-    const T a = A::norm(s00);
+    const T a = A::norm(A::unb(s00));
+    const T b01 = A::unb(s01);
     p.bad0 = nonpositive(A::hi(a));
     p.r1 = A::rsqrt(a);
-    const T det = A::norm(A::rank1(A::mul(a, s11), s01, s01));
+    const T det = A::norm(A::rank1(A::mul(a, A::unb(s11)), b01, b01));
     p.bad1 = nonpositive(A::hi(det));
     const T rd = A::rsqrt(det);
-    p.u1 = A::mul(s01, p.r1);
+    p.u1 = A::mul(b01, p.r1);
     p.r2 = A::mul(A::mul(a, p.r1), rd);
     p.tn = A::mul(t, rd);
     return p;

@@ -191,21 +191,24 @@ template <> __device__ __forceinline__ void warp_fold<double>(Acc<double>& a) {
 // ------------------------------------------------ warp-cooperative elimination --
 // Eliminates the first mode (rows 0,1) of the q-mode view (S, d, sr) into the
 // packed (2q-2)-row triangle dst; t_out = t * rho1 * rho2.  uw: shared scratch of
-// 4q entries.  All lanes compute the pivot chain redundantly (warp-uniform).
+// 4q entries.  All lanes compute the pivot chain redundantly (warp-uniform).  The
+// trailing entries [kbeg, kend) are this warp's share (several warps may split one
+// elimination: each recomputes the pivots and vectors, only part 0 writes t_out and
+// reports breakdowns).
 template <class T>
 __device__ void warp_elim(const T* S, int d, int sr, int q, T* dst, const T& t_in, T* t_out, T* uw,
-                          uint64_t mask, int nsel, unsigned long long* err) {
+                          uint64_t mask, int nsel, unsigned long long* err, int part = 0, int nparts = 1) {
     using A = Arith<T>;
     const int lane = threadIdx.x & 31;
     const Piv<T> pv = pivot2<T>(S[tri_ix(d, sr, sr)], S[tri_ix(d, sr, sr + 1)], S[tri_ix(d, sr + 1, sr + 1)], t_in);
     const T r1 = pv.r1, u1 = pv.u1, r2 = pv.r2;
-    if (lane == 0) {
+    if (lane == 0 && part == 0) {
         if (pv.bad0 || pv.bad1) report_breakdown(err, mask, 2 * nsel + (pv.bad0 ? 0 : 1));
         *t_out = pv.tn;
     }
     const int m = 2 * q;
     for (int j = 2 + lane; j < m; j += 32) {
-        const T uj = A::mul(S[tri_ix(d, sr, sr + j)], r1);
+        const T uj = A::mul(A::unb(S[tri_ix(d, sr, sr + j)]), r1);
         const T wj = A::mul(A::rank1s(S[tri_ix(d, sr + 1, sr + j)], u1, uj), r2);
         uw[j] = uj;
         uw[m + j] = wj;
@@ -215,18 +218,20 @@ __device__ void warp_elim(const T* S, int d, int sr, int q, T* dst, const T& t_i
     // (L2-resident) source reads overlap; positions advance incrementally.
     const int dn = m - 2;
     const int total = tri_sz(dn);
-    int i = 0, k0 = lane;
+    const int per = ((total + nparts - 1) / nparts + 127) & ~127;
+    const int kbeg = part * per, kend = min(total, kbeg + per);
+    int i = 0, k0 = kbeg + lane;
     while (i < dn && k0 >= dn - i) {
         k0 -= dn - i;
         ++i;
     }
     int j = i + k0;
-    for (int kb = 0; kb < total; kb += 128) {
+    for (int kb = kbeg; kb < kend; kb += 128) {
         int ii[4], jj[4];
         T sv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const bool ok = kb + lane + 32 * u < total;
+            const bool ok = kb + lane + 32 * u < kend;
             ii[u] = ok ? i : 0;
             jj[u] = ok ? j : 0;
             sv[u] = S[tri_ix(d, sr + 2 + ii[u], sr + 2 + jj[u])];
@@ -240,7 +245,7 @@ __device__ void warp_elim(const T* S, int d, int sr, int q, T* dst, const T& t_i
         for (int u = 0; u < 4; ++u) {
             const T v = A::rank2(sv[u], uw[2 + ii[u]], uw[2 + jj[u]], uw[m + 2 + ii[u]], uw[m + 2 + jj[u]]);
             const int k = kb + lane + 32 * u;
-            if (k < total) dst[k] = v;
+            if (k < kend) dst[k] = v;
         }
     }
     __syncwarp();
@@ -317,7 +322,7 @@ __device__ void dfs_elim(const T* P, int q, T* slot, bool write_slot, T* root, c
     for (int r = 0; r < 2; ++r) {
         const int jv = 2 + lane + 32 * r;
         if (jv < m) {
-            const T uj = A::mul(v0[r], pv.r1);
+            const T uj = A::mul(A::unb(v0[r]), pv.r1);
             uw[jv] = uj;
             uw[m + jv] = A::mul(A::rank1s(v1[r], pv.u1, uj), pv.r2);
         }
@@ -370,21 +375,23 @@ __device__ __forceinline__ void node_view(const PrefixGeom& g, const T* pool, co
     t = tpool[inst * g.inst_ts + g.toff[lvl] + p];
 }
 
-// Level e: every include node (inst, p), p < 2^(e-1), eliminates the first mode of
-// its parent view (e-1, p) into level-e buffer p.
+// Level e: every include node (inst, p), p in [plo, plo + cnt), eliminates the first
+// mode of its parent view (e-1, p) into level-e buffer p; `parts` warps share one
+// elimination (top levels: few nodes, long trailing updates).
 template <class T>
-__global__ void prefix_level_kernel(PrefixGeom g, T* pool, T* tpool, int e, int ninst,
-                                    unsigned long long* err) {
+__global__ void prefix_level_kernel(PrefixGeom g, T* pool, T* tpool, int e, int ninst, uint64_t plo, uint64_t cnt,
+                                    int parts, unsigned long long* err) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* uw_all = reinterpret_cast<T*>(smem_raw);
     const int wib = threadIdx.x >> 5;
     T* uw = uw_all + wib * (4 * g.n);
-    const uint64_t per = 1ull << (e - 1);
-    const uint64_t total = per * ninst;
+    const uint64_t total = cnt * ninst * parts;
     const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
     for (uint64_t it = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; it < total; it += nw) {
-        const int inst = static_cast<int>(it / per);
-        const uint64_t p = it % per;
+        const int part = static_cast<int>(it % parts);
+        const uint64_t node = it / parts;
+        const int inst = static_cast<int>(node / cnt);
+        const uint64_t p = plo + node % cnt;
         const T* base;
         int dim, skip;
         T t;
@@ -393,7 +400,7 @@ __global__ void prefix_level_kernel(PrefixGeom g, T* pool, T* tpool, int e, int 
         T* dst = pool + inst * g.inst_entries + g.off[e] + p * static_cast<uint64_t>(tri_sz(2 * (g.n - e)));
         T* tdst = tpool + inst * g.inst_ts + g.toff[e] + p;
         const uint64_t mask = ((p << 1) | 1ull) << (g.n - e);
-        warp_elim<T>(base, dim, 2 * skip, q, dst, t, tdst, uw, mask, __popcll(mask) - 1, err);
+        warp_elim<T>(base, dim, 2 * skip, q, dst, t, tdst, uw, mask, __popcll(mask) - 1, err, part, parts);
     }
 }
 
@@ -510,7 +517,7 @@ __device__ __forceinline__ void elim_reg(const St<T, Q>& S, St<T, Q - 1>& out, c
     T u[M], w[M];
 #pragma unroll
     for (int j = 2; j < M; ++j) {
-        u[j] = A::mul(S.e[cix<M>(0, j)], r1);
+        u[j] = A::mul(A::unb(S.e[cix<M>(0, j)]), r1);
         w[j] = A::mul(A::rank1s(S.e[cix<M>(1, j)], u1, u[j]), r2);
     }
 #pragma unroll
@@ -569,7 +576,8 @@ template <class T> struct SubReg<T, 1> {
     __device__ __forceinline__ static void run(const St<T, 1>& S, const T& t, bool neg, uint64_t mask, int nsel,
                                                Acc<T>& acc, unsigned long long* err) {
         using A = Arith<T>;
-        const T det = A::norm(A::rank1(A::mul(S.e[0], S.e[2]), S.e[1], S.e[1]));
+        const T s01 = A::unb(S.e[1]);
+        const T det = A::norm(A::rank1(A::mul(A::unb(S.e[0]), A::unb(S.e[2])), s01, s01));
         if (nonpositive(A::hi(det))) report_breakdown(err, mask | 1ull, 2 * nsel + 1);
         const T tn = A::mul(t, A::rsqrt(det));
         acc.add(tn, !neg, nsel + 1);
@@ -598,7 +606,7 @@ __device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t,
             T u[M], w[M];
 #pragma unroll
             for (int j = 2; j < M; ++j) {
-                u[j] = A::mul(S[tri_ix(d, sr, sr + j)], r1);
+                u[j] = A::mul(A::unb(S[tri_ix(d, sr, sr + j)]), r1);
                 w[j] = A::mul(A::rank1s(S[tri_ix(d, sr + 1, sr + j)], u1, u[j]), r2);
             }
 #pragma unroll
@@ -779,7 +787,7 @@ __device__ __forceinline__ void lane_tree_tmem(uint32_t row, const T& t, bool ne
             T u[M], w[M];
 #pragma unroll
             for (int j = 2; j < M; ++j) {
-                u[j] = A::mul(e0[j], pv.r1);
+                u[j] = A::mul(A::unb(e0[j]), pv.r1);
                 w[j] = A::mul(A::rank1s(e0[M + j - 1], pv.u1, u[j]), pv.r2);
             }
             // trailing block in two waves to bound live registers
@@ -855,7 +863,7 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
                 T u[M], w[M];
 #pragma unroll
                 for (int j = 2; j < M; ++j) {
-                    u[j] = A::mul(e0[j], pv.r1);
+                    u[j] = A::mul(A::unb(e0[j]), pv.r1);
                     w[j] = A::mul(A::rank1s(e0[M + j - 1], pv.u1, u[j]), pv.r2);
                 }
                 constexpr int H = (NT + 2) / 3;
@@ -912,7 +920,7 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
                 T u[M], w[M];
 #pragma unroll
                 for (int j = 2; j < M; ++j) {
-                    u[j] = A::mul(e0[j], pv.r1);
+                    u[j] = A::mul(A::unb(e0[j]), pv.r1);
                     w[j] = A::mul(A::rank1s(e0[M + j - 1], pv.u1, u[j]), pv.r2);
                 }
                 lt_wave<T, M, 0, NT>(row, u, w, Sn);
@@ -1098,7 +1106,7 @@ template <class T, int E_LVL> struct FanLevel {
             }
 #pragma unroll
             for (int s = 0; s < NVS; ++s) {
-                a[s] = A::mul(a[s], pv.r1);
+                a[s] = A::mul(A::unb(a[s]), pv.r1);
                 b[s] = A::mul(A::rank1s(b[s], pv.u1, a[s]), pv.r2);
             }
 #pragma unroll
@@ -1590,7 +1598,7 @@ __global__ void small_job_kernel(const Job<T>* jobs, uint64_t njobs, int nmodes,
             for (int b = a; b < d; ++b) {
                 const int ra = 2 * (J.skip + sel[a >> 1]) + (a & 1);
                 const int rb = 2 * (J.skip + sel[b >> 1]) + (b & 1);
-                M[tri_ix(d, a, b)] = J.base[tri_ix(J.dim, ra, rb)];
+                M[tri_ix(d, a, b)] = A::unb(J.base[tri_ix(J.dim, ra, rb)]);
             }
         T t = J.t;
         const uint64_t mask = J.mask | w;
@@ -1632,16 +1640,31 @@ template <class T> __host__ __device__ inline void merge_words(double* a, const 
     a[4] += b[4];
 }
 
-// One block per instance: in-place fixed binary tree over the instance's `per`
-// consecutive job partials (5 doubles each); result in partials[inst*per].
+// Fixed binary tree over an instance's `per` consecutive job partials (5 doubles
+// each): at stride s = 1, 2, 4, ... partial i (i = 0 mod 2s) absorbs partial i + s
+// (when i + s < per); the result lands in partial 0.  One pass folds, per block,
+// kFoldB consecutive elements of the level-S array (element k = partial k*S) -- an
+// aligned subtree of the same tree -- into its first element; passes at S = 1,
+// kFoldB, kFoldB^2, ... reproduce the whole tree exactly (bit-identical to a single
+// sequential fold, and to fold_words on the host).
+constexpr int kFoldB = 512;
 template <class T>
-__global__ void fold_kernel(double* partials, uint64_t per) {
-    double* p = partials + blockIdx.x * per * 5;
-    for (uint64_t s = 1; s < per; s <<= 1) {
-        for (uint64_t i = threadIdx.x * 2 * s; i + s < per; i += static_cast<uint64_t>(blockDim.x) * 2 * s)
-            merge_words<T>(p + i * 5, p + (i + s) * 5);
+__global__ void __launch_bounds__(kFoldB / 2) fold_pass_kernel(double* partials, uint64_t per, uint64_t S, int inst0) {
+    __shared__ double sh[kFoldB * 5];
+    double* p = partials + (inst0 + static_cast<uint64_t>(blockIdx.y)) * per * 5;
+    const uint64_t cnt = (per + S - 1) / S;
+    const uint64_t k0 = static_cast<uint64_t>(blockIdx.x) * kFoldB;
+    for (int x = threadIdx.x; x < kFoldB * 5; x += blockDim.x) {
+        const uint64_t k = k0 + x / 5;
+        sh[x] = k < cnt ? p[(k * S) * 5 + x % 5] : 0.0;
+    }
+    __syncthreads();
+    for (int s = 1; s < kFoldB; s <<= 1) {
+        const int i = threadIdx.x * 2 * s;
+        if (i < kFoldB && k0 + i + s < cnt) merge_words<T>(sh + i * 5, sh + (i + s) * 5);
         __syncthreads();
     }
+    if (threadIdx.x < 5) p[(k0 * S) * 5 + threadIdx.x] = sh[threadIdx.x];
 }
 
 // ------------------------------------------------------------ host side ----
@@ -1880,14 +1903,24 @@ class PlanImpl final : public Plan {
         if (use_levels_) {
             const int wpb = 4;
             const size_t sm = sizeof(T) * 4 * n_ * wpb;
+            const uint64_t lo = clo_ << (c_ - kbits_), hi = chi_ << (c_ - kbits_);
             for (int e = 1; e <= g_.c; ++e) {
-                const uint64_t items = (1ull << (e - 1)) * ninst_;
-                const uint64_t blocks = std::min<uint64_t>((items + wpb - 1) / wpb, 65535ull * 4);
-                prefix_level_kernel<T><<<static_cast<unsigned>(blocks), 32 * wpb, sm, st_>>>(g_, pool(), tpool(), e,
-                                                                                               ninst_, errw);
+                // only the level-e buffers under this plan's class range: the e-bit prefixes
+                // of [lo, hi) ending in an include, p = prefix >> 1 (a contiguous range)
+                const uint64_t plo = lo >> (c_ - e + 1), phi = (hi - 1) >> (c_ - e + 1);
+                const uint64_t cnt = phi - plo + 1;
+                const uint64_t items = cnt * ninst_;
+                // few nodes: several warps per elimination (>= 128 trailing entries each)
+                const int tot = tri_sz(2 * (n_ - e));
+                int parts = 1;
+                while (parts < 32 && items * parts * 2 <= static_cast<uint64_t>(sm_count_) * 8 &&
+                       tot / (parts * 2) >= 128)
+                    parts *= 2;
+                const uint64_t blocks = std::min<uint64_t>((items * parts + wpb - 1) / wpb, 65535ull * 4);
+                prefix_level_kernel<T><<<static_cast<unsigned>(blocks), 32 * wpb, sm, st_>>>(
+                    g_, pool(), tpool(), e, ninst_, plo, cnt, parts, errw);
                 ++launches;
             }
-            const uint64_t lo = clo_ << (c_ - kbits_), hi = chi_ << (c_ - kbits_);
             const uint64_t blocks = std::min<uint64_t>((njobs_ + 255) / 256, 1ull << 20);
             make_jobs_kernel<T><<<static_cast<unsigned>(blocks), 256, 0, st_>>>(g_, pool(), tpool(), ninst_, lo, hi,
                                                                                 jobs);
@@ -1915,8 +1948,15 @@ class PlanImpl final : public Plan {
         ++launches;
         CK(cudaGetLastError());
         CK(cudaEventRecord(ev_[2], st_));
-        fold_kernel<T><<<ninst_, 256, 0, st_>>>(parts, per_);
-        ++launches;
+        for (uint64_t S = 1; S < per_; S *= kFoldB) {
+            const uint64_t cnt = (per_ + S - 1) / S;
+            for (int i0 = 0; i0 < ninst_; i0 += 65535) {
+                const int ni = std::min(ninst_ - i0, 65535);
+                fold_pass_kernel<T><<<dim3(static_cast<unsigned>((cnt + kFoldB - 1) / kFoldB), ni), kFoldB / 2, 0,
+                                      st_>>>(parts, per_, S, i0);
+                ++launches;
+            }
+        }
         CK(cudaGetLastError());
         CK(cudaEventRecord(ev_[3], st_));
         std::vector<double> res(static_cast<size_t>(ninst_) * 5);
@@ -2062,7 +2102,7 @@ int engine_run(int device, int mode, const std::vector<PreparedInput>& inputs, c
 }
 
 void fold_words(int mode, const double* parts, int count, double* out5) {
-    // same pairwise tree as fold_kernel over `count` shard partials (5 doubles each)
+    // same pairwise tree as fold_pass_kernel over `count` shard partials (5 doubles each)
     std::vector<double> p(parts, parts + 5 * static_cast<size_t>(count));
     for (int s = 1; s < count; s <<= 1)
         for (int i = 0; i + s < count; i += 2 * s) {
