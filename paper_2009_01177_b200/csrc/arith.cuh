@@ -69,12 +69,21 @@ TOR_HD bool nonpositive(double x) {
 #endif
 }
 
-// Full-precision fp64 reciprocal square root for x > 0.
-TOR_HD double rsqrt_d(double x) {
+// fp64 reciprocal square root seed: MUFU.RSQ64H (~2^-23 relative).
+TOR_HD double rsqrt_seed(double x) {
 #if defined(__CUDA_ARCH__)
-    // MUFU.RSQ64H seed (~2^-23) then two Newton steps in fp64 -> ~1 ulp.
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+#else
+    return 1.0 / std::sqrt(x);
+#endif
+}
+// Two fp64 Newton steps from the seed y ~ 1/sqrt(x) -> ~1 ulp.  The seed may come from
+// an approximation of x (e.g. an unnormalised leading word): the steps converge to
+// 1/sqrt(x) for any seed within a few 2^-20 of it.
+TOR_HD double rsqrt_newton(double x, double y) {
+#if defined(__CUDA_ARCH__)
     double h = x * y;
     double r = fma_(-h, y, 1.0);
     y = fma_(0.5 * y, r, y);
@@ -83,9 +92,12 @@ TOR_HD double rsqrt_d(double x) {
     y = fma_(0.5 * y, r, y);
     return y;
 #else
+    (void)y;
     return 1.0 / std::sqrt(x);
 #endif
 }
+// Full-precision fp64 reciprocal square root for x > 0.
+TOR_HD double rsqrt_d(double x) { return rsqrt_newton(x, rsqrt_seed(x)); }
 
 // ===================================================================== DD ==
 struct dd {
@@ -212,10 +224,11 @@ TOR_HD dd dd_rank1_grid(dd s, dd a, dd b) {
     return dd{z1 - kGridC, lo};
 }
 
-// 1/sqrt(x) for normalised x > 0: fp64 seed + one DD Newton step on the exact
-// residual r = 1 - x*y^2 (y^2 exact by TwoProd).  Result is (y, y*r/2), |lo| <= ulp.
-TOR_HD dd dd_rsqrt(dd x) {
-    const double y = rsqrt_d(x.hi);
+// 1/sqrt(x) for normalised x > 0 from the fp64 seed y0 (of x.hi or an approximation
+// of it): fp64 Newton to ~1 ulp, then one DD Newton step on the exact residual
+// r = 1 - x*y^2 (y^2 exact by TwoProd).  Result is (y, y*r/2), |lo| <= ulp.
+TOR_HD dd dd_rsqrt_seeded(dd x, double y0) {
+    const double y = rsqrt_newton(x.hi, y0);
     double p, pe;
     two_prod(y, y, p, pe);
     double r = fma_(-x.hi, p, 1.0);
@@ -223,6 +236,26 @@ TOR_HD dd dd_rsqrt(dd x) {
     r = fma_(-x.lo, p, r);
     const double c = (0.5 * y) * r;
     return dd{y, c};
+}
+TOR_HD dd dd_rsqrt(dd x) { return dd_rsqrt_seeded(x, rsqrt_seed(x.hi)); }
+
+// det [[a, b], [b, c]] = a c - b^2 for DD a, b, c: TwoProds of the leading words, ONE
+// TwoSum for the (possibly cancelling) difference, the cross products into the low word,
+// then a fast renormalisation.  h (the rounded leading difference, available a few
+// operations in) is a good enough seed argument for the reciprocal square root.
+TOR_HD dd dd_det2(const dd& a, const dd& b, const dd& c, double& h) {
+    const double p = a.hi * c.hi;
+    const double pe = fma_(a.hi, c.hi, -p);
+    const double q = b.hi * b.hi;
+    const double qe = fma_(b.hi, b.hi, -q);
+    double he;
+    two_sum(p, -q, h, he);
+    double t = fma_(a.hi, c.lo, a.lo * c.hi);
+    t = fma_(-2.0 * b.hi, b.lo, t);
+    const double lo = (he + (pe - qe)) + t;
+    dd r;
+    fast_two_sum(h, lo, r.hi, r.lo);
+    return r;
 }
 
 // ===================================================================== QD ==
@@ -462,6 +495,45 @@ TOR_HD Piv<T> pivot2(const T& s00, const T& s01, const T& s11, const T& t) {
     p.r2 = A::mul(A::mul(a, p.r1), rd);
     p.tn = A::mul(t, rd);
     return p;
+}
+
+// DD: the two reciprocal square roots start from seeds of the un-normalised leading
+// words (MUFU latency overlaps the renormalisations), det by dd_det2 (one TwoSum).
+template <>
+TOR_HD Piv<dd> pivot2<dd>(const dd& s00, const dd& s01, const dd& s11, const dd& t) {
+    using A = Arith<dd>;
+    Piv<dd> p;
+    const dd a0 = A::unb(s00), b = A::unb(s01), c = A::unb(s11);
+    const double y1 = rsqrt_seed(a0.hi);
+    const dd a = dd_norm(a0);
+    p.bad0 = nonpositive(a.hi);
+    double h;
+    const dd det = dd_det2(a0, b, c, h);
+    const double yd = rsqrt_seed(h);
+    p.bad1 = nonpositive(det.hi);
+    p.r1 = dd_rsqrt_seeded(a, y1);
+    const dd rd = dd_rsqrt_seeded(det, yd);
+    p.u1 = A::mul(b, p.r1);
+    p.r2 = A::mul(A::mul(a, p.r1), rd);
+    p.tn = A::mul(t, rd);
+    return p;
+}
+// Term factor of a one-mode (leaf) state: t / sqrt(det).
+template <class T>
+TOR_HD T leaf_term(const T& s00, const T& s01, const T& s11, const T& t, bool& bad) {
+    using A = Arith<T>;
+    const T b = A::unb(s01);
+    const T det = A::norm(A::rank1(A::mul(A::unb(s00), A::unb(s11)), b, b));
+    bad = nonpositive(A::hi(det));
+    return A::mul(t, A::rsqrt(det));
+}
+template <>
+TOR_HD dd leaf_term<dd>(const dd& s00, const dd& s01, const dd& s11, const dd& t, bool& bad) {
+    using A = Arith<dd>;
+    double h;
+    const dd det = dd_det2(A::unb(s00), A::unb(s01), A::unb(s11), h);
+    bad = nonpositive(det.hi);
+    return A::mul(t, dd_rsqrt_seeded(det, rsqrt_seed(h)));
 }
 
 // ========================================================== accumulators ==

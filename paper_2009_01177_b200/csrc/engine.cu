@@ -575,11 +575,9 @@ template <class T, int Q> struct SubReg {
 template <class T> struct SubReg<T, 1> {
     __device__ __forceinline__ static void run(const St<T, 1>& S, const T& t, bool neg, uint64_t mask, int nsel,
                                                Acc<T>& acc, unsigned long long* err) {
-        using A = Arith<T>;
-        const T s01 = A::unb(S.e[1]);
-        const T det = A::norm(A::rank1(A::mul(A::unb(S.e[0]), A::unb(S.e[2])), s01, s01));
-        if (nonpositive(A::hi(det))) report_breakdown(err, mask | 1ull, 2 * nsel + 1);
-        const T tn = A::mul(t, A::rsqrt(det));
+        bool bad;
+        const T tn = leaf_term<T>(S.e[0], S.e[1], S.e[2], t, bad);
+        if (bad) report_breakdown(err, mask | 1ull, 2 * nsel + 1);
         acc.add(tn, !neg, nsel + 1);
     }
 };
