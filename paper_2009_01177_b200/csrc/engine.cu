@@ -111,6 +111,13 @@ template <> struct Cfg<qd> {
 
 template <class T> constexpr int root_modes() { return Cfg<T>::L + FAN; }
 
+// WS mode 2: first fan-out level run by the consumer warps (the producers run the DFS
+// and levels 1 .. kConsFirst-1)
+#ifndef TOR_CONS_FIRST
+#define TOR_CONS_FIRST 3
+#endif
+constexpr int kConsFirst = TOR_CONS_FIRST;
+
 constexpr int kIjTabEntries = ijtab_off(kMaxJobModes);
 __device__ uint32_t g_ijtab[kIjTabEntries];
 
@@ -1327,7 +1334,8 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         PHASE_MARK(1);
         FanLevel<T, 1>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
         FanLevel<T, 2>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
-        FanLevel<T, 3>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
+        if constexpr (Cfg<T>::WS_MODE != 2 || kConsFirst > 3)
+            FanLevel<T, 3>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
         if constexpr (Cfg<T>::WS_MODE != 2) FanLevel<T, 4>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
         if constexpr (!Cfg<T>::WS) FanLevel<T, 5>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
     };
@@ -1442,6 +1450,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 const unsigned long long job = meta[c].job;
                 const int leaf_sel = meta[c].sel, flags = meta[c].flags;
                 if (flags & 2) break;
+                if constexpr (kConsFirst <= 3) FanLevel<T, 3>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
                 FanLevel<T, 4>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
                 FanLevel<T, FAN>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
                 const T vt = ctv[node_ref<T>(tabs, FAN, lane).tix];

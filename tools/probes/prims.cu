@@ -31,11 +31,10 @@ __device__ double sink(const Acc<qd>& a) { return a.s.x[0] + a.s.x[1] + a.s.x[2]
         flags[i] = p.bad0 | (p.bad1 << 1);                                                     \
     }                                                                                          \
     extern "C" __global__ void leaf_##NAME(const T* in, T* out, int* flags) {                 \
-        using A = Arith<T>;                                                                    \
         const int i = threadIdx.x;                                                             \
-        const T det = A::norm(A::rank1(A::mul(in[i], in[i + 64]), in[i + 32], in[i + 32]));  \
-        flags[i] = nonpositive(A::hi(det));                                                    \
-        out[i] = A::mul(in[i + 96], A::rsqrt(det));                                            \
+        bool bad;                                                                              \
+        out[i] = leaf_term<T>(in[i], in[i + 32], in[i + 64], in[i + 96], bad);                 \
+        flags[i] = bad;                                                                        \
     }                                                                                          \
     extern "C" __global__ void accadd1_##NAME(const T* in, double* out, const int* z) {        \
         const int i = threadIdx.x;                                                             \
