@@ -589,6 +589,62 @@ template <class T> struct SubReg<T, 1> {
     }
 };
 
+// Two independent 2-mode register states A and B (their own terms already emitted):
+// all 3 + 3 extension terms, written as one straight-line block so the two pivot chains
+// and the four leaf chains overlap (instruction-level parallelism for the lane
+// subtrees, whose chains are otherwise serial).  Breakdowns are collected and reported
+// after the block.  Terms are added in SubReg<2>'s order (A0, A00, A1, B0, B00, B1).
+template <class T>
+__device__ __forceinline__ void sub2_pair(const St<T, 2>& SA, const T& tA, bool negA, uint64_t maskA, int nselA,
+                                          const St<T, 2>& SB, const T& tB, bool negB, uint64_t maskB, int nselB,
+                                          Acc<T>& acc, unsigned long long* err) {
+    using A = Arith<T>;
+    const Piv<T> pa = piv_lt<T>(SA.e[0], SA.e[1], SA.e[4], tA);
+    const Piv<T> pb = piv_lt<T>(SB.e[0], SB.e[1], SB.e[4], tB);
+    St<T, 1> ca, cb;
+    {
+        T u[4], w[4];
+#pragma unroll
+        for (int j = 2; j < 4; ++j) {
+            u[j] = A::mul(A::unb(SA.e[cix<4>(0, j)]), pa.r1);
+            w[j] = A::mul(A::rank1s(SA.e[cix<4>(1, j)], pa.u1, u[j]), pa.r2);
+        }
+        ca.e[0] = A::rank2(SA.e[cix<4>(2, 2)], u[2], u[2], w[2], w[2]);
+        ca.e[1] = A::rank2(SA.e[cix<4>(2, 3)], u[2], u[3], w[2], w[3]);
+        ca.e[2] = A::rank2(SA.e[cix<4>(3, 3)], u[3], u[3], w[3], w[3]);
+    }
+    {
+        T u[4], w[4];
+#pragma unroll
+        for (int j = 2; j < 4; ++j) {
+            u[j] = A::mul(A::unb(SB.e[cix<4>(0, j)]), pb.r1);
+            w[j] = A::mul(A::rank1s(SB.e[cix<4>(1, j)], pb.u1, u[j]), pb.r2);
+        }
+        cb.e[0] = A::rank2(SB.e[cix<4>(2, 2)], u[2], u[2], w[2], w[2]);
+        cb.e[1] = A::rank2(SB.e[cix<4>(2, 3)], u[2], u[3], w[2], w[3]);
+        cb.e[2] = A::rank2(SB.e[cix<4>(3, 3)], u[3], u[3], w[3], w[3]);
+    }
+    bool b1, b2, b3, b4;
+    const T la0 = leaf_term<T>(ca.e[0], ca.e[1], ca.e[2], pa.tn, b1);
+    const T la1 = leaf_term<T>(SA.e[cix<4>(2, 2)], SA.e[cix<4>(2, 3)], SA.e[cix<4>(3, 3)], tA, b2);
+    const T lb0 = leaf_term<T>(cb.e[0], cb.e[1], cb.e[2], pb.tn, b3);
+    const T lb1 = leaf_term<T>(SB.e[cix<4>(2, 2)], SB.e[cix<4>(2, 3)], SB.e[cix<4>(3, 3)], tB, b4);
+    acc.add(pa.tn, !negA, nselA + 1);
+    acc.add(la0, negA, nselA + 2);
+    acc.add(la1, !negA, nselA + 1);
+    acc.add(pb.tn, !negB, nselB + 1);
+    acc.add(lb0, negB, nselB + 2);
+    acc.add(lb1, !negB, nselB + 1);
+    if (pa.bad0 || pa.bad1 || pb.bad0 || pb.bad1 || b1 || b2 || b3 || b4) {
+        if (pa.bad0 || pa.bad1) report_breakdown(err, maskA | 2ull, 2 * nselA + (pa.bad0 ? 0 : 1));
+        if (b1) report_breakdown(err, maskA | 3ull, 2 * nselA + 3);
+        if (b2) report_breakdown(err, maskA | 1ull, 2 * nselA + 1);
+        if (pb.bad0 || pb.bad1) report_breakdown(err, maskB | 2ull, 2 * nselB + (pb.bad0 ? 0 : 1));
+        if (b3) report_breakdown(err, maskB | 3ull, 2 * nselB + 3);
+        if (b4) report_breakdown(err, maskB | 1ull, 2 * nselB + 1);
+    }
+}
+
 // Lane subtree rooted at an L-mode view in shared memory: emits the node's own
 // term and all 2^L - 1 extensions.  Branch 0 includes the first view mode (its
 // elimination reads shared memory), branch 1 excludes it (loads the trailing block).
@@ -851,6 +907,45 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
     constexpr int K01 = 2 * M - 1;  // entries of rows 0 and 1
     constexpr int NT = tri_sz(M - 2);
     const uint64_t bit = 1ull << (L - 1);
+#ifndef TOR_PAIR3
+#define TOR_PAIR3 0
+#endif
+    if constexpr (L == 3 && TOR_PAIR3) {
+        // both children (2 modes) in registers, then their subtrees as one pair
+        St<T, 2> Sa, Sb;
+        T ta;
+        bool bad0, bad1;
+        {
+            uint32_t r0[4 * K01];
+            tm_ld_entries<M, 0, K01>(row, r0);
+            tm_wait_ld();
+            T e0[K01];
+#pragma unroll
+            for (int k = 0; k < K01; ++k) e0[k] = u32_to_dd(r0[4 * k], r0[4 * k + 1], r0[4 * k + 2], r0[4 * k + 3]);
+            const Piv<T> pv = piv_lt<T>(e0[0], e0[1], e0[M], t);
+            bad0 = pv.bad0;
+            bad1 = pv.bad1;
+            ta = pv.tn;
+            T u[M], w[M];
+#pragma unroll
+            for (int j = 2; j < M; ++j) {
+                u[j] = A::mul(A::unb(e0[j]), pv.r1);
+                w[j] = A::mul(A::rank1s(e0[M + j - 1], pv.u1, u[j]), pv.r2);
+            }
+            lt_wave<T, M, 0, NT>(row, u, w, Sa);
+        }
+        {
+            uint32_t rt[4 * NT];
+            tm_ld_entries<M, K01, NT>(row, rt);
+            tm_wait_ld();
+#pragma unroll
+            for (int kk = 0; kk < NT; ++kk) Sb.e[kk] = u32_to_dd(rt[4 * kk], rt[4 * kk + 1], rt[4 * kk + 2], rt[4 * kk + 3]);
+        }
+        if (bad0 || bad1) report_breakdown(err, mask | bit, 2 * nsel + (bad0 ? 0 : 1));
+        acc.add(ta, !neg, nsel + 1);
+        sub2_pair<T>(Sa, ta, !neg, mask | bit, nsel + 1, Sb, t, neg, mask, nsel, acc, err);
+        return;
+    }
 #pragma unroll 1
     for (int br = 0; br < 2; ++br) {
         T tn;
