@@ -1047,10 +1047,22 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
 template <class T> struct WarpSmem {
     static constexpr int L = Cfg<T>::L;
     static constexpr int Q0 = L + FAN;
+    // Level-e include buffers: base lvl_off(e), child x at + x * buf_stride(e).  For the
+    // TMEM (DD) layout the level-1 base is padded by 2 entries, the level-2 base by 1 and
+    // the level-2 stride by 1 (5 entries per area): the 16 level-4 node states (level-5
+    // parents, read lane-pair-wise by FanLevel<5>) then start on every 16-byte bank slot
+    // mod 8 exactly twice and the 8 level-3 nodes on distinct slots, so those reads are
+    // free of bank conflicts (found by exhaustive search over small paddings).
+    __host__ __device__ static constexpr int lvl_pad(int e) {
+        return Cfg<T>::TMEM ? (e == 1 ? 2 : (e == 2 ? 1 : 0)) : 0;
+    }
+    __host__ __device__ static constexpr int buf_stride(int e) {
+        return tri_sz(2 * (Q0 - e)) + (Cfg<T>::TMEM && e == 2 ? 1 : 0);
+    }
     __host__ __device__ static constexpr int lvl_off(int e) {
         int o = tri_sz(2 * Q0);
-        for (int x = 1; x < e; ++x) o += (1 << (x - 1)) * tri_sz(2 * (Q0 - x));
-        return e == 0 ? 0 : o;
+        for (int x = 1; x < e; ++x) o += lvl_pad(x) + (1 << (x - 1)) * buf_stride(x);
+        return e == 0 ? 0 : o + lvl_pad(e);
     }
     // with TMEM the last level's include states never touch shared memory
     static constexpr int kBufEntries = Cfg<T>::TMEM ? lvl_off(FAN) : lvl_off(FAN + 1);
@@ -1111,7 +1123,7 @@ __device__ __forceinline__ int node_off(int e, int c) {
     const int lvl = e - tz;
     const int p = (c >> tz) >> 1;
     const int dim = 2 * (Q0 - lvl);
-    return WarpSmem<T>::lvl_off(lvl) + p * tri_sz(dim) + tri_ix(dim, 2 * tz, 2 * tz);
+    return WarpSmem<T>::lvl_off(lvl) + p * WarpSmem<T>::buf_stride(lvl) + tri_ix(dim, 2 * tz, 2 * tz);
 }
 __device__ __forceinline__ int node_tix(int e, int c) {
     if (c == 0) return 31;
@@ -1281,7 +1293,11 @@ template <class T, int E_LVL> struct FanLevel {
 #pragma unroll
             for (int u = 0; u < UB; ++u) {
                 const int s = s0 + u;
-                if (s < NIT && (s < NIT - 1 || lane + 32 * s < NE)) out[32 * s] = sv[u];
+                if (s < NIT && (s < NIT - 1 || lane + 32 * s < NE)) {
+                    constexpr int kAdd = WarpSmem<T>::buf_stride(E_LVL) - tn;  // padded child stride
+                    if constexpr (kAdd == 0) out[32 * s] = sv[u];
+                    else out[32 * s + ((lane + 32 * s) / tn) * kAdd] = sv[u];
+                }
             }
         }
         __syncwarp();
