@@ -1190,10 +1190,75 @@ template <class T, int E_LVL> struct FanLevel {
     static constexpr int m = 2 * q;
     static constexpr int dn = m - 2;
     static constexpr int tn = tri_sz(dn);
+    // Last level -> TMEM, lane-pair form: lanes (2x, 2x+1) own parent x (level-4 node
+    // x) throughout.  Both compute its pivots; the even lane forms u_j, w_j for
+    // j = 2..5, the odd lane for j = 9..6 (reversed), and the halves cross by shuffle,
+    // so each lane holds all eight (the odd lane in mirrored order) without a shared-
+    // memory round trip.  Then the mirror-split update (MirChunk): lane 2x+1 owns the
+    // include child x, lane 2x the exclude child (parent x's trailing block); the
+    // include child's entries split by the anti-transpose mirror (i,j) -> (7-j,7-i)
+    // so (i,j) are compile-time for both lanes; each lane stores its node's state to
+    // its own TMEM row in mir_slot order.
+    __device__ __forceinline__ static void run_tmem_pairs(T* sm, T* tvals, const uint32_t* tabs, uint64_t leaf_mask,
+                                                          int leaf_sel, unsigned long long* err, uint32_t tm_row) {
+        using A = Arith<T>;
+        static_assert(dn == kMirD && tn == 36 && E == 16, "mirror split layout");
+        const int lane = threadIdx.x & 31;
+        const int xe = lane >> 1, h = lane & 1;
+        const NodeRef nr = node_ref<T>(tabs, E_LVL - 1, xe);
+        const T* P = sm + nr.off;
+        const Piv<T> pv = pivot2<T>(P[0], P[1], P[m], tvals[nr.tix]);
+        T a[4], b[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const int j = h ? m - 1 - s : 2 + s;
+            a[s] = P[j];
+            b[s] = P[m - 1 + j];
+        }
+        if (h == 0) {
+            const uint64_t nm = leaf_mask | (static_cast<uint64_t>((xe << 1) | 1) << (Q0 - E_LVL));
+            if (pv.bad0 || pv.bad1) report_breakdown(err, nm, 2 * (leaf_sel + __popc(xe)) + (pv.bad0 ? 0 : 1));
+            tvals[E - 1 + xe] = pv.tn;  // level e-1 t values live below index E-1: no hazard
+        }
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            a[s] = A::mul(A::unb(a[s]), pv.r1);
+            b[s] = A::mul(A::rank1s(b[s], pv.u1, a[s]), pv.r2);
+        }
+        T u[dn], w[dn];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            u[s] = a[s];
+            w[s] = b[s];
+            u[4 + s] = shfl_xor_t(a[3 - s], 1);
+            w[4 + s] = shfl_xor_t(b[3 - s], 1);
+        }
+        const T* Pt = P + 2 * m - 1;
+        MirChunk<T, m, 0>::run(Pt, u, w, h, tm_row);
+        {
+            uint32_t r[16];
+#pragma unroll
+            for (int a2 = 0; a2 < 4; ++a2) {
+                const T sv = Pt[cix<dn>(a2, dn - 1 - a2)];
+                const T v = A::rank2(sv, u[dn - 1 - a2], u[a2], w[dn - 1 - a2], w[a2]);
+                if constexpr (sizeof(T) == sizeof(dd)) dd_to_u32(h ? v : sv, r + 4 * a2);
+            }
+            tm_st16(tm_row + 16 * 8, r);
+        }
+        tm_wait_st();
+        __syncwarp();
+    }
     __device__ __forceinline__ static void run(T* sm, T* tvals, T* uwv, const uint32_t* tabs, uint64_t leaf_mask,
                                                int leaf_sel, unsigned long long* err, uint32_t tm_row) {
         using A = Arith<T>;
         const int lane = threadIdx.x & 31;
+#ifndef TOR_L5_SHFL
+#define TOR_L5_SHFL 0
+#endif
+        if constexpr (Cfg<T>::TMEM && E_LVL == FAN && TOR_L5_SHFL) {
+            run_tmem_pairs(sm, tvals, tabs, leaf_mask, leaf_sel, err, tm_row);
+            return;
+        }
         const int x = lane & (E - 1), g = lane / E;
         PHASE_T0();
         const NodeRef nr = node_ref<T>(tabs, E_LVL - 1, x);
