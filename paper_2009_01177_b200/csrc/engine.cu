@@ -101,9 +101,15 @@ template <> struct Cfg<dd> {
     static constexpr bool TMEM = TOR_DD_TMEM;
 };
 template <> struct Cfg<qd> {
-    static constexpr int L = 3;
+#ifndef TOR_QD_L
+#define TOR_QD_L 3
+#endif
+#ifndef TOR_QD_MINB
+#define TOR_QD_MINB 1
+#endif
+    static constexpr int L = TOR_QD_L;
     static constexpr int WPB = 1;
-    static constexpr int MINB = 1;
+    static constexpr int MINB = TOR_QD_MINB;
     static constexpr bool TMEM = false;
     static constexpr bool WS = false;
     static constexpr int WS_MODE = 0;
@@ -117,6 +123,11 @@ template <class T> constexpr int root_modes() { return Cfg<T>::L + FAN; }
 #define TOR_CONS_FIRST 3
 #endif
 constexpr int kConsFirst = TOR_CONS_FIRST;
+// ... and the producers take level 3 of a leaf whenever they would otherwise wait
+#ifndef TOR_STEAL_L3
+#define TOR_STEAL_L3 0
+#endif
+constexpr bool kStealL3 = TOR_STEAL_L3;
 
 constexpr int kIjTabEntries = ijtab_off(kMaxJobModes);
 __device__ uint32_t g_ijtab[kIjTabEntries];
@@ -1546,6 +1557,8 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         };
         __shared__ WsMeta meta[8];
         __shared__ __align__(8) unsigned long long mbar[16];  // full[0..7], empty[8..15]
+        __shared__ int cbusy[8];  // consumer c is in its lane subtrees (level-3 stealing hint)
+        if (threadIdx.x < 8) cbusy[threadIdx.x] = 0;
         if (threadIdx.x < 16) {
             const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[threadIdx.x]));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(32) : "memory");
@@ -1555,6 +1568,16 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         auto mb_arrive = [&](int i) {
             const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[i]));
             asm volatile("{.reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0];}\n" ::"r"(a) : "memory");
+        };
+        auto mb_test = [&](int i, uint32_t parity) {
+            const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[i]));
+            uint32_t ok;
+            asm volatile(
+                "{.reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p;}\n"
+                : "=r"(ok)
+                : "r"(a), "r"(parity)
+                : "memory");
+            return __shfl_sync(0xffffffffu, ok, 0) != 0;
         };
         auto mb_wait = [&](int i, uint32_t parity) {
             const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[i]));
@@ -1592,11 +1615,26 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                     mb_wait(8 + c, (uses[s] & 1) ^ 1);
                     T* cslots = scratch + (static_cast<size_t>(blockIdx.x * 4 + p) * 2 + s) * scratch_stride;
                     produce_leaf(J[s], leaf[s], 0u, area(c), dfs_t + 32 * s, cslots);
+                    // Dynamic balance: when the other context's consumer still holds its
+                    // area (the producer would wait there anyway), run this leaf's level 3
+                    // here instead of on the consumer.
+                    bool l3 = false;
+                    if constexpr (kConsFirst == 3 && kStealL3) {
+                        // ... i.e. while consumer c is still in its lane subtrees
+                        int busy = 0;
+                        if (lane == 0) busy = *reinterpret_cast<volatile int*>(&cbusy[c]);
+                        l3 = __shfl_sync(0xffffffffu, busy, 0) != 0;
+                        if (l3) {
+                            const uint64_t lm = J[s].mask | (leaf[s] << Q0);
+                            FanLevel<T, 3>::run(area(c), area(c) + SM::kTOff, uwv, tabs, lm,
+                                                J[s].nsel + __popcll(leaf[s]), err, 0u);
+                        }
+                    }
                     if (lane == 0) {
                         meta[c].mask = J[s].mask | (leaf[s] << Q0);
                         meta[c].job = jid[s];
                         meta[c].sel = J[s].nsel + __popcll(leaf[s]);
-                        meta[c].flags = leaf[s] + 1 == (1ull << D) ? 1 : 0;
+                        meta[c].flags = (leaf[s] + 1 == (1ull << D) ? 1 : 0) | (l3 ? 4 : 0);
                     }
                     __syncwarp();
                     mb_arrive(c);
@@ -1626,17 +1664,22 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 const unsigned long long job = meta[c].job;
                 const int leaf_sel = meta[c].sel, flags = meta[c].flags;
                 if (flags & 2) break;
-                if constexpr (kConsFirst <= 3) FanLevel<T, 3>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
+                if constexpr (kConsFirst <= 3)
+                    if (!(flags & 4)) FanLevel<T, 3>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
                 FanLevel<T, 4>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
                 FanLevel<T, FAN>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
                 const T vt = ctv[node_ref<T>(tabs, FAN, lane).tix];
                 __syncwarp();
+                if constexpr (kConsFirst == 3 && kStealL3)
+                    if (lane == 0) *reinterpret_cast<volatile int*>(&cbusy[c]) = 1;
                 mb_arrive(8 + c);  // the producer may refill root..L3 and t values 0..6, 31
                 const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(lane) << L);
                 const int lsel = leaf_sel + __popc(lane);
                 const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
                 acc.add(vt, nodeneg, lsel);
                 tmem_ext<T, L>(crow, crow + 4 * tri_sz(2 * L), vt, nodeneg, lmask, lsel, acc, err);
+                if constexpr (kConsFirst == 3 && kStealL3)
+                    if (lane == 0) *reinterpret_cast<volatile int*>(&cbusy[c]) = 0;
                 acc.flush();
                 if (flags & 1) {
                     write_partial(acc, job);

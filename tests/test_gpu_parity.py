@@ -295,3 +295,18 @@ def test_full_pipeline_dd_vs_qd(n):
     assert ok, f"n={n}: DD vs QD {rel:.3g} sum|t|"
     assert rel < 2.0 ** -100
     assert abs(dd["sum_abs_terms"] - q["sum_abs_terms"]) <= 1e-12 * q["sum_abs_terms"]
+
+
+@pytest.mark.parametrize("prec,mode", [("128", "dd"), ("256", "qd"), ("fp64", "fp64")])
+def test_uneven_class_ranges(prec, mode):
+    # class ranges that are not aligned powers of two (ragged prefix-level ranges, a
+    # fixed-order fold over a non-power-of-two job count): the pieces add up to the whole
+    m = W.load_config_instance(2)
+    whole = T.torontonian(m, prec)
+    for k, cuts in ((3, (0, 3, 8)), (5, (0, 1, 7, 19, 32)), (9, (0, 100, 301, 512))):
+        parts = [T.torontonian_slice(m, prec, k, a, b) for a, b in zip(cuts, cuts[1:])]
+        total = sum((words_value(p["words"]) for p in parts), start=words_value([0.0]))
+        sum_abs = sum(p["sum_abs"] for p in parts)
+        assert sum_abs == pytest.approx(whole["sum_abs_terms"], rel=1e-12)
+        ok, rel = within(total, words_value(whole["words"]), whole["sum_abs_terms"], mode)
+        assert ok, f"k={k} cuts={cuts}: {rel:.3g} sum|t|"
