@@ -69,21 +69,24 @@ TOR_HD bool nonpositive(double x) {
 #endif
 }
 
-// fp64 reciprocal square root seed: MUFU.RSQ64H (~2^-23 relative).
+// fp64 reciprocal square root seed: MUFU.RSQ64H (~2^-23 relative).  The host build
+// (arithmetic unit tests) emulates the seed's accuracy by truncating 1/sqrt(x) to its
+// leading 20 significand bits, so the Newton steps below run on the same path.
 TOR_HD double rsqrt_seed(double x) {
 #if defined(__CUDA_ARCH__)
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
     return y;
 #else
-    return 1.0 / std::sqrt(x);
+    int e;
+    const double f = std::frexp(1.0 / std::sqrt(x), &e);
+    return std::ldexp(std::floor(std::ldexp(f, 20)), e - 20);
 #endif
 }
 // Two fp64 Newton steps from the seed y ~ 1/sqrt(x) -> ~1 ulp.  The seed may come from
 // an approximation of x (e.g. an unnormalised leading word): the steps converge to
 // 1/sqrt(x) for any seed within a few 2^-20 of it.
 TOR_HD double rsqrt_newton(double x, double y) {
-#if defined(__CUDA_ARCH__)
     double h = x * y;
     double r = fma_(-h, y, 1.0);
     y = fma_(0.5 * y, r, y);
@@ -91,10 +94,6 @@ TOR_HD double rsqrt_newton(double x, double y) {
     r = fma_(-h, y, 1.0);
     y = fma_(0.5 * y, r, y);
     return y;
-#else
-    (void)y;
-    return 1.0 / std::sqrt(x);
-#endif
 }
 // Full-precision fp64 reciprocal square root for x > 0.
 TOR_HD double rsqrt_d(double x) { return rsqrt_newton(x, rsqrt_seed(x)); }
@@ -239,9 +238,9 @@ TOR_HD dd dd_rsqrt_seeded(dd x, double y0) {
 }
 TOR_HD dd dd_rsqrt(dd x) { return dd_rsqrt_seeded(x, rsqrt_seed(x.hi)); }
 
-// det [[a, b], [b, c]] = a c - b^2 for DD a, b, c: TwoProds of the leading words, ONE
-// TwoSum for the (possibly cancelling) difference, the cross products into the low word,
-// then a fast renormalisation.  h (the rounded leading difference, available a few
+// det [[a, b], [b, c]] = a c - b^2 for DD a, b, c (possibly un-normalised): TwoProds of
+// the leading words, ONE TwoSum for the (possibly cancelling) difference, the cross and
+// low*low products into the low word, then a fast renormalisation.  h (the rounded leading difference, available a few
 // operations in) is a good enough seed argument for the reciprocal square root.
 TOR_HD dd dd_det2(const dd& a, const dd& b, const dd& c, double& h) {
     const double p = a.hi * c.hi;
@@ -252,6 +251,9 @@ TOR_HD dd dd_det2(const dd& a, const dd& b, const dd& c, double& h) {
     two_sum(p, -q, h, he);
     double t = fma_(a.hi, c.lo, a.lo * c.hi);
     t = fma_(-2.0 * b.hi, b.lo, t);
+    // grid state entries are un-normalised (|lo| up to 2^-50 absolute): keep lo*lo
+    t = fma_(a.lo, c.lo, t);
+    t = fma_(-b.lo, b.lo, t);
     const double lo = (he + (pe - qe)) + t;
     dd r;
     fast_two_sum(h, lo, r.hi, r.lo);
