@@ -362,14 +362,169 @@ TOR_HD qd qd_mul_d(const qd& a, double b) {
     return qd_renorm5_bf(s0, s1, s2, s3, s4);
 }
 
+// Fused s - a*b - c*d with ONE renormalisation (instead of two products and two sums,
+// each renormalised).  Terms are collected by order (2^-53k of the operands' scale):
+// order 0..2 products by TwoProd, order 3 plainly; each order is summed exactly with
+// TwoSums whose errors drop to the next order; order 3 is summed plainly.  Error
+// ~2^-208 of max(|s|, |ab|, |cd|) (tests/test_arith.py).
+#ifndef TOR_QD_LAZY
+#define TOR_QD_LAZY 1
+#endif
+constexpr bool kQdLazy = TOR_QD_LAZY;
+struct QAcc {  // exact running sum of one order; errors go to the next order's list
+    double h;
+    TOR_HD void add(double t, double& err) {
+        double e;
+        two_sum(h, t, h, e);
+        err = e;
+    }
+};
+template <bool kNorm>
+TOR_HD_RNI qd qd_rank2_fused(qd s, qd a, qd b, qd c, qd d) {
+    double p0, e0, q0, f0;
+    two_prod(a.x[0], b.x[0], p0, e0);
+    two_prod(c.x[0], d.x[0], q0, f0);
+    double l1[8];
+    QAcc o0{s.x[0]};
+    o0.add(-p0, l1[0]);
+    o0.add(-q0, l1[1]);
+    // order 1
+    double pa, ea, pb, eb, qa, fa, qb, fb;
+    two_prod(a.x[0], b.x[1], pa, ea);
+    two_prod(a.x[1], b.x[0], pb, eb);
+    two_prod(c.x[0], d.x[1], qa, fa);
+    two_prod(c.x[1], d.x[0], qb, fb);
+    QAcc o1{s.x[1]};
+    double l2[18];
+    o1.add(l1[0], l2[0]);
+    o1.add(l1[1], l2[1]);
+    o1.add(-e0, l2[2]);
+    o1.add(-f0, l2[3]);
+    o1.add(-pa, l2[4]);
+    o1.add(-pb, l2[5]);
+    o1.add(-qa, l2[6]);
+    o1.add(-qb, l2[7]);
+    // order 2
+    double r[6], re[6];
+    two_prod(a.x[0], b.x[2], r[0], re[0]);
+    two_prod(a.x[1], b.x[1], r[1], re[1]);
+    two_prod(a.x[2], b.x[0], r[2], re[2]);
+    two_prod(c.x[0], d.x[2], r[3], re[3]);
+    two_prod(c.x[1], d.x[1], r[4], re[4]);
+    two_prod(c.x[2], d.x[0], r[5], re[5]);
+    QAcc o2{s.x[2]};
+    double l3[18];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o2.add(l2[i], l3[i]);
+    o2.add(-ea, l3[8]);
+    o2.add(-eb, l3[9]);
+    o2.add(-fa, l3[10]);
+    o2.add(-fb, l3[11]);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) o2.add(-r[i], l3[12 + i]);
+    // order 3: plain
+    double h3 = s.x[3];
+#pragma unroll
+    for (int i = 0; i < 18; ++i) h3 += l3[i];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) h3 -= re[i];
+    double t3 = a.x[0] * b.x[3];
+    t3 = fma_(a.x[1], b.x[2], t3);
+    t3 = fma_(a.x[2], b.x[1], t3);
+    t3 = fma_(a.x[3], b.x[0], t3);
+    t3 = fma_(c.x[0], d.x[3], t3);
+    t3 = fma_(c.x[1], d.x[2], t3);
+    t3 = fma_(c.x[2], d.x[1], t3);
+    t3 = fma_(c.x[3], d.x[0], t3);
+    h3 -= t3;
+    if constexpr (kNorm) return qd_renorm5_bf(o0.h, o1.h, o2.h, h3, 0.0);
+    else return qd{{o0.h, o1.h, o2.h, h3}};
+}
+// s - a*b, same scheme
+template <bool kNorm>
+TOR_HD_RNI qd qd_rank1_fused(qd s, qd a, qd b) {
+    double p0, e0;
+    two_prod(a.x[0], b.x[0], p0, e0);
+    double l1;
+    QAcc o0{s.x[0]};
+    o0.add(-p0, l1);
+    double pa, ea, pb, eb;
+    two_prod(a.x[0], b.x[1], pa, ea);
+    two_prod(a.x[1], b.x[0], pb, eb);
+    QAcc o1{s.x[1]};
+    double l2[4];
+    o1.add(l1, l2[0]);
+    o1.add(-e0, l2[1]);
+    o1.add(-pa, l2[2]);
+    o1.add(-pb, l2[3]);
+    double r[3], re[3];
+    two_prod(a.x[0], b.x[2], r[0], re[0]);
+    two_prod(a.x[1], b.x[1], r[1], re[1]);
+    two_prod(a.x[2], b.x[0], r[2], re[2]);
+    QAcc o2{s.x[2]};
+    double l3[9];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o2.add(l2[i], l3[i]);
+    o2.add(-ea, l3[4]);
+    o2.add(-eb, l3[5]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) o2.add(-r[i], l3[6 + i]);
+    double h3 = s.x[3];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) h3 += l3[i];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) h3 -= re[i];
+    double t3 = a.x[0] * b.x[3];
+    t3 = fma_(a.x[1], b.x[2], t3);
+    t3 = fma_(a.x[2], b.x[1], t3);
+    t3 = fma_(a.x[3], b.x[0], t3);
+    h3 -= t3;
+    if constexpr (kNorm) return qd_renorm5_bf(o0.h, o1.h, o2.h, h3, 0.0);
+    else return qd{{o0.h, o1.h, o2.h, h3}};
+}
+// Schur-state updates skip the final renormalisation (like the lazy DD products): every
+// state entry is O(1) in absolute terms (|S_ij| <= max_k R_kk), so words ordered by
+// ABSOLUTE scale 2^-53k keep the fused algorithm's error at ~2^-208 of that scale even
+// when the leading word has cancelled; entries are renormalised where they become
+// pivots, and the products that consume them renormalise their results.
+#ifndef TOR_QD_UNFUSED
+TOR_HD_RNI qd qd_rank2(qd s, qd a, qd b, qd c, qd d) { return qd_rank2_fused<!kQdLazy>(s, a, b, c, d); }
+TOR_HD_RNI qd qd_rank1(qd s, qd a, qd b) { return qd_rank1_fused<true>(s, a, b); }
+TOR_HD_RNI qd qd_rank1_lazy(qd s, qd a, qd b) { return qd_rank1_fused<!kQdLazy>(s, a, b); }
+#else
 // s - a*b - c*d.
 TOR_HD_RNI qd qd_rank2(qd s, qd a, qd b, qd c, qd d) {
     return qd_sub(qd_sub(s, qd_mul(a, b)), qd_mul(c, d));
 }
 TOR_HD_RNI qd qd_rank1(qd s, qd a, qd b) { return qd_sub(s, qd_mul(a, b)); }
+TOR_HD_RNI qd qd_rank1_lazy(qd s, qd a, qd b) { return qd_sub(s, qd_mul(a, b)); }
+#endif
 
+// 1/sqrt(x), x > 0 normalised: DD value y = (y0, y1) (~2^-104), then one Newton step
+// y + y e / 2 with e = 1 - x y^2 by the fused rank-1 (y^2 formed exactly enough from
+// TwoProds of the DD words) and the correction as a DD product (e ~ 2^-104 needs only
+// ~2^-106 relative).  One renormalisation.
+TOR_HD_NI qd qd_rsqrt_fast(qd x) {
+    const dd y = dd_rsqrt(dd_norm(dd{x.x[0], x.x[1]}));
+    // y^2 = p + (pe + q) + (qe + ll) + lle, words by order (2^-53k)
+    double p, pe, q, qe, ll, lle, m1, m2, n2, n3, n4;
+    two_prod(y.hi, y.hi, p, pe);
+    two_prod(2.0 * y.hi, y.lo, q, qe);
+    two_prod(y.lo, y.lo, ll, lle);
+    two_sum(pe, q, m1, m2);
+    two_sum(m2, qe, n2, n3);
+    two_sum(n2, ll, n2, n4);
+    const qd y2{{p, m1, n2, (n3 + n4) + lle}};
+    const qd e = qd_rank1_fused<true>(qd{{1.0, 0.0, 0.0, 0.0}}, x, y2);
+    // corr = (y/2) * (e0 + e1), DD product
+    double c0, c1;
+    two_prod(0.5 * y.hi, e.x[0], c0, c1);
+    c1 = fma_(0.5 * y.hi, e.x[1], c1);
+    c1 = fma_(0.5 * y.lo, e.x[0], c1);
+    return qd_renorm5_bf(y.hi, y.lo, c0, c1, 0.0);
+}
 // 1/sqrt(x), x > 0: DD seed then one QD Newton step y + y(1 - x y^2)/2.
-TOR_HD_NI qd qd_rsqrt(qd x) {
+TOR_HD_NI qd qd_rsqrt_slow(qd x) {
     const dd ys = dd_rsqrt(dd_norm(dd{x.x[0], x.x[1]}));
     const qd y = qd{{ys.hi, ys.lo, 0.0, 0.0}};
     const qd y2 = qd_mul(y, y);
@@ -378,6 +533,12 @@ TOR_HD_NI qd qd_rsqrt(qd x) {
     const qd corr = qd_mul(y, qd_mul_d(r, 0.5));
     return qd_add(y, corr);
 }
+
+#ifndef TOR_QD_SLOW_RSQRT
+TOR_HD qd qd_rsqrt(const qd& x) { return qd_rsqrt_fast(x); }
+#else
+TOR_HD qd qd_rsqrt(const qd& x) { return qd_rsqrt_slow(x); }
+#endif
 
 // ================================================================ traits ==
 // Uniform interface used by the kernels.  Word type W, number of doubles K.
@@ -462,8 +623,12 @@ template <> struct Arith<qd> {
         return qd_rank2(s, a, b, c, d);
     }
     TOR_HD static qd rank1(const qd& s, const qd& a, const qd& b) { return qd_rank1(s, a, b); }
-    TOR_HD static qd rank1s(const qd& s, const qd& a, const qd& b) { return qd_rank1(s, a, b); }
+    TOR_HD static qd rank1s(const qd& s, const qd& a, const qd& b) { return qd_rank1_lazy(s, a, b); }
     TOR_HD static qd rsqrt(const qd& a) { return qd_rsqrt(a); }
+    // a*c - b*b (2x2 determinant) by one fused update
+    TOR_HD static qd det2(const qd& a, const qd& b, const qd& c) {
+        return qd_rank2_fused<true>(qd{{0.0, 0.0, 0.0, 0.0}}, qd_neg(a), c, b, b);
+    }
     TOR_HD static qd unb(const qd& a) { return a; }
     TOR_HD static qd neg(const qd& a) { return qd_neg(a); }
     TOR_HD static void words(const qd& a, double* w) {
@@ -520,6 +685,22 @@ TOR_HD Piv<dd> pivot2<dd>(const dd& s00, const dd& s01, const dd& s11, const dd&
     p.tn = A::mul(t, rd);
     return p;
 }
+// QD: det by one fused update
+template <>
+TOR_HD Piv<qd> pivot2<qd>(const qd& s00, const qd& s01, const qd& s11, const qd& t) {
+    using A = Arith<qd>;
+    Piv<qd> p;
+    const qd a = A::norm(s00);
+    p.bad0 = nonpositive(a.x[0]);
+    p.r1 = A::rsqrt(a);
+    const qd det = A::det2(a, s01, s11);
+    p.bad1 = nonpositive(det.x[0]);
+    const qd rd = A::rsqrt(det);
+    p.u1 = A::mul(s01, p.r1);
+    p.r2 = A::mul(A::mul(a, p.r1), rd);
+    p.tn = A::mul(t, rd);
+    return p;
+}
 // Term factor of a one-mode (leaf) state: t / sqrt(det).
 template <class T>
 TOR_HD T leaf_term(const T& s00, const T& s01, const T& s11, const T& t, bool& bad) {
@@ -527,6 +708,13 @@ TOR_HD T leaf_term(const T& s00, const T& s01, const T& s11, const T& t, bool& b
     const T b = A::unb(s01);
     const T det = A::norm(A::rank1(A::mul(A::unb(s00), A::unb(s11)), b, b));
     bad = nonpositive(A::hi(det));
+    return A::mul(t, A::rsqrt(det));
+}
+template <>
+TOR_HD qd leaf_term<qd>(const qd& s00, const qd& s01, const qd& s11, const qd& t, bool& bad) {
+    using A = Arith<qd>;
+    const qd det = A::det2(s00, s01, s11);
+    bad = nonpositive(det.x[0]);
     return A::mul(t, A::rsqrt(det));
 }
 template <>
