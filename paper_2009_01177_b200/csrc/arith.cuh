@@ -482,6 +482,43 @@ TOR_HD_RNI qd qd_rank1_fused(qd s, qd a, qd b) {
     if constexpr (kNorm) return qd_renorm5_bf(o0.h, o1.h, o2.h, h3, 0.0);
     else return qd{{o0.h, o1.h, o2.h, h3}};
 }
+// a*b by the same order-collected scheme (products have no cancellation: without the
+// final renormalisation the words are still ordered 2^-53k relative to |ab|)
+template <bool kNorm>
+TOR_HD_RNI qd qd_mul_fused(qd a, qd b) {
+    double p0, e0;
+    two_prod(a.x[0], b.x[0], p0, e0);
+    double pa, ea, pb, eb;
+    two_prod(a.x[0], b.x[1], pa, ea);
+    two_prod(a.x[1], b.x[0], pb, eb);
+    QAcc o1{e0};
+    double l2[2];
+    o1.add(pa, l2[0]);
+    o1.add(pb, l2[1]);
+    double r[3], re[3];
+    two_prod(a.x[0], b.x[2], r[0], re[0]);
+    two_prod(a.x[1], b.x[1], r[1], re[1]);
+    two_prod(a.x[2], b.x[0], r[2], re[2]);
+    QAcc o2{r[0]};
+    double l3[6];
+    o2.add(r[1], l3[0]);
+    o2.add(r[2], l3[1]);
+    o2.add(ea, l3[2]);
+    o2.add(eb, l3[3]);
+    o2.add(l2[0], l3[4]);
+    o2.add(l2[1], l3[5]);
+    double h3 = re[0] + re[1];
+    h3 += re[2];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) h3 += l3[i];
+    h3 = fma_(a.x[0], b.x[3], h3);
+    h3 = fma_(a.x[1], b.x[2], h3);
+    h3 = fma_(a.x[2], b.x[1], h3);
+    h3 = fma_(a.x[3], b.x[0], h3);
+    if constexpr (kNorm) return qd_renorm5_bf(p0, o1.h, o2.h, h3, 0.0);
+    else return qd{{p0, o1.h, o2.h, h3}};
+}
+
 // Schur-state updates skip the final renormalisation (like the lazy DD products): every
 // state entry is O(1) in absolute terms (|S_ij| <= max_k R_kk), so words ordered by
 // ABSOLUTE scale 2^-53k keep the fused algorithm's error at ~2^-208 of that scale even
@@ -618,7 +655,11 @@ template <> struct Arith<qd> {
     TOR_HD static qd from(double x) { return qd{{x, 0.0, 0.0, 0.0}}; }
     TOR_HD static double hi(const qd& a) { return a.x[0]; }
     TOR_HD static qd norm(const qd& a) { return qd_renorm5_bf(a.x[0], a.x[1], a.x[2], a.x[3], 0.0); }
+#ifndef TOR_QD_UNFUSED
+    TOR_HD static qd mul(const qd& a, const qd& b) { return qd_mul_fused<true>(a, b); }
+#else
     TOR_HD static qd mul(const qd& a, const qd& b) { return qd_mul(a, b); }
+#endif
     TOR_HD static qd rank2(const qd& s, const qd& a, const qd& b, const qd& c, const qd& d) {
         return qd_rank2(s, a, b, c, d);
     }

@@ -69,3 +69,6 @@ void h_dd_acc(const double* t, const int* neg, int n, int flush, double* o) {
     o[2] = a.abs_sum;
 }
 }
+extern "C" void h_qd_mul_fused(const double* a, const double* b, double* o) {
+    put(Arith<qd>::mul(Q(a), Q(b)), o);
+}

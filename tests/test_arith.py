@@ -184,6 +184,8 @@ def test_qd_ops(lib):
         lib.h_qd_mul(a, b, o)
         ex = F(a) * F(b)
         assert abs(F(o) - ex) <= 2.0 ** -200 * abs(ex)
+        lib.h_qd_mul_fused(a, b, o)  # the engine's product (Arith<qd>::mul)
+        assert abs(F(o) - ex) <= 2.0 ** -204 * abs(ex)
         s, c, d = (D4(*rand_qd(rng, -1.5, 1.5)) for _ in range(3))
         lib.h_qd_rank2(s, a, b, c, d, o)
         ex = F(s) - F(a) * F(b) - F(c) * F(d)

@@ -61,3 +61,17 @@ __device__ double sink(const Acc<qd>& a) { return a.s.x[0] + a.s.x[1] + a.s.x[2]
 PROBES(double, fp64)
 PROBES(dd, dd)
 PROBES(qd, qd)
+
+// QD building blocks (for the QD cost breakdown)
+extern "C" __global__ void mul_qd(const qd* in, qd* out) {
+    const int i = threadIdx.x;
+    out[i] = qd_mul(in[i], in[i + 32]);
+}
+extern "C" __global__ void add_qd(const qd* in, qd* out) {
+    const int i = threadIdx.x;
+    out[i] = qd_add(in[i], in[i + 32]);
+}
+extern "C" __global__ void rsqrt_qd(const qd* in, qd* out) {
+    const int i = threadIdx.x;
+    out[i] = qd_rsqrt(in[i]);
+}
