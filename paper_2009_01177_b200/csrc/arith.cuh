@@ -849,15 +849,30 @@ template <> struct Acc<dd> {
 };
 
 template <> struct Acc<qd> {
+    // running sum s (renormalised QD) + a lazy block b: per term, exact TwoSums on the
+    // words of orders 0..2 (each order's errors into the next order), order 3 plainly;
+    // the block is renormalised and added to s by flush() (every lane subtree).
     qd s{{0.0, 0.0, 0.0, 0.0}};
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
     double abs_sum = 0.0;
     int sc = 0;
     TOR_HD void add(const qd& t, bool negative, int z) {
         (void)z;  // QD words are never grid-scaled
-        s = qd_add(s, negative ? qd_neg(t) : t);
+        const double g = negative ? -1.0 : 1.0;
+        double e0, e1, e2, e3, e4, e5;
+        two_sum(b0, g * t.x[0], b0, e0);
+        two_sum(b1, g * t.x[1], b1, e1);
+        two_sum(b1, e0, b1, e2);
+        two_sum(b2, g * t.x[2], b2, e3);
+        two_sum(b2, e1, b2, e4);
+        two_sum(b2, e2, b2, e5);
+        b3 += ((g * t.x[3] + e3) + e4) + e5;
         abs_sum += fabs(t.x[0]);
     }
-    TOR_HD void flush() {}
+    TOR_HD void flush() {
+        s = qd_add(s, qd_renorm5_bf(b0, b1, b2, b3, 0.0));
+        b0 = b1 = b2 = b3 = 0.0;
+    }
     TOR_HD void merge(const Acc& o) {
         s = qd_add(s, o.s);
         abs_sum += o.abs_sum;

@@ -298,7 +298,7 @@ __device__ void dfs_elim(const T* P, int q, T* slot, bool write_slot, T* root, c
 #define TOR_NB 6
 #endif
 #ifndef TOR_QD_NB
-#define TOR_QD_NB 1
+#define TOR_QD_NB 2
 #endif
     constexpr int NB = sizeof(T) == sizeof(qd) ? TOR_QD_NB : TOR_NB;  // entries per lane per batch
     constexpr int RT = tri_sz(2 * Q0);

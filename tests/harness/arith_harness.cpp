@@ -72,3 +72,16 @@ void h_dd_acc(const double* t, const int* neg, int n, int flush, double* o) {
 extern "C" void h_qd_mul_fused(const double* a, const double* b, double* o) {
     put(Arith<qd>::mul(Q(a), Q(b)), o);
 }
+// QD accumulator: n terms (4 words each), flush every `flush` terms; out = 4 words, sum|t|
+extern "C" void h_qd_acc(const double* t, const int* neg, int n, int flush, double* o) {
+    Acc<qd> a;
+    for (int i = 0; i < n; ++i) {
+        a.add(Q(t + 4 * i), neg[i] != 0, 0);
+        if (flush && (i + 1) % flush == 0) a.flush();
+    }
+    a.flush();
+    double w[4];
+    a.words(w);
+    for (int i = 0; i < 4; ++i) o[i] = w[i];
+    o[4] = a.abs_sum;
+}

@@ -228,3 +228,17 @@ def test_qd_lazy_state_chain(lib):
             exact -= F(a) * F(b) + F(c) * F(d)
             s = o
         assert abs(F(s) - exact) <= 2.0 ** -200
+
+
+def test_qd_accumulator(lib):
+    rng = random.Random(9)
+    n = 4096
+    terms = [rand_qd(rng, 1e-6, 1.0) for _ in range(n)]
+    negs = [rng.random() < 0.5 for _ in range(n)]
+    buf = (C.c_double * (4 * n))(*[w for t in terms for w in t])
+    ng = (C.c_int * n)(*negs)
+    o = (C.c_double * 5)()
+    lib.h_qd_acc(buf, ng, n, 8, o)
+    exact = sum(((-F(t)) if s else F(t) for t, s in zip(terms, negs)), Fraction(0))
+    sabs = sum(abs(t[0]) for t in terms)
+    assert abs(F(o[0:4]) - exact) <= 2.0 ** -200 * sabs
