@@ -8,7 +8,9 @@ using namespace tor;
 // every accumulator word reaches memory (differences of probes cancel these adds)
 __device__ double sink(const Acc<double>& a) { return a.s.hi + a.s.lo + a.abs_sum; }
 __device__ double sink(const Acc<dd>& a) { return a.s.hi + a.s.lo + a.h + a.c + a.abs_sum; }
-__device__ double sink(const Acc<qd>& a) { return a.s.x[0] + a.s.x[1] + a.s.x[2] + a.s.x[3] + a.abs_sum; }
+__device__ double sink(const Acc<qd>& a) {
+    return a.s.x[0] + a.s.x[1] + a.s.x[2] + a.s.x[3] + a.b0 + a.b1 + a.b2 + a.b3 + a.abs_sum;
+}
 
 #define PROBES(T, NAME)                                                                        \
     extern "C" __global__ void rank2_##NAME(const T* in, T* out) {                            \
