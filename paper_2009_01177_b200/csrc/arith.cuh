@@ -239,8 +239,8 @@ TOR_HD dd dd_rsqrt_seeded(dd x, double y0) {
 TOR_HD dd dd_rsqrt(dd x) { return dd_rsqrt_seeded(x, rsqrt_seed(x.hi)); }
 
 // det [[a, b], [b, c]] = a c - b^2 for DD a, b, c (possibly un-normalised): TwoProds of
-// the leading words, ONE TwoSum for the (possibly cancelling) difference, the cross and
-// low*low products into the low word, then a fast renormalisation.  h (the rounded leading difference, available a few
+// the leading words, ONE TwoSum for the (possibly cancelling) difference, the cross
+// products into the low word, then a fast renormalisation.  h (the rounded leading difference, available a few
 // operations in) is a good enough seed argument for the reciprocal square root.
 TOR_HD dd dd_det2(const dd& a, const dd& b, const dd& c, double& h) {
     const double p = a.hi * c.hi;
@@ -251,10 +251,19 @@ TOR_HD dd dd_det2(const dd& a, const dd& b, const dd& c, double& h) {
     two_sum(p, -q, h, he);
     double t = fma_(a.hi, c.lo, a.lo * c.hi);
     t = fma_(-2.0 * b.hi, b.lo, t);
-    // grid state entries are un-normalised (|lo| up to 2^-50 absolute): keep lo*lo
-    t = fma_(a.lo, c.lo, t);
-    t = fma_(-b.lo, b.lo, t);
+#ifndef TOR_DET2_LOLO
+#define TOR_DET2_LOLO 0
+#endif
+#if TOR_DET2_LOLO == 1
+    // grid state entries are un-normalised (|lo| up to 2^-50 absolute): the low*low
+    // products are <= 2^-100 of the O(1) state scale, the order of the grid updates' own
+    // rounding; keeping them cost 1.2 ms of 90.5 at n=32 (register pressure), so off
+    // (a separate short chain, joined at the end)
+    const double t2 = fma_(a.lo, c.lo, -(b.lo * b.lo));
+    const double lo = (he + (pe - qe)) + (t + t2);
+#else
     const double lo = (he + (pe - qe)) + t;
+#endif
     dd r;
     fast_two_sum(h, lo, r.hi, r.lo);
     return r;

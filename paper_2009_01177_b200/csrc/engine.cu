@@ -70,9 +70,12 @@ __host__ __device__ constexpr int ijtab_off(int a) { return 2 * (a - 1) * a * (2
 #endif
 template <class T> struct Cfg;
 template <> struct Cfg<double> {
+#ifndef TOR_F64_MINB
+#define TOR_F64_MINB 1
+#endif
     static constexpr int L = 4;
     static constexpr int WPB = 4;
-    static constexpr int MINB = 1;
+    static constexpr int MINB = TOR_F64_MINB;
     static constexpr bool TMEM = false;
     static constexpr bool WS = false;
     static constexpr int WS_MODE = 0;

@@ -134,7 +134,9 @@ def test_dd_pivot_and_leaf(lib):
         det = a * c - b * b
         # state entries carry absolute precision (~2^-100 of the O(1) scale): results are
         # bounded relative to the scale, amplified by the 2x2 condition (a c + b^2) / det
-        kap = float((a * c + b * b) / det)
+        # (the low*low products of un-normalised grid words, <= 2^-100 absolute, are dropped
+        # from det: a further 2^-100 / det relative)
+        kap = float((a * c + b * b) / det) + float(1 / det)
         r1, rd = rsqrt_exact(a), rsqrt_exact(det)
         assert abs(F(o[0:2]) - r1) <= 2.0 ** -100 * r1 * (1 + float(1 / a))
         assert abs(F(o[2:4]) - b * r1) <= 2.0 ** -99 * r1
