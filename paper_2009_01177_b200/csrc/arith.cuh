@@ -86,7 +86,18 @@ TOR_HD double rsqrt_seed(double x) {
 // Two fp64 Newton steps from the seed y ~ 1/sqrt(x) -> ~1 ulp.  The seed may come from
 // an approximation of x (e.g. an unnormalised leading word): the steps converge to
 // 1/sqrt(x) for any seed within a few 2^-20 of it.
+#ifndef TOR_RSQRT_HOUSEHOLDER
+#define TOR_RSQRT_HOUSEHOLDER 1
+#endif
 TOR_HD double rsqrt_newton(double x, double y) {
+#if TOR_RSQRT_HOUSEHOLDER
+    // one third-order step y (1 + r/2 + 3 r^2 / 8), r = 1 - x y^2: from a 2^-20 seed the
+    // truncation error is ~(5/16) r^3 < 2^-58, i.e. the result is fp64-rounding-limited
+    // (~1 ulp) after 4 dependent operations instead of 6 for two Newton steps
+    const double r = fma_(-x, y * y, 1.0);
+    const double p = fma_(0.375, r, 0.5);
+    return fma_(y * r, p, y);
+#else
     double h = x * y;
     double r = fma_(-h, y, 1.0);
     y = fma_(0.5 * y, r, y);
@@ -94,6 +105,7 @@ TOR_HD double rsqrt_newton(double x, double y) {
     r = fma_(-h, y, 1.0);
     y = fma_(0.5 * y, r, y);
     return y;
+#endif
 }
 // Full-precision fp64 reciprocal square root for x > 0.
 TOR_HD double rsqrt_d(double x) { return rsqrt_newton(x, rsqrt_seed(x)); }
