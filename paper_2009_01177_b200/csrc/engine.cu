@@ -131,6 +131,11 @@ constexpr int kConsFirst = TOR_CONS_FIRST;
 #define TOR_STEAL_L3 0
 #endif
 constexpr bool kStealL3 = TOR_STEAL_L3;
+// ... or the producers run level 3's pivot chains and vectors, the consumers its items
+#ifndef TOR_L3_SPLIT
+#define TOR_L3_SPLIT 0
+#endif
+constexpr bool kL3Split = TOR_L3_SPLIT && !TOR_STEAL_L3;
 
 constexpr int kIjTabEntries = ijtab_off(kMaxJobModes);
 __device__ uint32_t g_ijtab[kIjTabEntries];
@@ -1193,6 +1198,10 @@ template <class T, int M, int C> struct MirChunk {
 #ifndef TOR_UB
 #define TOR_UB 5
 #endif
+#ifndef TOR_ITEM_UNROLL
+#define TOR_ITEM_UNROLL 1
+#endif
+constexpr int kItemUnroll = TOR_ITEM_UNROLL;  // fan-out item batches per loop trip
 #ifndef TOR_QD_UB
 #define TOR_QD_UB 1
 #endif
@@ -1262,6 +1271,9 @@ template <class T, int E_LVL> struct FanLevel {
         tm_wait_st();
         __syncwarp();
     }
+    // PH: bit 0 = pivots and pivot-row vectors (to uwv, t values), bit 1 = the trailing
+    // update (reads uwv); the phases may run on different warps (see kL3Split).
+    template <int PH = 3>
     __device__ __forceinline__ static void run(T* sm, T* tvals, T* uwv, const uint32_t* tabs, uint64_t leaf_mask,
                                                int leaf_sel, unsigned long long* err, uint32_t tm_row) {
         using A = Arith<T>;
@@ -1273,6 +1285,7 @@ template <class T, int E_LVL> struct FanLevel {
             run_tmem_pairs(sm, tvals, tabs, leaf_mask, leaf_sel, err, tm_row);
             return;
         }
+        if constexpr (PH & 1) {
         const int x = lane & (E - 1), g = lane / E;
         PHASE_T0();
         const NodeRef nr = node_ref<T>(tabs, E_LVL - 1, x);
@@ -1309,6 +1322,8 @@ template <class T, int E_LVL> struct FanLevel {
         }
         __syncwarp();
         PHASE_MARK(6 + 3 * (E_LVL - 1));
+        }
+        if constexpr (!(PH & 2)) return;
         if constexpr (Cfg<T>::TMEM && E_LVL == FAN) {
             // last level -> TMEM: lane 2x+1 owns include child x, lane 2x the exclude
             // child (= parent x's trailing block Pt).  The pair splits the include
@@ -1351,7 +1366,7 @@ template <class T, int E_LVL> struct FanLevel {
         constexpr int UB = sizeof(T) == sizeof(qd) ? TOR_QD_UB : TOR_UB;  // items per batch (loads before stores)
         const uint32_t* itb = tabs + WarpSmem<T>::item_off(E_LVL) + lane;
         T* out = sm + WarpSmem<T>::lvl_off(E_LVL) + lane;
-#pragma unroll 1
+#pragma unroll(kItemUnroll)
         for (int s0 = 0; s0 < NIT; s0 += UB) {
             T sv[UB], ui[UB], uj[UB], wi[UB], wj[UB];
 #pragma unroll
@@ -1526,6 +1541,8 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         FanLevel<T, 2>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
         if constexpr (Cfg<T>::WS_MODE != 2 || kConsFirst > 3)
             FanLevel<T, 3>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
+        else if constexpr (kL3Split)  // level-3 pivots and vectors, into the consumer's vectors
+            FanLevel<T, 3>::template run<1>(fsm, ftv, fsm + SM::kUwOff, tabs, leaf_mask, leaf_sel, err, tm_slot);
         if constexpr (Cfg<T>::WS_MODE != 2) FanLevel<T, 4>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
         if constexpr (!Cfg<T>::WS) FanLevel<T, 5>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
     };
@@ -1667,8 +1684,10 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 const unsigned long long job = meta[c].job;
                 const int leaf_sel = meta[c].sel, flags = meta[c].flags;
                 if (flags & 2) break;
-                if constexpr (kConsFirst <= 3)
-                    if (!(flags & 4)) FanLevel<T, 3>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
+                if constexpr (kConsFirst <= 3) {
+                    if constexpr (kL3Split) FanLevel<T, 3>::template run<2>(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
+                    else if (!(flags & 4)) FanLevel<T, 3>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
+                }
                 FanLevel<T, 4>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
                 FanLevel<T, FAN>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
                 const T vt = ctv[node_ref<T>(tabs, FAN, lane).tix];
