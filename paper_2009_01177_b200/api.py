@@ -139,8 +139,16 @@ def raw_limbs(words, width_bits: int, frac_bits: int) -> tuple:
     two's-complement 64-bit limbs (low first, 4 entries like FixedValue::limbs)."""
     if width_bits not in (128, 256):
         return (0, 0, 0, 0)
-    v = words_fraction(words) * (1 << frac_bits)
-    q = math.floor(v + Fraction(1, 2))
+    # exact integer arithmetic: every word is n / 2^k; common denominator 2^K
+    parts = [float(w).as_integer_ratio() for w in words]
+    K = max(d.bit_length() - 1 for _, d in parts)
+    total = sum(n << (K - (d.bit_length() - 1)) for n, d in parts)
+    # round(total * 2^f / 2^K), ties up (floor(v + 1/2))
+    if frac_bits >= K:
+        q = total << (frac_bits - K)
+    else:
+        sh = K - frac_bits
+        q = (total + (1 << (sh - 1))) >> sh
     q %= 1 << width_bits
     return tuple((q >> (64 * i)) & ((1 << 64) - 1) if i < width_bits // 64 else 0 for i in range(4))
 

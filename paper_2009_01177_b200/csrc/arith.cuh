@@ -18,6 +18,7 @@
 #include <cstdint>
 
 #if defined(__CUDACC__)
+#define TOR_UNROLL _Pragma("unroll")
 #define TOR_HD __host__ __device__ __forceinline__
 // large QD routines: inline by default (measured faster than out-of-line calls even
 // though the QD kernel's SASS is ~60K instructions); -DTOR_QD_NOINLINE for experiments
@@ -34,6 +35,7 @@
 #define TOR_HD_RNI TOR_HD
 #endif
 #else
+#define TOR_UNROLL
 #define TOR_HD inline
 #define TOR_HD_NI inline
 #define TOR_HD_RNI inline
@@ -435,19 +437,19 @@ TOR_HD_RNI qd qd_rank2_fused(qd s, qd a, qd b, qd c, qd d) {
     two_prod(c.x[2], d.x[0], r[5], re[5]);
     QAcc o2{s.x[2]};
     double l3[18];
-#pragma unroll
+TOR_UNROLL
     for (int i = 0; i < 8; ++i) o2.add(l2[i], l3[i]);
     o2.add(-ea, l3[8]);
     o2.add(-eb, l3[9]);
     o2.add(-fa, l3[10]);
     o2.add(-fb, l3[11]);
-#pragma unroll
+TOR_UNROLL
     for (int i = 0; i < 6; ++i) o2.add(-r[i], l3[12 + i]);
     // order 3: plain
     double h3 = s.x[3];
-#pragma unroll
+TOR_UNROLL
     for (int i = 0; i < 18; ++i) h3 += l3[i];
-#pragma unroll
+TOR_UNROLL
     for (int i = 0; i < 6; ++i) h3 -= re[i];
     double t3 = a.x[0] * b.x[3];
     t3 = fma_(a.x[1], b.x[2], t3);
@@ -484,16 +486,16 @@ TOR_HD_RNI qd qd_rank1_fused(qd s, qd a, qd b) {
     two_prod(a.x[2], b.x[0], r[2], re[2]);
     QAcc o2{s.x[2]};
     double l3[9];
-#pragma unroll
+TOR_UNROLL
     for (int i = 0; i < 4; ++i) o2.add(l2[i], l3[i]);
     o2.add(-ea, l3[4]);
     o2.add(-eb, l3[5]);
-#pragma unroll
+TOR_UNROLL
     for (int i = 0; i < 3; ++i) o2.add(-r[i], l3[6 + i]);
     double h3 = s.x[3];
-#pragma unroll
+TOR_UNROLL
     for (int i = 0; i < 9; ++i) h3 += l3[i];
-#pragma unroll
+TOR_UNROLL
     for (int i = 0; i < 3; ++i) h3 -= re[i];
     double t3 = a.x[0] * b.x[3];
     t3 = fma_(a.x[1], b.x[2], t3);
@@ -530,7 +532,7 @@ TOR_HD_RNI qd qd_mul_fused(qd a, qd b) {
     o2.add(l2[1], l3[5]);
     double h3 = re[0] + re[1];
     h3 += re[2];
-#pragma unroll
+TOR_UNROLL
     for (int i = 0; i < 6; ++i) h3 += l3[i];
     h3 = fma_(a.x[0], b.x[3], h3);
     h3 = fma_(a.x[1], b.x[2], h3);

@@ -5,6 +5,10 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <algorithm>
+#include <exception>
+#include <thread>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -36,6 +40,33 @@ int fail(tor_error* e, const HostError& h) {
 
 void clear_err(tor_error* e) {
     if (e) set_err(e, "", "");
+}
+
+// Host-side preparation of many instances (validation, precision bounds, exact R) in
+// parallel chunks; the first failure in index order is rethrown (deterministic).
+template <class F>
+void parallel_for(int n, F f) {
+    const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    const int nt = std::min(hw, std::max(1, n / 64));
+    if (nt <= 1) {
+        for (int i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::vector<std::exception_ptr> errs(nt);
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            const int lo = static_cast<int>(static_cast<int64_t>(n) * t / nt);
+            const int hi = static_cast<int>(static_cast<int64_t>(n) * (t + 1) / nt);
+            try {
+                for (int i = lo; i < hi; ++i) f(i);
+            } catch (...) {
+                errs[t] = std::current_exception();
+            }
+        });
+    for (auto& x : th) x.join();
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
 }
 
 Input checked_input(const tor_input* in, int nmax) {
@@ -84,11 +115,18 @@ void device_check(int device) {
 // Runs the engine and maps its failures onto the error taxonomy.
 std::vector<EngineOut> run(int device, int mode, const std::vector<Input>& ins, const WorkRange& range,
                            EngineStats* stats) {
+    const auto t0 = std::chrono::steady_clock::now();
     device_check(device);
+    const auto t1 = std::chrono::steady_clock::now();
     std::vector<PreparedInput> prep(ins.size());
-    for (size_t i = 0; i < ins.size(); ++i) {
+    parallel_for(static_cast<int>(ins.size()), [&](int i) {
         prep[i].n = ins[i].n;
         prep[i].R = build_R(ins[i], mode_words(mode), mode == MODE_DD, &prep[i].tscale_log2);
+    });
+    if (std::getenv("TOR_DEBUG_TIMING")) {
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "[tor] run: device_check %.2f ms, build_R %.2f ms\n", ms(t0, t1),
+                     ms(t1, std::chrono::steady_clock::now()));
     }
     std::vector<EngineOut> out;
     std::string err;
@@ -357,16 +395,13 @@ int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, i
         clear_err(err);
         if (count < 1 || !ins) throw HostError(TOR_E_INVALID, "torontonian/range", "empty batch");
         const auto t0 = std::chrono::steady_clock::now();
-        std::vector<Input> as;
-        as.reserve(count);
-        for (int i = 0; i < count; ++i) {
-            as.push_back(checked_input(&ins[i], 40));
-            if (as.back().n != as.front().n)
-                throw HostError(TOR_E_INVALID, "torontonian/range", "batch instances must share N");
-        }
+        std::vector<Input> as(count);
         const int mode = prec == TOR_PREC_AUTO ? MODE_DD : mode_of(prec);
         std::vector<PrecCfg> cfgs(count);
-        for (int i = 0; i < count; ++i) {
+        parallel_for(count, [&](int i) {
+            as[i] = checked_input(&ins[i], 40);
+            if (as[i].n != ins[0].n)
+                throw HostError(TOR_E_INVALID, "torontonian/range", "batch instances must share N");
             if (prec == TOR_PREC_AUTO) {
                 cfgs[i] = select_precision(as[i], as[i].n, 3, 0.5);
                 if (cfgs[i].width_bits != 128)
@@ -378,11 +413,18 @@ int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, i
             } else {
                 cfgs[i] = force_width(as[i], prec == TOR_PREC_W128_DD ? 128 : 256);
             }
-        }
+        });
+        const auto t1 = std::chrono::steady_clock::now();
         EngineStats st;
         const auto res = run(device, mode, as, WorkRange{}, &st);
-        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        const auto t2 = std::chrono::steady_clock::now();
+        const double wall = std::chrono::duration<double>(t2 - t0).count();
         for (int i = 0; i < count; ++i) fill_result(as[i], mode, cfgs[i], res[i], st, wall, 1, &outs[i]);
+        if (std::getenv("TOR_DEBUG_TIMING")) {
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            std::fprintf(stderr, "[tor] batch: validate+precision %.2f ms, run %.2f ms, results %.2f ms\n",
+                         ms(t0, t1), ms(t1, t2), ms(t2, std::chrono::steady_clock::now()));
+        }
         return TOR_OK;
     } catch (const HostError& h) {
         return fail(err, h);

@@ -2112,22 +2112,24 @@ class PlanImpl final : public Plan {
             scr_stride_ = std::max<size_t>(stride, 1);
             CK(scr_.alloc(sizeof(T) * scr_stride_ * blocks_ * WPB, device_));
         }
-        // resident inputs: the exact R of every instance
-        std::vector<T> host(static_cast<size_t>(tri_sz(2 * n_)));
+        // resident inputs: the exact R of every instance, one strided copy for the batch
+        const size_t rt = static_cast<size_t>(tri_sz(2 * n_));
+        std::vector<T> host(rt * ninst_);
         for (int i = 0; i < ninst_; ++i) {
             const auto& R = inputs[i].R;
-            for (size_t k = 0; k < host.size(); ++k) {
+            T* h = host.data() + i * rt;
+            for (size_t k = 0; k < rt; ++k) {
                 double w[4] = {0, 0, 0, 0};
                 for (int x = 0; x < K; ++x) w[x] = R[k * K + x];
-                if constexpr (K == 1) host[k] = w[0];
-                else if constexpr (K == 2) host[k] = dd{w[0], w[1]};
-                else host[k] = qd{{w[0], w[1], w[2], w[3]}};
+                if constexpr (K == 1) h[k] = w[0];
+                else if constexpr (K == 2) h[k] = dd{w[0], w[1]};
+                else h[k] = qd{{w[0], w[1], w[2], w[3]}};
             }
-            CK(cudaMemcpyAsync(pool() + i * g_.inst_entries, host.data(), sizeof(T) * host.size(),
-                               cudaMemcpyHostToDevice, st_));
-            CK(cudaStreamSynchronize(st_));
         }
-        h2d_bytes_ = sizeof(T) * host.size() * ninst_;
+        CK(cudaMemcpy2DAsync(pool(), sizeof(T) * g_.inst_entries, host.data(), sizeof(T) * rt, sizeof(T) * rt,
+                             ninst_, cudaMemcpyHostToDevice, st_));
+        CK(cudaStreamSynchronize(st_));
+        h2d_bytes_ = sizeof(T) * rt * ninst_;
         return 0;
     }
 
@@ -2208,9 +2210,8 @@ class PlanImpl final : public Plan {
         CK(cudaGetLastError());
         CK(cudaEventRecord(ev_[3], st_));
         std::vector<double> res(static_cast<size_t>(ninst_) * 5);
-        for (int i = 0; i < ninst_; ++i)
-            CK(cudaMemcpyAsync(&res[i * 5], parts + static_cast<size_t>(i) * per_ * 5, 5 * sizeof(double),
-                               cudaMemcpyDeviceToHost, st_));
+        CK(cudaMemcpy2DAsync(res.data(), 5 * sizeof(double), parts, per_ * 5 * sizeof(double), 5 * sizeof(double),
+                             ninst_, cudaMemcpyDeviceToHost, st_));
         unsigned long long herr = 0;
         CK(cudaMemcpyAsync(&herr, errw, sizeof(herr), cudaMemcpyDeviceToHost, st_));
         CK(cudaStreamSynchronize(st_));

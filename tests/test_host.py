@@ -201,3 +201,17 @@ def test_config_fixtures_reproduce_survey_values(golden):
     assert golden["cfg1"]["fixed128"]["value"] == 6.5025695289866082e-05
     assert golden["cfg2"]["fixed128"]["value"] == 1.1801356334058375e-07
     assert golden["cfg3_items"]["0"]["fixed128"]["value"] == pytest.approx(1.2392775476016946e-10, rel=1e-15)
+
+
+def test_batch_validation_errors_before_device():
+    # the batch validates its instances on host threads; the first bad instance in index
+    # order is reported, before any device work
+    good = [diag_instance(3, [0.1, 0.2, 0.3]) for _ in range(300)]
+    skew = diag_instance(3, [0.1, 0.2, 0.3])
+    skew.a00[0] = 0.1 + 0.05j
+    with pytest.raises(T.TorfpError) as e:
+        T.torontonian_batch(good[:150] + [skew] + good[150:] + [diag_instance(4, [0.1] * 4)], "128")
+    assert e.value.code == "torontonian/symmetry"
+    with pytest.raises(T.InvalidArgument) as e:
+        T.torontonian_batch(good + [diag_instance(4, [0.1] * 4)] + good[:10], "fp64")
+    assert e.value.code == "torontonian/range"
