@@ -126,16 +126,6 @@ template <class T> constexpr int root_modes() { return Cfg<T>::L + FAN; }
 #define TOR_CONS_FIRST 3
 #endif
 constexpr int kConsFirst = TOR_CONS_FIRST;
-// ... and the producers take level 3 of a leaf whenever they would otherwise wait
-#ifndef TOR_STEAL_L3
-#define TOR_STEAL_L3 0
-#endif
-constexpr bool kStealL3 = TOR_STEAL_L3;
-// ... or the producers run level 3's pivot chains and vectors, the consumers its items
-#ifndef TOR_L3_SPLIT
-#define TOR_L3_SPLIT 0
-#endif
-constexpr bool kL3Split = TOR_L3_SPLIT && !TOR_STEAL_L3;
 
 constexpr int kIjTabEntries = ijtab_off(kMaxJobModes);
 __device__ uint32_t g_ijtab[kIjTabEntries];
@@ -608,62 +598,6 @@ template <class T> struct SubReg<T, 1> {
     }
 };
 
-// Two independent 2-mode register states A and B (their own terms already emitted):
-// all 3 + 3 extension terms, written as one straight-line block so the two pivot chains
-// and the four leaf chains overlap (instruction-level parallelism for the lane
-// subtrees, whose chains are otherwise serial).  Breakdowns are collected and reported
-// after the block.  Terms are added in SubReg<2>'s order (A0, A00, A1, B0, B00, B1).
-template <class T>
-__device__ __forceinline__ void sub2_pair(const St<T, 2>& SA, const T& tA, bool negA, uint64_t maskA, int nselA,
-                                          const St<T, 2>& SB, const T& tB, bool negB, uint64_t maskB, int nselB,
-                                          Acc<T>& acc, unsigned long long* err) {
-    using A = Arith<T>;
-    const Piv<T> pa = piv_lt<T>(SA.e[0], SA.e[1], SA.e[4], tA);
-    const Piv<T> pb = piv_lt<T>(SB.e[0], SB.e[1], SB.e[4], tB);
-    St<T, 1> ca, cb;
-    {
-        T u[4], w[4];
-#pragma unroll
-        for (int j = 2; j < 4; ++j) {
-            u[j] = A::mul(A::unb(SA.e[cix<4>(0, j)]), pa.r1);
-            w[j] = A::mul(A::rank1s(SA.e[cix<4>(1, j)], pa.u1, u[j]), pa.r2);
-        }
-        ca.e[0] = A::rank2(SA.e[cix<4>(2, 2)], u[2], u[2], w[2], w[2]);
-        ca.e[1] = A::rank2(SA.e[cix<4>(2, 3)], u[2], u[3], w[2], w[3]);
-        ca.e[2] = A::rank2(SA.e[cix<4>(3, 3)], u[3], u[3], w[3], w[3]);
-    }
-    {
-        T u[4], w[4];
-#pragma unroll
-        for (int j = 2; j < 4; ++j) {
-            u[j] = A::mul(A::unb(SB.e[cix<4>(0, j)]), pb.r1);
-            w[j] = A::mul(A::rank1s(SB.e[cix<4>(1, j)], pb.u1, u[j]), pb.r2);
-        }
-        cb.e[0] = A::rank2(SB.e[cix<4>(2, 2)], u[2], u[2], w[2], w[2]);
-        cb.e[1] = A::rank2(SB.e[cix<4>(2, 3)], u[2], u[3], w[2], w[3]);
-        cb.e[2] = A::rank2(SB.e[cix<4>(3, 3)], u[3], u[3], w[3], w[3]);
-    }
-    bool b1, b2, b3, b4;
-    const T la0 = leaf_term<T>(ca.e[0], ca.e[1], ca.e[2], pa.tn, b1);
-    const T la1 = leaf_term<T>(SA.e[cix<4>(2, 2)], SA.e[cix<4>(2, 3)], SA.e[cix<4>(3, 3)], tA, b2);
-    const T lb0 = leaf_term<T>(cb.e[0], cb.e[1], cb.e[2], pb.tn, b3);
-    const T lb1 = leaf_term<T>(SB.e[cix<4>(2, 2)], SB.e[cix<4>(2, 3)], SB.e[cix<4>(3, 3)], tB, b4);
-    acc.add(pa.tn, !negA, nselA + 1);
-    acc.add(la0, negA, nselA + 2);
-    acc.add(la1, !negA, nselA + 1);
-    acc.add(pb.tn, !negB, nselB + 1);
-    acc.add(lb0, negB, nselB + 2);
-    acc.add(lb1, !negB, nselB + 1);
-    if (pa.bad0 || pa.bad1 || pb.bad0 || pb.bad1 || b1 || b2 || b3 || b4) {
-        if (pa.bad0 || pa.bad1) report_breakdown(err, maskA | 2ull, 2 * nselA + (pa.bad0 ? 0 : 1));
-        if (b1) report_breakdown(err, maskA | 3ull, 2 * nselA + 3);
-        if (b2) report_breakdown(err, maskA | 1ull, 2 * nselA + 1);
-        if (pb.bad0 || pb.bad1) report_breakdown(err, maskB | 2ull, 2 * nselB + (pb.bad0 ? 0 : 1));
-        if (b3) report_breakdown(err, maskB | 3ull, 2 * nselB + 3);
-        if (b4) report_breakdown(err, maskB | 1ull, 2 * nselB + 1);
-    }
-}
-
 // Lane subtree rooted at an L-mode view in shared memory: emits the node's own
 // term and all 2^L - 1 extensions.  Branch 0 includes the first view mode (its
 // elimination reads shared memory), branch 1 excludes it (loads the trailing block).
@@ -926,45 +860,6 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
     constexpr int K01 = 2 * M - 1;  // entries of rows 0 and 1
     constexpr int NT = tri_sz(M - 2);
     const uint64_t bit = 1ull << (L - 1);
-#ifndef TOR_PAIR3
-#define TOR_PAIR3 0
-#endif
-    if constexpr (L == 3 && TOR_PAIR3) {
-        // both children (2 modes) in registers, then their subtrees as one pair
-        St<T, 2> Sa, Sb;
-        T ta;
-        bool bad0, bad1;
-        {
-            uint32_t r0[4 * K01];
-            tm_ld_entries<M, 0, K01>(row, r0);
-            tm_wait_ld();
-            T e0[K01];
-#pragma unroll
-            for (int k = 0; k < K01; ++k) e0[k] = u32_to_dd(r0[4 * k], r0[4 * k + 1], r0[4 * k + 2], r0[4 * k + 3]);
-            const Piv<T> pv = piv_lt<T>(e0[0], e0[1], e0[M], t);
-            bad0 = pv.bad0;
-            bad1 = pv.bad1;
-            ta = pv.tn;
-            T u[M], w[M];
-#pragma unroll
-            for (int j = 2; j < M; ++j) {
-                u[j] = A::mul(A::unb(e0[j]), pv.r1);
-                w[j] = A::mul(A::rank1s(e0[M + j - 1], pv.u1, u[j]), pv.r2);
-            }
-            lt_wave<T, M, 0, NT>(row, u, w, Sa);
-        }
-        {
-            uint32_t rt[4 * NT];
-            tm_ld_entries<M, K01, NT>(row, rt);
-            tm_wait_ld();
-#pragma unroll
-            for (int kk = 0; kk < NT; ++kk) Sb.e[kk] = u32_to_dd(rt[4 * kk], rt[4 * kk + 1], rt[4 * kk + 2], rt[4 * kk + 3]);
-        }
-        if (bad0 || bad1) report_breakdown(err, mask | bit, 2 * nsel + (bad0 ? 0 : 1));
-        acc.add(ta, !neg, nsel + 1);
-        sub2_pair<T>(Sa, ta, !neg, mask | bit, nsel + 1, Sb, t, neg, mask, nsel, acc, err);
-        return;
-    }
 #pragma unroll 1
     for (int br = 0; br < 2; ++br) {
         T tn;
@@ -1213,79 +1108,10 @@ template <class T, int E_LVL> struct FanLevel {
     static constexpr int m = 2 * q;
     static constexpr int dn = m - 2;
     static constexpr int tn = tri_sz(dn);
-    // Last level -> TMEM, lane-pair form: lanes (2x, 2x+1) own parent x (level-4 node
-    // x) throughout.  Both compute its pivots; the even lane forms u_j, w_j for
-    // j = 2..5, the odd lane for j = 9..6 (reversed), and the halves cross by shuffle,
-    // so each lane holds all eight (the odd lane in mirrored order) without a shared-
-    // memory round trip.  Then the mirror-split update (MirChunk): lane 2x+1 owns the
-    // include child x, lane 2x the exclude child (parent x's trailing block); the
-    // include child's entries split by the anti-transpose mirror (i,j) -> (7-j,7-i)
-    // so (i,j) are compile-time for both lanes; each lane stores its node's state to
-    // its own TMEM row in mir_slot order.
-    __device__ __forceinline__ static void run_tmem_pairs(T* sm, T* tvals, const uint32_t* tabs, uint64_t leaf_mask,
-                                                          int leaf_sel, unsigned long long* err, uint32_t tm_row) {
-        using A = Arith<T>;
-        static_assert(dn == kMirD && tn == 36 && E == 16, "mirror split layout");
-        const int lane = threadIdx.x & 31;
-        const int xe = lane >> 1, h = lane & 1;
-        const NodeRef nr = node_ref<T>(tabs, E_LVL - 1, xe);
-        const T* P = sm + nr.off;
-        const Piv<T> pv = pivot2<T>(P[0], P[1], P[m], tvals[nr.tix]);
-        T a[4], b[4];
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-            const int j = h ? m - 1 - s : 2 + s;
-            a[s] = P[j];
-            b[s] = P[m - 1 + j];
-        }
-        if (h == 0) {
-            const uint64_t nm = leaf_mask | (static_cast<uint64_t>((xe << 1) | 1) << (Q0 - E_LVL));
-            if (pv.bad0 || pv.bad1) report_breakdown(err, nm, 2 * (leaf_sel + __popc(xe)) + (pv.bad0 ? 0 : 1));
-            tvals[E - 1 + xe] = pv.tn;  // level e-1 t values live below index E-1: no hazard
-        }
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-            a[s] = A::mul(A::unb(a[s]), pv.r1);
-            b[s] = A::mul(A::rank1s(b[s], pv.u1, a[s]), pv.r2);
-        }
-        T u[dn], w[dn];
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-            u[s] = a[s];
-            w[s] = b[s];
-            u[4 + s] = shfl_xor_t(a[3 - s], 1);
-            w[4 + s] = shfl_xor_t(b[3 - s], 1);
-        }
-        const T* Pt = P + 2 * m - 1;
-        MirChunk<T, m, 0>::run(Pt, u, w, h, tm_row);
-        {
-            uint32_t r[16];
-#pragma unroll
-            for (int a2 = 0; a2 < 4; ++a2) {
-                const T sv = Pt[cix<dn>(a2, dn - 1 - a2)];
-                const T v = A::rank2(sv, u[dn - 1 - a2], u[a2], w[dn - 1 - a2], w[a2]);
-                if constexpr (sizeof(T) == sizeof(dd)) dd_to_u32(h ? v : sv, r + 4 * a2);
-            }
-            tm_st16(tm_row + 16 * 8, r);
-        }
-        tm_wait_st();
-        __syncwarp();
-    }
-    // PH: bit 0 = pivots and pivot-row vectors (to uwv, t values), bit 1 = the trailing
-    // update (reads uwv); the phases may run on different warps (see kL3Split).
-    template <int PH = 3>
     __device__ __forceinline__ static void run(T* sm, T* tvals, T* uwv, const uint32_t* tabs, uint64_t leaf_mask,
                                                int leaf_sel, unsigned long long* err, uint32_t tm_row) {
         using A = Arith<T>;
         const int lane = threadIdx.x & 31;
-#ifndef TOR_L5_SHFL
-#define TOR_L5_SHFL 0
-#endif
-        if constexpr (Cfg<T>::TMEM && E_LVL == FAN && TOR_L5_SHFL) {
-            run_tmem_pairs(sm, tvals, tabs, leaf_mask, leaf_sel, err, tm_row);
-            return;
-        }
-        if constexpr (PH & 1) {
         const int x = lane & (E - 1), g = lane / E;
         PHASE_T0();
         const NodeRef nr = node_ref<T>(tabs, E_LVL - 1, x);
@@ -1322,8 +1148,6 @@ template <class T, int E_LVL> struct FanLevel {
         }
         __syncwarp();
         PHASE_MARK(6 + 3 * (E_LVL - 1));
-        }
-        if constexpr (!(PH & 2)) return;
         if constexpr (Cfg<T>::TMEM && E_LVL == FAN) {
             // last level -> TMEM: lane 2x+1 owns include child x, lane 2x the exclude
             // child (= parent x's trailing block Pt).  The pair splits the include
@@ -1541,8 +1365,6 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         FanLevel<T, 2>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
         if constexpr (Cfg<T>::WS_MODE != 2 || kConsFirst > 3)
             FanLevel<T, 3>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
-        else if constexpr (kL3Split)  // level-3 pivots and vectors, into the consumer's vectors
-            FanLevel<T, 3>::template run<1>(fsm, ftv, fsm + SM::kUwOff, tabs, leaf_mask, leaf_sel, err, tm_slot);
         if constexpr (Cfg<T>::WS_MODE != 2) FanLevel<T, 4>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
         if constexpr (!Cfg<T>::WS) FanLevel<T, 5>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
     };
@@ -1577,8 +1399,6 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         };
         __shared__ WsMeta meta[8];
         __shared__ __align__(8) unsigned long long mbar[16];  // full[0..7], empty[8..15]
-        __shared__ int cbusy[8];  // consumer c is in its lane subtrees (level-3 stealing hint)
-        if (threadIdx.x < 8) cbusy[threadIdx.x] = 0;
         if (threadIdx.x < 16) {
             const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[threadIdx.x]));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(32) : "memory");
@@ -1588,16 +1408,6 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         auto mb_arrive = [&](int i) {
             const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[i]));
             asm volatile("{.reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0];}\n" ::"r"(a) : "memory");
-        };
-        auto mb_test = [&](int i, uint32_t parity) {
-            const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[i]));
-            uint32_t ok;
-            asm volatile(
-                "{.reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p;}\n"
-                : "=r"(ok)
-                : "r"(a), "r"(parity)
-                : "memory");
-            return __shfl_sync(0xffffffffu, ok, 0) != 0;
         };
         auto mb_wait = [&](int i, uint32_t parity) {
             const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[i]));
@@ -1635,26 +1445,11 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                     mb_wait(8 + c, (uses[s] & 1) ^ 1);
                     T* cslots = scratch + (static_cast<size_t>(blockIdx.x * 4 + p) * 2 + s) * scratch_stride;
                     produce_leaf(J[s], leaf[s], 0u, area(c), dfs_t + 32 * s, cslots);
-                    // Dynamic balance: when the other context's consumer still holds its
-                    // area (the producer would wait there anyway), run this leaf's level 3
-                    // here instead of on the consumer.
-                    bool l3 = false;
-                    if constexpr (kConsFirst == 3 && kStealL3) {
-                        // ... i.e. while consumer c is still in its lane subtrees
-                        int busy = 0;
-                        if (lane == 0) busy = *reinterpret_cast<volatile int*>(&cbusy[c]);
-                        l3 = __shfl_sync(0xffffffffu, busy, 0) != 0;
-                        if (l3) {
-                            const uint64_t lm = J[s].mask | (leaf[s] << Q0);
-                            FanLevel<T, 3>::run(area(c), area(c) + SM::kTOff, uwv, tabs, lm,
-                                                J[s].nsel + __popcll(leaf[s]), err, 0u);
-                        }
-                    }
                     if (lane == 0) {
                         meta[c].mask = J[s].mask | (leaf[s] << Q0);
                         meta[c].job = jid[s];
                         meta[c].sel = J[s].nsel + __popcll(leaf[s]);
-                        meta[c].flags = (leaf[s] + 1 == (1ull << D) ? 1 : 0) | (l3 ? 4 : 0);
+                        meta[c].flags = leaf[s] + 1 == (1ull << D) ? 1 : 0;
                     }
                     __syncwarp();
                     mb_arrive(c);
@@ -1684,24 +1479,17 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 const unsigned long long job = meta[c].job;
                 const int leaf_sel = meta[c].sel, flags = meta[c].flags;
                 if (flags & 2) break;
-                if constexpr (kConsFirst <= 3) {
-                    if constexpr (kL3Split) FanLevel<T, 3>::template run<2>(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
-                    else if (!(flags & 4)) FanLevel<T, 3>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
-                }
+                if constexpr (kConsFirst <= 3) FanLevel<T, 3>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
                 FanLevel<T, 4>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
                 FanLevel<T, FAN>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
                 const T vt = ctv[node_ref<T>(tabs, FAN, lane).tix];
                 __syncwarp();
-                if constexpr (kConsFirst == 3 && kStealL3)
-                    if (lane == 0) *reinterpret_cast<volatile int*>(&cbusy[c]) = 1;
                 mb_arrive(8 + c);  // the producer may refill root..L3 and t values 0..6, 31
                 const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(lane) << L);
                 const int lsel = leaf_sel + __popc(lane);
                 const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
                 acc.add(vt, nodeneg, lsel);
                 tmem_ext<T, L>(crow, crow + 4 * tri_sz(2 * L), vt, nodeneg, lmask, lsel, acc, err);
-                if constexpr (kConsFirst == 3 && kStealL3)
-                    if (lane == 0) *reinterpret_cast<volatile int*>(&cbusy[c]) = 0;
                 acc.flush();
                 if (flags & 1) {
                     write_partial(acc, job);
