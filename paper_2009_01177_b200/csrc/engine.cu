@@ -73,7 +73,10 @@ template <> struct Cfg<double> {
 #ifndef TOR_F64_MINB
 #define TOR_F64_MINB 1
 #endif
-    static constexpr int L = 4;
+#ifndef TOR_F64_L
+#define TOR_F64_L 5
+#endif
+    static constexpr int L = TOR_F64_L;
     static constexpr int WPB = 4;
     static constexpr int MINB = TOR_F64_MINB;
     static constexpr bool TMEM = false;
@@ -1007,7 +1010,7 @@ template <class T> struct WarpSmem {
     static constexpr int kProdEntries = kProdUw + 64;
     static constexpr size_t kWarpBytes = kEntries * sizeof(T);
     // Block-wide item tables of the fan-out trailing updates: level e has E*tn items
-    // (it = x*tn + k: child x, entry k); word = src | ui << 11 | uj << 20 with src the
+    // (it = x*tn + k: child x, entry k); word = src | ui << 12 | uj << 22 with src the
     // parent entry (index into the warp area; the smem layout is static, so this is a
     // constant per item), ui/uj the uw indices of u_i/u_j (w_i/w_j at +m).
     // Levels 1..kItemLevels use item tables; with TMEM the last level uses the (i,j)
@@ -1023,7 +1026,7 @@ template <class T> struct WarpSmem {
     static constexpr int kNodeOff = kLastTabOff + (Cfg<T>::TMEM ? tri_sz(2 * (Q0 - FAN)) : 0);
     static constexpr int kTabEntries = kNodeOff + (2 << FAN) - 1;
     static constexpr size_t kTabBytes = ((kTabEntries * 4 + 15) / 16) * 16;
-    static_assert(kBufEntries < 2048 && uw_need() <= 512, "item word fields");
+    static_assert(kBufEntries < 4096 && uw_need() <= 1024, "item word fields");
 };
 
 // Node (e, c) of the breadth-first fan-out rooted at the copied root (level 0): its
@@ -1198,8 +1201,8 @@ template <class T, int E_LVL> struct FanLevel {
                 const int s = s0 + u;
                 const bool ok = s < NIT && (s < NIT - 1 || lane + 32 * s < NE);
                 const uint32_t w = ok ? itb[32 * s] : 0u;
-                const int src = static_cast<int>(w & 0x7ffu);
-                const int a = static_cast<int>((w >> 11) & 0x1ffu), b = static_cast<int>(w >> 20);
+                const int src = static_cast<int>(w & 0xfffu);
+                const int a = static_cast<int>((w >> 12) & 0x3ffu), b = static_cast<int>(w >> 22);
                 sv[u] = sm[src];
                 ui[u] = uwv[a];
                 uj[u] = uwv[b];
@@ -1246,8 +1249,8 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
             }
             const int src = node_off<T>(e - 1, x) + 2 * m - 1 + (it - x * tn);
             const int ui = x * (2 * m + 1) + 2 + i, uj = x * (2 * m + 1) + 2 + i + r;
-            tabs[SM::item_off(e) + it] = static_cast<uint32_t>(src) | (static_cast<uint32_t>(ui) << 11) |
-                                         (static_cast<uint32_t>(uj) << 20);
+            tabs[SM::item_off(e) + it] = static_cast<uint32_t>(src) | (static_cast<uint32_t>(ui) << 12) |
+                                         (static_cast<uint32_t>(uj) << 22);
         }
     }
     for (int e = 0; e <= FAN; ++e)
