@@ -704,6 +704,19 @@ __host__ __device__ constexpr int tri_col(int D, int k) {
 // (n, D-1-n) by both.  TMEM slot 4c+p holds A[2c+p], slot 4c+2+p its mirror
 // (c < 8), slot 32+n anti-diagonal entry n.  Column of entry k = 4 * slot(k).
 constexpr int kMirD = 8;
+// Level-5 (TMEM) lane maps, found by tools/l5_layout_search.py for the padded fan-out
+// layout: 128-bit shared-memory loads are served per 8-lane phase, so which parents share a
+// phase decides the bank conflicts.  kL5VecMap: lane & 15 -> parent for the pivot / vector
+// phase (conflict-free); kL5PairMap: lane pair -> parent for the mirror-split update (272 vs
+// 459 wavefronts per leaf for the identity map, ideal 208).  Nibble i = map(i).
+#ifndef TOR_L5_MAPS
+#define TOR_L5_MAPS 1
+#endif
+constexpr uint64_t kL5PairMap = TOR_L5_MAPS ? 0x0e249f35d71bac68ull : 0xfedcba9876543210ull;
+constexpr uint64_t kL5VecMap = TOR_L5_MAPS ? 0x79b0ec2568adf134ull : 0xfedcba9876543210ull;
+__host__ __device__ __forceinline__ int l5_map(uint64_t map, int i) { return static_cast<int>((map >> (4 * i)) & 15); }
+// level-5 node held by a consumer lane (lane pair -> parent x: nodes 2x, 2x + 1)
+__host__ __device__ __forceinline__ int l5_lane_node(int lane) { return 2 * l5_map(kL5PairMap, lane >> 1) + (lane & 1); }
 __host__ __device__ constexpr int mir_a_index(int i, int j) {  // index of (i,j) in A
     int n = 0;
     for (int a = 0; a < kMirD; ++a)
@@ -1115,7 +1128,8 @@ template <class T, int E_LVL> struct FanLevel {
                                                int leaf_sel, unsigned long long* err, uint32_t tm_row) {
         using A = Arith<T>;
         const int lane = threadIdx.x & 31;
-        const int x = lane & (E - 1), g = lane / E;
+        const int x = (Cfg<T>::TMEM && E_LVL == FAN) ? l5_map(kL5VecMap, lane & (E - 1)) : lane & (E - 1);
+        const int g = lane / E;
         PHASE_T0();
         const NodeRef nr = node_ref<T>(tabs, E_LVL - 1, x);
         const T* P = sm + nr.off;
@@ -1161,7 +1175,7 @@ template <class T, int E_LVL> struct FanLevel {
             // odd lane keeps them).  Even-lane results cross over by shuffle; each lane
             // stores its node's state to its TMEM row in mir_slot order.
             static_assert(dn == kMirD && tn == 36 && E == 16, "mirror split layout");
-            const int xe = lane >> 1, h = lane & 1;
+            const int xe = l5_map(kL5PairMap, lane >> 1), h = lane & 1;
             const T* Pt = sm + node_ref<T>(tabs, E_LVL - 1, xe).off + 2 * m - 1;
             const T* uwe = uwv + xe * (2 * m + 1);
             T u[dn], w[dn];
@@ -1485,11 +1499,12 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 if constexpr (kConsFirst <= 3) FanLevel<T, 3>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
                 FanLevel<T, 4>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
                 FanLevel<T, FAN>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
-                const T vt = ctv[node_ref<T>(tabs, FAN, lane).tix];
+                const int node = l5_lane_node(lane);  // the level-5 node in this lane's TMEM row
+                const T vt = ctv[node_ref<T>(tabs, FAN, node).tix];
                 __syncwarp();
                 mb_arrive(8 + c);  // the producer may refill root..L3 and t values 0..6, 31
-                const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(lane) << L);
-                const int lsel = leaf_sel + __popc(lane);
+                const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(node) << L);
+                const int lsel = leaf_sel + __popc(node);
                 const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
                 acc.add(vt, nodeneg, lsel);
                 tmem_ext<T, L>(crow, crow + 4 * tri_sz(2 * L), vt, nodeneg, lmask, lsel, acc, err);
@@ -1552,7 +1567,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 T* fsm = area(2 * pair + slot);
                 T* ftv = fsm + SM::kTOff;
                 FanLevel<T, FAN>::run(fsm, ftv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
-                const int c = lane;
+                const int c = l5_lane_node(lane);
                 const T vt = ftv[node_ref<T>(tabs, FAN, c).tix];
                 const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(c) << L);
                 const int lsel = leaf_sel + __popc(c);
@@ -1585,10 +1600,10 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
             for (uint64_t leaf = 0; leaf < (1ull << D); ++leaf) {
                 produce_leaf(J, leaf, tm_row, sm, dfs_t, slots);
                 PHASE_T0();
-                // lanes: node (FAN, lane)
+                // lanes: node (FAN, c); TMEM rows hold the nodes of the level-5 lane map
                 const uint64_t leaf_mask = J.mask | (leaf << Q0);
                 const int leaf_sel = J.nsel + __popcll(leaf);
-                const int c = lane;
+                const int c = Cfg<T>::TMEM ? l5_lane_node(lane) : lane;
                 const NodeRef nr = node_ref<T>(tabs, FAN, c);
                 const T vt = tvals[nr.tix];
                 const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(c) << L);
