@@ -172,7 +172,8 @@ int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, i
 
 /* Partial sum over prefix classes [class_lo, class_hi) of the top class_bits mask
  * bits on one device (the subset of torontonian_partial's masks with those
- * prefixes).  prec must not be AUTO. */
+ * prefixes).  prec must not be AUTO.  N in [1, 50] (beyond the reference's 40: the
+ * paper's n = 50 case as checkpointable class ranges); slices, shards and plans only. */
 int tor_torontonian_slice(const tor_input* in, tor_precision prec, int class_bits, uint64_t class_lo,
                           uint64_t class_hi, int device, tor_partial* out, tor_error* err);
 

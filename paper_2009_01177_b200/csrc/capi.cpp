@@ -69,10 +69,17 @@ void parallel_for(int n, F f) {
         if (e) std::rethrow_exception(e);
 }
 
+// The reference's torontonian() takes N <= 40 (torontonian.cpp:153-154) and so does
+// tor_torontonian; prefix-class slices / shards / plans go to N = 50 (the paper's 100x100
+// case: checkpointable class ranges across devices and calls).
+constexpr int kMaxSliceModes = 50;
+
 Input checked_input(const tor_input* in, int nmax) {
     if (!in || in->n < 1 || in->n > nmax || !in->a00_upper || !in->a01_upper)
         throw HostError(TOR_E_INVALID, "torontonian/range",
-                        nmax == 20 ? "reference path supports 1 <= N <= 20" : "engine supports 1 <= N <= 40");
+                        nmax == 20   ? "reference path supports 1 <= N <= 20"
+                        : nmax == 40 ? "engine supports 1 <= N <= 40"
+                                     : "slices and shards support 1 <= N <= 50");
     Input a = make_input(in->n, in->a00_upper, in->a01_upper);
     for (auto* v : {&a.a00, &a.a01})
         for (const auto& x : *v)
@@ -435,7 +442,7 @@ int tor_torontonian_slice(const tor_input* in, tor_precision prec, int class_bit
                           uint64_t class_hi, int device, tor_partial* out, tor_error* err) {
     try {
         clear_err(err);
-        const Input a = checked_input(in, 40);
+        const Input a = checked_input(in, kMaxSliceModes);
         if (prec == TOR_PREC_AUTO) throw HostError(TOR_E_INVALID, "precision/range", "slice needs an explicit mode");
         if (class_bits < 0 || class_bits > a.n || class_hi <= class_lo || class_hi > (1ull << class_bits))
             throw HostError(TOR_E_INVALID, "torontonian/slice", "bad class range");
@@ -482,7 +489,7 @@ int tor_fold_partials(const tor_partial* parts, int count, const tor_input* in, 
     try {
         clear_err(err);
         if (count < 1 || !parts) throw HostError(TOR_E_INVALID, "torontonian/shard", "no partials");
-        const Input a = checked_input(in, 40);
+        const Input a = checked_input(in, kMaxSliceModes);
         const int mode = mode_of(static_cast<tor_precision>(parts[0].mode));
         std::vector<double> buf(static_cast<size_t>(count) * 5);
         uint64_t terms = 0;
@@ -514,7 +521,7 @@ int tor_plan_create(const tor_input* in, tor_precision prec, int class_bits, uin
     try {
         clear_err(err);
         *out = nullptr;
-        const Input a = checked_input(in, 40);
+        const Input a = checked_input(in, kMaxSliceModes);
         if (prec == TOR_PREC_AUTO || prec < TOR_PREC_AUTO || prec > TOR_PREC_FP64)
             throw HostError(TOR_E_INVALID, "precision/range", "plan needs an explicit mode");
         if (class_bits < 0 || class_bits > a.n || class_hi <= class_lo || class_hi > (1ull << class_bits))

@@ -39,8 +39,11 @@ namespace {
 
 constexpr int FAN = 5;  // breadth-first fan-out levels -> 32 lane nodes
 constexpr int MAX_LEVELS = 48;
-constexpr int kMaxJobModes = 24;
+// job states have <= kMaxJobModes modes: the prefix depth is c >= n - kMaxJobModes, and 32
+// keeps the prefix levels of an n = 50 shard (the paper's case) within a few GB
+constexpr int kMaxJobModes = 32;
 constexpr uint64_t kWantJobs = 262144;
+constexpr int kShardBits = 6;
 
 __host__ __device__ constexpr int tri_sz(int d) { return d * (d + 1) / 2; }
 __host__ __device__ __forceinline__ int tri_ix(int d, int i, int j) {
@@ -149,6 +152,8 @@ struct PrefixGeom {
     int c;                             // prefix depth
     size_t off[MAX_LEVELS + 1];        // entry offset of level e buffers (per instance)
     size_t toff[MAX_LEVELS + 1];       // offset of level e t values (per instance)
+    uint64_t plo[MAX_LEVELS + 1];      // level e stores include nodes p = plo[e] .. (compact: a
+                                       // shard keeps only the nodes under its class range)
     size_t inst_entries;               // entries per instance
     size_t inst_ts;                    // t values per instance
 };
@@ -389,9 +394,9 @@ __device__ __forceinline__ void node_view(const PrefixGeom& g, const T* pool, co
     const int lvl = e - tz;
     const uint64_t p = (c >> tz) >> 1;
     dim = 2 * (g.n - lvl);
-    base = ib + g.off[lvl] + p * static_cast<uint64_t>(tri_sz(dim));
+    base = ib + g.off[lvl] + (p - g.plo[lvl]) * static_cast<uint64_t>(tri_sz(dim));
     skip = tz;
-    t = tpool[inst * g.inst_ts + g.toff[lvl] + p];
+    t = tpool[inst * g.inst_ts + g.toff[lvl] + (p - g.plo[lvl])];
 }
 
 // Level e: every include node (inst, p), p in [plo, plo + cnt), eliminates the first
@@ -416,8 +421,8 @@ __global__ void prefix_level_kernel(PrefixGeom g, T* pool, T* tpool, int e, int 
         T t;
         node_view<T>(g, pool, tpool, inst, e - 1, p, base, dim, skip, t);
         const int q = g.n - (e - 1);
-        T* dst = pool + inst * g.inst_entries + g.off[e] + p * static_cast<uint64_t>(tri_sz(2 * (g.n - e)));
-        T* tdst = tpool + inst * g.inst_ts + g.toff[e] + p;
+        T* dst = pool + inst * g.inst_entries + g.off[e] + (p - g.plo[e]) * static_cast<uint64_t>(tri_sz(2 * (g.n - e)));
+        T* tdst = tpool + inst * g.inst_ts + g.toff[e] + (p - g.plo[e]);
         const uint64_t mask = ((p << 1) | 1ull) << (g.n - e);
         warp_elim<T>(base, dim, 2 * skip, q, dst, t, tdst, uw, mask, __popcll(mask) - 1, err, part, parts);
     }
@@ -1008,7 +1013,8 @@ template <class T> struct WarpSmem {
     static constexpr int kUwOff = kTOff + 32;
     static constexpr int kUwEntries = uw_need();
     static constexpr int kDfsT = kUwOff + kUwEntries;  // DFS slot t values (<= 32)
-    static constexpr int kEntries = kDfsT + 32;
+    // (warp-specialised: the DFS t values are producer-private, see kProdEntries)
+    static constexpr int kEntries = kDfsT + (Cfg<T>::WS_MODE == 2 ? 0 : 32);
     // WS mode 2 producer-private: pivot-row vectors of the DFS and levels 1..3, DFS t
     // values of its two job contexts
     __host__ __device__ static constexpr int prod_uw() {
@@ -1846,6 +1852,15 @@ class PlanImpl final : public Plan {
             while ((static_cast<uint64_t>(ninst_) << cw) < want_jobs && cw < n_ - Q0) ++cw;
             c_ = std::max(cw, n_ - kMaxJobModes);
             c_ = std::min(c_, n_ - Q0);
+            // Narrow slices (more than kShardBits class bits, e.g. checkpointed n = 50
+            // pieces) deepen the prefix until the slice itself holds kWantJobs jobs; shards
+            // of up to 2^kShardBits ranks keep the whole-problem depth (bit-identical folds).
+            if (kbits_ > kShardBits) {
+                int cs = kbits_;
+                while (((chi_ - clo_) * static_cast<uint64_t>(ninst_) << (cs - kbits_)) < want_jobs && cs < n_ - Q0)
+                    ++cs;
+                c_ = std::max(c_, cs);
+            }
         }
         use_levels_ = kbits_ <= c_;
         cj_ = use_levels_ ? c_ : kbits_;
@@ -1858,10 +1873,15 @@ class PlanImpl final : public Plan {
         g_.c = use_levels_ ? c_ : 0;
         size_t o = tri_sz(2 * n_), to = 0;
         for (int e = 1; e <= g_.c; ++e) {
+            // the level-e buffers under this plan's class range: the e-bit prefixes of
+            // [lo, hi) ending in an include, p = prefix >> 1 (a contiguous range)
+            const uint64_t lo = clo_ << (c_ - kbits_), hi = chi_ << (c_ - kbits_);
+            const uint64_t plo = lo >> (c_ - e + 1), phi = (hi - 1) >> (c_ - e + 1);
+            g_.plo[e] = plo;
             g_.off[e] = o;
             g_.toff[e] = to;
-            o += (static_cast<size_t>(1) << (e - 1)) * tri_sz(2 * (n_ - e));
-            to += static_cast<size_t>(1) << (e - 1);
+            o += (phi - plo + 1) * tri_sz(2 * (n_ - e));
+            to += phi - plo + 1;
         }
         g_.inst_entries = o;
         g_.inst_ts = std::max<size_t>(to, 1);
@@ -1961,9 +1981,8 @@ class PlanImpl final : public Plan {
             const size_t sm = sizeof(T) * 4 * n_ * wpb;
             const uint64_t lo = clo_ << (c_ - kbits_), hi = chi_ << (c_ - kbits_);
             for (int e = 1; e <= g_.c; ++e) {
-                // only the level-e buffers under this plan's class range: the e-bit prefixes
-                // of [lo, hi) ending in an include, p = prefix >> 1 (a contiguous range)
-                const uint64_t plo = lo >> (c_ - e + 1), phi = (hi - 1) >> (c_ - e + 1);
+                // only the level-e buffers under this plan's class range (PrefixGeom::plo)
+                const uint64_t plo = g_.plo[e], phi = (hi - 1) >> (c_ - e + 1);
                 const uint64_t cnt = phi - plo + 1;
                 const uint64_t items = cnt * ninst_;
                 // few nodes: several warps per elimination (>= 128 trailing entries each)

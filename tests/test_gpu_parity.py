@@ -310,3 +310,36 @@ def test_uneven_class_ranges(prec, mode):
         assert sum_abs == pytest.approx(whole["sum_abs_terms"], rel=1e-12)
         ok, rel = within(total, words_value(whole["words"]), whole["sum_abs_terms"], mode)
         assert ok, f"k={k} cuts={cuts}: {rel:.3g} sum|t|"
+
+
+def _cfg5_extended(n):
+    # config 5's m = 100 state, its 40 click modes plus the lowest unused ones
+    from paper_2009_01177_b200.matrix import select_modes
+    sel = set(W.click_set(5))
+    extra = [j for j in range(100) if j not in sel][: n - 40]
+    return select_modes(W.full_state(5), sorted(sel | set(extra)))
+
+
+def test_slices_beyond_n40():
+    # the reference's torontonian() takes N <= 40; slices / shards go to N = 50 (the paper's
+    # 100 x 100 case) as checkpointable class ranges.  n = 44: one class at k = 22 (2^22
+    # subsets) in DD and QD, and its refinement into two classes at k = 23.
+    m = _cfg5_extended(44)
+    with pytest.raises(T.InvalidArgument):
+        T.torontonian(m, "128")
+    k, cls = 22, 0x2a5a5
+    dd = T.torontonian_slice(m, "128", k, cls, cls + 1)
+    qd = T.torontonian_slice(m, "256", k, cls, cls + 1)
+    ok, rel = within(words_value(dd["words"]), words_value(qd["words"]), qd["sum_abs"], "dd")
+    assert ok, f"DD vs QD {rel:.3g} sum|t|"
+    assert dd["term_count"] == 1 << (44 - k)
+    halves = [T.torontonian_slice(m, "256", k + 1, 2 * cls + h, 2 * cls + h + 1) for h in (0, 1)]
+    tot = words_value(halves[0]["words"]) + words_value(halves[1]["words"])
+    ok, rel = within(tot, words_value(qd["words"]), qd["sum_abs"], "qd")
+    assert ok, f"refinement {rel:.3g} sum|t|"
+    # a whole-range slice at n = 50 is accepted and sized by class range (shard of 2^14)
+    m50 = _cfg5_extended(50)
+    p = T.torontonian_slice(m50, "128", 30, 12345, 12346)
+    assert p["term_count"] == 1 << 20 and p["sum_abs"] > 0
+    with pytest.raises(T.InvalidArgument):
+        T.torontonian_slice(_cfg5_extended(51), "128", 30, 0, 1)

@@ -215,3 +215,15 @@ def test_batch_validation_errors_before_device():
     with pytest.raises(T.InvalidArgument) as e:
         T.torontonian_batch(good + [diag_instance(4, [0.1] * 4)] + good[:10], "fp64")
     assert e.value.code == "torontonian/range"
+
+
+def test_slice_range_beyond_reference_limit():
+    # tor_torontonian keeps the reference's N <= 40; slices/shards/plans accept N <= 50
+    with pytest.raises(T.InvalidArgument):
+        T.torontonian(diag_instance(41, [0.1] * 41), "128")
+    with pytest.raises(T.InvalidArgument) as e:
+        T.torontonian_slice(diag_instance(51, [0.1] * 51), "128", 30, 0, 1)
+    assert "50" in str(e.value)
+    if T.device_count() == 0:
+        with pytest.raises(T.DeviceError):  # validated, then needs the device
+            T.torontonian_slice(diag_instance(50, [0.1] * 50), "128", 30, 0, 1)
