@@ -988,10 +988,18 @@ template <class T> struct WarpSmem {
     // parents, read lane-pair-wise by FanLevel<5>) then start on every 16-byte bank slot
     // mod 8 exactly twice and the 8 level-3 nodes on distinct slots, so those reads are
     // free of bank conflicts (found by exhaustive search over small paddings).
+    // fp64 (8-byte words, level-5 states in shared memory, read lane-wise by the lane
+    // subtrees in two 16-lane phases of 8-byte banks): base pads (0,0,1,2,8) and stride
+    // adds (1,0,3,0,0) for levels 1..5 (24 entries per area) cut the worst per-phase
+    // multiplicity of the 32 level-5 node bases mod 16 from 3+3 to 2+1
+    // (tools/f64_layout_search.py).
+    static constexpr bool kF64Pad = sizeof(T) == sizeof(double) && !Cfg<T>::TMEM;
     __host__ __device__ static constexpr int lvl_pad(int e) {
+        if constexpr (kF64Pad) return e == 3 ? 1 : (e == 4 ? 2 : (e == 5 ? 8 : 0));
         return Cfg<T>::TMEM ? (e == 1 ? 2 : (e == 2 ? 1 : 0)) : 0;
     }
     __host__ __device__ static constexpr int buf_stride(int e) {
+        if constexpr (kF64Pad) return tri_sz(2 * (Q0 - e)) + (e == 1 ? 1 : (e == 3 ? 3 : 0));
         return tri_sz(2 * (Q0 - e)) + (Cfg<T>::TMEM && e == 2 ? 1 : 0);
     }
     __host__ __device__ static constexpr int lvl_off(int e) {
