@@ -256,6 +256,16 @@ def main():
         if s >= args.warmup:
             e2e_ms.append(dt)
     e2e_step = statistics.median(e2e_ms)
+    # bytes moved per step, all ranks: each rank uploads the exact R (the single-device
+    # call reports its own counts) and reads back its partial; with N > 1 each rank also
+    # uploads its 10-double partial for the all-gather and reads the N gathered ones back
+    words = {"fp64": 1, "dd": 2, "qd": 4}[dtype]
+    r_bytes = (2 * n) * (2 * n + 1) // 2 * words * 8
+    if world == 1:
+        h2d_step, d2h_step = int(result.get("h2d_bytes", r_bytes)), int(result.get("d2h_bytes", 48))
+    else:
+        h2d_step = world * (r_bytes + 80)
+        d2h_step = world * (48 + world * 80)
 
     if rank == 0:
         def _load(name):
@@ -302,9 +312,7 @@ def main():
                        "l2": "flushed between steps (256 MiB write)", "prefix_classes_per_rank": f"2^{k} split",
                        "parallelism": f"prefix-class shards x{world}"},
             "e2e": {"value": terms_total / (e2e_step * 1e-3), "unit": UNIT,
-                    "h2d_bytes_per_step": int(result.get("h2d_bytes", 0)) if world == 1 else None,
-                    "d2h_bytes_per_step": int(result.get("d2h_bytes", 0)) if world == 1 else None,
-                    "ms_per_step": e2e_step},
+                    "h2d_bytes_per_step": h2d_step, "d2h_bytes_per_step": d2h_step, "ms_per_step": e2e_step},
             "gpu_launches": int(launches) * args.steps,
             "kernel_ms_per_step": kstep_ms,
             "result": {"value": result["value"], "words": list(result["words"]),
