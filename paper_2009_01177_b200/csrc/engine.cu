@@ -1450,6 +1450,13 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                     : "r"(a), "r"(parity), "r"(1000000u)
                     : "memory");
         };
+#ifndef TOR_WS_REGS
+#define TOR_WS_REGS 0  // e.g. 120: producers give registers to the consumers (setmaxnreg)
+#endif
+        if constexpr (TOR_WS_REGS > 0) {
+            if (wib < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(TOR_WS_REGS));
+            else asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(168 + (168 - TOR_WS_REGS) / 2));
+        }
         if (wib < 4) {
             const int p = wib;
             Job<T> J[2];
