@@ -343,3 +343,15 @@ def test_slices_beyond_n40():
     assert p["term_count"] == 1 << 20 and p["sum_abs"] > 0
     with pytest.raises(T.InvalidArgument):
         T.torontonian_slice(_cfg5_extended(51), "128", 30, 0, 1)
+
+
+def test_batch_beyond_grid_y_limit():
+    # 70000 instances: the per-instance fold passes run in chunks of 65535 grid rows
+    base = [W.generate_instance(12, 0.16, 0.06, s) for s in range(1, 9)]
+    ms = [base[i % 8] for i in range(70000)]
+    rs = T.torontonian_batch(ms, "128")
+    singles = [T.torontonian(b, "128") for b in base]
+    for i in (0, 7, 65534, 65535, 65536, 69999):
+        want = singles[i % 8]
+        ok, rel = within(words_value(rs[i]["words"]), words_value(want["words"]), want["sum_abs_terms"], "dd")
+        assert ok, f"item {i}: {rel:.3g} sum|t|"
