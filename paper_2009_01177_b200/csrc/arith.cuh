@@ -402,8 +402,13 @@ struct QAcc {  // exact running sum of one order; errors go to the next order's 
         err = e;
     }
 };
+#ifndef TOR_QD_R2_INLINE
+#define TOR_HD_R2 TOR_HD_RNI
+#else
+#define TOR_HD_R2 TOR_HD
+#endif
 template <bool kNorm>
-TOR_HD_RNI qd qd_rank2_fused(qd s, qd a, qd b, qd c, qd d) {
+TOR_HD_R2 qd qd_rank2_fused(qd s, qd a, qd b, qd c, qd d) {
     double p0, e0, q0, f0;
     two_prod(a.x[0], b.x[0], p0, e0);
     two_prod(c.x[0], d.x[0], q0, f0);
@@ -548,9 +553,12 @@ TOR_UNROLL
 // when the leading word has cancelled; entries are renormalised where they become
 // pivots, and the products that consume them renormalise their results.
 #ifndef TOR_QD_UNFUSED
-TOR_HD_RNI qd qd_rank2(qd s, qd a, qd b, qd c, qd d) { return qd_rank2_fused<!kQdLazy>(s, a, b, c, d); }
-TOR_HD_RNI qd qd_rank1(qd s, qd a, qd b) { return qd_rank1_fused<true>(s, a, b); }
-TOR_HD_RNI qd qd_rank1_lazy(qd s, qd a, qd b) { return qd_rank1_fused<!kQdLazy>(s, a, b); }
+// (thin inline wrappers: one out-of-line call per update, to the fused body)
+TOR_HD qd qd_rank2(const qd& s, const qd& a, const qd& b, const qd& c, const qd& d) {
+    return qd_rank2_fused<!kQdLazy>(s, a, b, c, d);
+}
+TOR_HD qd qd_rank1(const qd& s, const qd& a, const qd& b) { return qd_rank1_fused<true>(s, a, b); }
+TOR_HD qd qd_rank1_lazy(const qd& s, const qd& a, const qd& b) { return qd_rank1_fused<!kQdLazy>(s, a, b); }
 #else
 // s - a*b - c*d.
 TOR_HD_RNI qd qd_rank2(qd s, qd a, qd b, qd c, qd d) {
