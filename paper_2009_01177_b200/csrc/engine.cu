@@ -44,6 +44,10 @@ constexpr int MAX_LEVELS = 48;
 constexpr int kMaxJobModes = 32;
 constexpr uint64_t kWantJobs = 262144;
 constexpr int kShardBits = 6;
+#ifndef TOR_MB_HINT
+#define TOR_MB_HINT 100  // mbarrier try_wait suspend-time hint (ns): 1e6 measured 0.3% slower
+#endif
+
 
 __host__ __device__ constexpr int tri_sz(int d) { return d * (d + 1) / 2; }
 __host__ __device__ __forceinline__ int tri_ix(int d, int i, int j) {
@@ -1447,7 +1451,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 asm volatile(
                     "{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p;}\n"
                     : "=r"(ok)
-                    : "r"(a), "r"(parity), "r"(1000000u)
+                    : "r"(a), "r"(parity), "r"(static_cast<uint32_t>(TOR_MB_HINT))
                     : "memory");
         };
 #ifndef TOR_WS_REGS
