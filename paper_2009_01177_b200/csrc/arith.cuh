@@ -394,14 +394,36 @@ TOR_HD qd qd_mul_d(const qd& a, double b) {
 #define TOR_QD_LAZY 1
 #endif
 constexpr bool kQdLazy = TOR_QD_LAZY;
-struct QAcc {  // exact running sum of one order; errors go to the next order's list
-    double h;
-    TOR_HD void add(double t, double& err) {
-        double e;
-        two_sum(h, t, h, e);
-        err = e;
+// Exact pairwise (tree) sum of N doubles: the rounded total, and the N - 1 TwoSum errors
+// in a fixed order.  ceil(log2 N) dependent TwoSums instead of N - 1 for a running sum --
+// the QD kernel runs one warp per SM sub-partition, so its time is these chains.
+template <int N>
+TOR_HD double tree_sum(const double (&t)[N], double* err) {
+    if constexpr (N == 1) {
+        return t[0];
+    } else {
+        constexpr int H = N / 2;
+        double u[N - H];
+        TOR_UNROLL
+        for (int i = 0; i < H; ++i) two_sum(t[2 * i], t[2 * i + 1], u[i], err[i]);
+        if constexpr (N & 1) u[H] = t[N - 1];
+        return tree_sum<N - H>(u, err + H);
     }
-};
+}
+// plain pairwise sum (the last order: its rounding errors are below the QD budget)
+template <int N>
+TOR_HD double tree_add(const double (&t)[N]) {
+    if constexpr (N == 1) {
+        return t[0];
+    } else {
+        constexpr int H = N / 2;
+        double u[N - H];
+        TOR_UNROLL
+        for (int i = 0; i < H; ++i) u[i] = t[2 * i] + t[2 * i + 1];
+        if constexpr (N & 1) u[H] = t[N - 1];
+        return tree_add<N - H>(u);
+    }
+}
 #ifndef TOR_QD_R2_INLINE
 #define TOR_HD_R2 TOR_HD_RNI
 #else
@@ -412,27 +434,11 @@ TOR_HD_R2 qd qd_rank2_fused(qd s, qd a, qd b, qd c, qd d) {
     double p0, e0, q0, f0;
     two_prod(a.x[0], b.x[0], p0, e0);
     two_prod(c.x[0], d.x[0], q0, f0);
-    double l1[8];
-    QAcc o0{s.x[0]};
-    o0.add(-p0, l1[0]);
-    o0.add(-q0, l1[1]);
-    // order 1
     double pa, ea, pb, eb, qa, fa, qb, fb;
     two_prod(a.x[0], b.x[1], pa, ea);
     two_prod(a.x[1], b.x[0], pb, eb);
     two_prod(c.x[0], d.x[1], qa, fa);
     two_prod(c.x[1], d.x[0], qb, fb);
-    QAcc o1{s.x[1]};
-    double l2[18];
-    o1.add(l1[0], l2[0]);
-    o1.add(l1[1], l2[1]);
-    o1.add(-e0, l2[2]);
-    o1.add(-f0, l2[3]);
-    o1.add(-pa, l2[4]);
-    o1.add(-pb, l2[5]);
-    o1.add(-qa, l2[6]);
-    o1.add(-qb, l2[7]);
-    // order 2
     double r[6], re[6];
     two_prod(a.x[0], b.x[2], r[0], re[0]);
     two_prod(a.x[1], b.x[1], r[1], re[1]);
@@ -440,111 +446,77 @@ TOR_HD_R2 qd qd_rank2_fused(qd s, qd a, qd b, qd c, qd d) {
     two_prod(c.x[0], d.x[2], r[3], re[3]);
     two_prod(c.x[1], d.x[1], r[4], re[4]);
     two_prod(c.x[2], d.x[0], r[5], re[5]);
-    QAcc o2{s.x[2]};
+    // order 0
+    const double t0[3] = {s.x[0], -p0, -q0};
+    double l1[2];
+    const double h0 = tree_sum(t0, l1);
+    // order 1
+    const double t1[9] = {s.x[1], l1[0], l1[1], -e0, -f0, -pa, -pb, -qa, -qb};
+    double l2[8];
+    const double h1 = tree_sum(t1, l2);
+    // order 2
+    const double t2[19] = {s.x[2], l2[0], l2[1], l2[2], l2[3], l2[4], l2[5], l2[6], l2[7], -ea, -eb, -fa, -fb,
+                           -r[0],  -r[1], -r[2], -r[3], -r[4], -r[5]};
     double l3[18];
-TOR_UNROLL
-    for (int i = 0; i < 8; ++i) o2.add(l2[i], l3[i]);
-    o2.add(-ea, l3[8]);
-    o2.add(-eb, l3[9]);
-    o2.add(-fa, l3[10]);
-    o2.add(-fb, l3[11]);
-TOR_UNROLL
-    for (int i = 0; i < 6; ++i) o2.add(-r[i], l3[12 + i]);
+    const double h2 = tree_sum(t2, l3);
     // order 3: plain
-    double h3 = s.x[3];
-TOR_UNROLL
-    for (int i = 0; i < 18; ++i) h3 += l3[i];
-TOR_UNROLL
-    for (int i = 0; i < 6; ++i) h3 -= re[i];
-    double t3 = a.x[0] * b.x[3];
-    t3 = fma_(a.x[1], b.x[2], t3);
-    t3 = fma_(a.x[2], b.x[1], t3);
-    t3 = fma_(a.x[3], b.x[0], t3);
-    t3 = fma_(c.x[0], d.x[3], t3);
-    t3 = fma_(c.x[1], d.x[2], t3);
-    t3 = fma_(c.x[2], d.x[1], t3);
-    t3 = fma_(c.x[3], d.x[0], t3);
-    h3 -= t3;
-    if constexpr (kNorm) return qd_renorm5_bf(o0.h, o1.h, o2.h, h3, 0.0);
-    else return qd{{o0.h, o1.h, o2.h, h3}};
+    const double t3[28] = {s.x[3], l3[0], l3[1], l3[2], l3[3], l3[4], l3[5], l3[6], l3[7], l3[8],
+                           l3[9],  l3[10], l3[11], l3[12], l3[13], l3[14], l3[15], l3[16], l3[17],
+                           -re[0], -re[1], -re[2], -re[3], -re[4], -re[5],
+                           -fma_(a.x[0], b.x[3], a.x[1] * b.x[2]), -fma_(a.x[2], b.x[1], a.x[3] * b.x[0]),
+                           -fma_(c.x[0], d.x[3], fma_(c.x[1], d.x[2], fma_(c.x[2], d.x[1], c.x[3] * d.x[0])))};
+    const double h3 = tree_add(t3);
+    if constexpr (kNorm) return qd_renorm5_bf(h0, h1, h2, h3, 0.0);
+    else return qd{{h0, h1, h2, h3}};
 }
 // s - a*b, same scheme
 template <bool kNorm>
 TOR_HD_RNI qd qd_rank1_fused(qd s, qd a, qd b) {
-    double p0, e0;
+    double p0, e0, pa, ea, pb, eb, r[3], re[3];
     two_prod(a.x[0], b.x[0], p0, e0);
-    double l1;
-    QAcc o0{s.x[0]};
-    o0.add(-p0, l1);
-    double pa, ea, pb, eb;
     two_prod(a.x[0], b.x[1], pa, ea);
     two_prod(a.x[1], b.x[0], pb, eb);
-    QAcc o1{s.x[1]};
-    double l2[4];
-    o1.add(l1, l2[0]);
-    o1.add(-e0, l2[1]);
-    o1.add(-pa, l2[2]);
-    o1.add(-pb, l2[3]);
-    double r[3], re[3];
     two_prod(a.x[0], b.x[2], r[0], re[0]);
     two_prod(a.x[1], b.x[1], r[1], re[1]);
     two_prod(a.x[2], b.x[0], r[2], re[2]);
-    QAcc o2{s.x[2]};
+    const double t0[2] = {s.x[0], -p0};
+    double l1[1];
+    const double h0 = tree_sum(t0, l1);
+    const double t1[5] = {s.x[1], l1[0], -e0, -pa, -pb};
+    double l2[4];
+    const double h1 = tree_sum(t1, l2);
+    const double t2[10] = {s.x[2], l2[0], l2[1], l2[2], l2[3], -ea, -eb, -r[0], -r[1], -r[2]};
     double l3[9];
-TOR_UNROLL
-    for (int i = 0; i < 4; ++i) o2.add(l2[i], l3[i]);
-    o2.add(-ea, l3[4]);
-    o2.add(-eb, l3[5]);
-TOR_UNROLL
-    for (int i = 0; i < 3; ++i) o2.add(-r[i], l3[6 + i]);
-    double h3 = s.x[3];
-TOR_UNROLL
-    for (int i = 0; i < 9; ++i) h3 += l3[i];
-TOR_UNROLL
-    for (int i = 0; i < 3; ++i) h3 -= re[i];
-    double t3 = a.x[0] * b.x[3];
-    t3 = fma_(a.x[1], b.x[2], t3);
-    t3 = fma_(a.x[2], b.x[1], t3);
-    t3 = fma_(a.x[3], b.x[0], t3);
-    h3 -= t3;
-    if constexpr (kNorm) return qd_renorm5_bf(o0.h, o1.h, o2.h, h3, 0.0);
-    else return qd{{o0.h, o1.h, o2.h, h3}};
+    const double h2 = tree_sum(t2, l3);
+    const double t3[14] = {s.x[3], l3[0], l3[1], l3[2], l3[3], l3[4], l3[5], l3[6], l3[7], l3[8],
+                           -re[0], -re[1], -re[2],
+                           -fma_(a.x[0], b.x[3], fma_(a.x[1], b.x[2], fma_(a.x[2], b.x[1], a.x[3] * b.x[0])))};
+    const double h3 = tree_add(t3);
+    if constexpr (kNorm) return qd_renorm5_bf(h0, h1, h2, h3, 0.0);
+    else return qd{{h0, h1, h2, h3}};
 }
 // a*b by the same order-collected scheme (products have no cancellation: without the
 // final renormalisation the words are still ordered 2^-53k relative to |ab|)
 template <bool kNorm>
 TOR_HD_RNI qd qd_mul_fused(qd a, qd b) {
-    double p0, e0;
+    double p0, e0, pa, ea, pb, eb, r[3], re[3];
     two_prod(a.x[0], b.x[0], p0, e0);
-    double pa, ea, pb, eb;
     two_prod(a.x[0], b.x[1], pa, ea);
     two_prod(a.x[1], b.x[0], pb, eb);
-    QAcc o1{e0};
-    double l2[2];
-    o1.add(pa, l2[0]);
-    o1.add(pb, l2[1]);
-    double r[3], re[3];
     two_prod(a.x[0], b.x[2], r[0], re[0]);
     two_prod(a.x[1], b.x[1], r[1], re[1]);
     two_prod(a.x[2], b.x[0], r[2], re[2]);
-    QAcc o2{r[0]};
+    const double t1[3] = {e0, pa, pb};
+    double l2[2];
+    const double h1 = tree_sum(t1, l2);
+    const double t2[7] = {r[0], r[1], r[2], ea, eb, l2[0], l2[1]};
     double l3[6];
-    o2.add(r[1], l3[0]);
-    o2.add(r[2], l3[1]);
-    o2.add(ea, l3[2]);
-    o2.add(eb, l3[3]);
-    o2.add(l2[0], l3[4]);
-    o2.add(l2[1], l3[5]);
-    double h3 = re[0] + re[1];
-    h3 += re[2];
-TOR_UNROLL
-    for (int i = 0; i < 6; ++i) h3 += l3[i];
-    h3 = fma_(a.x[0], b.x[3], h3);
-    h3 = fma_(a.x[1], b.x[2], h3);
-    h3 = fma_(a.x[2], b.x[1], h3);
-    h3 = fma_(a.x[3], b.x[0], h3);
-    if constexpr (kNorm) return qd_renorm5_bf(p0, o1.h, o2.h, h3, 0.0);
-    else return qd{{p0, o1.h, o2.h, h3}};
+    const double h2 = tree_sum(t2, l3);
+    const double t3[10] = {re[0], re[1], re[2], l3[0], l3[1], l3[2], l3[3], l3[4], l3[5],
+                           fma_(a.x[0], b.x[3], fma_(a.x[1], b.x[2], fma_(a.x[2], b.x[1], a.x[3] * b.x[0])))};
+    const double h3 = tree_add(t3);
+    if constexpr (kNorm) return qd_renorm5_bf(p0, h1, h2, h3, 0.0);
+    else return qd{{p0, h1, h2, h3}};
 }
 
 // Schur-state updates skip the final renormalisation (like the lazy DD products): every
