@@ -430,7 +430,7 @@ TOR_HD double tree_add(const double (&t)[N]) {
 #define TOR_HD_R2 TOR_HD
 #endif
 template <bool kNorm>
-TOR_HD_R2 qd qd_rank2_fused(qd s, qd a, qd b, qd c, qd d) {
+TOR_HD qd qd_rank2_body(const qd& s, const qd& a, const qd& b, const qd& c, const qd& d) {
     double p0, e0, q0, f0;
     two_prod(a.x[0], b.x[0], p0, e0);
     two_prod(c.x[0], d.x[0], q0, f0);
@@ -468,6 +468,10 @@ TOR_HD_R2 qd qd_rank2_fused(qd s, qd a, qd b, qd c, qd d) {
     const double h3 = tree_add(t3);
     if constexpr (kNorm) return qd_renorm5_bf(h0, h1, h2, h3, 0.0);
     else return qd{{h0, h1, h2, h3}};
+}
+template <bool kNorm>
+TOR_HD_R2 qd qd_rank2_fused(qd s, qd a, qd b, qd c, qd d) {
+    return qd_rank2_body<kNorm>(s, a, b, c, d);
 }
 // s - a*b, same scheme
 template <bool kNorm>
@@ -596,6 +600,7 @@ template <> struct Arith<double> {
         return fma_(-c, d, fma_(-a, b, s));
     }
     TOR_HD static double rank1(double s, double a, double b) { return fma_(-a, b, s); }
+    TOR_HD static double rank2_item(double s, double a, double b, double c, double d) { return rank2(s, a, b, c, d); }
     TOR_HD static double rank1s(double s, double a, double b) { return fma_(-a, b, s); }
     TOR_HD static double rsqrt(double a) { return rsqrt_d(a); }
     TOR_HD static double unb(double a) { return a; }
@@ -643,6 +648,9 @@ template <> struct Arith<dd> {
 #endif
     // general (non-state) s - a*b
     TOR_HD static dd rank1(const dd& s, const dd& a, const dd& b) { return dd_rank1(s, a, b); }
+    TOR_HD static dd rank2_item(const dd& s, const dd& a, const dd& b, const dd& c, const dd& d) {
+        return rank2(s, a, b, c, d);
+    }
     TOR_HD static dd rsqrt(const dd& a) { return dd_rsqrt(a); }
     TOR_HD static dd neg(const dd& a) { return dd_neg(a); }
     TOR_HD static void words(const dd& a, double* w) {
@@ -666,6 +674,16 @@ template <> struct Arith<qd> {
     TOR_HD static qd rank2(const qd& s, const qd& a, const qd& b, const qd& c, const qd& d) {
         return qd_rank2(s, a, b, c, d);
     }
+#ifdef TOR_QD_ITEM_INLINE
+    // the fan-out item loops' update, inlined (one copy per fan-out level)
+    TOR_HD static qd rank2_item(const qd& s, const qd& a, const qd& b, const qd& c, const qd& d) {
+        return qd_rank2_body<!kQdLazy>(s, a, b, c, d);
+    }
+#else
+    TOR_HD static qd rank2_item(const qd& s, const qd& a, const qd& b, const qd& c, const qd& d) {
+        return rank2(s, a, b, c, d);
+    }
+#endif
     TOR_HD static qd rank1(const qd& s, const qd& a, const qd& b) { return qd_rank1(s, a, b); }
     TOR_HD static qd rank1s(const qd& s, const qd& a, const qd& b) { return qd_rank1_lazy(s, a, b); }
     TOR_HD static qd rsqrt(const qd& a) { return qd_rsqrt(a); }

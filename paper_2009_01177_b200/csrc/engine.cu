@@ -1242,7 +1242,7 @@ template <class T, int E_LVL> struct FanLevel {
                 wj[u] = uwv[b + m];
             }
 #pragma unroll
-            for (int u = 0; u < UB; ++u) sv[u] = A::rank2(sv[u], ui[u], uj[u], wi[u], wj[u]);
+            for (int u = 0; u < UB; ++u) sv[u] = A::rank2_item(sv[u], ui[u], uj[u], wi[u], wj[u]);
 #pragma unroll
             for (int u = 0; u < UB; ++u) {
                 const int s = s0 + u;
