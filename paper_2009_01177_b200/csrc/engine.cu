@@ -776,12 +776,31 @@ template <class T, int M, int K, int END> struct LtUpd {
 };
 // Loads entries [K0, K0+N) of this lane's D-row TMEM state (issue only; tm_wait_ld
 // before use).
+__device__ __forceinline__ void tm_ld16(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+}
+#ifndef TOR_TM_LD16
+#define TOR_TM_LD16 1
+#endif
 template <int D, int K, int N> struct TmLd {
     __device__ __forceinline__ static void run(uint32_t row, uint32_t* r) {
         if constexpr (N > 0) {
             constexpr int col = tm_col<D>(K);
-            tm_ld4(row + col, r[0], r[1], r[2], r[3]);
-            TmLd<D, K + 1, N - 1>::run(row, r + 4);
+            // natural column layout (the scratch states): four consecutive entries per
+            // 16-column load
+            if constexpr (TOR_TM_LD16 && N >= 4 && D != kMirD) {
+                tm_ld16(row + col, r);
+                TmLd<D, K + 4, N - 4>::run(row, r + 16);
+            } else {
+                tm_ld4(row + col, r[0], r[1], r[2], r[3]);
+                TmLd<D, K + 1, N - 1>::run(row, r + 4);
+            }
         }
     }
 };
