@@ -874,25 +874,58 @@ __device__ __forceinline__ void lane_tree_tmem(uint32_t row, const T& t, bool ne
 // by entry into the scratch columns scr (natural layout), the exclude child (the
 // parent's trailing block) is copied there, and one copy of the (L-1)-mode code runs
 // for both; the 3-mode level keeps its children (2 modes) in registers.
+// entries K..K+Q-1 of the trailing update into 4Q words (compile-time (i,j))
+template <class T, int M, int K, int Q> struct LtQuad {
+    __device__ __forceinline__ static void run(const uint32_t* rt, const T (&u)[M], const T (&w)[M], uint32_t* r) {
+        if constexpr (Q > 0) {
+            constexpr int D = M - 2;
+            constexpr int i = tri_row(D, K), j = tri_col(D, K);
+            const T v =
+                Arith<T>::rank2(u32_to_dd(rt[0], rt[1], rt[2], rt[3]), u[2 + i], u[2 + j], w[2 + i], w[2 + j]);
+            dd_to_u32(v, r);
+            LtQuad<T, M, K + 1, Q - 1>::run(rt + 4, u, w, r + 4);
+        }
+    }
+};
+__device__ __forceinline__ void tm_st16p(uint32_t taddr, const uint32_t* r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16};\n" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
 template <class T, int M, int K, int END> struct LtUpdTm {
     __device__ __forceinline__ static void run(const uint32_t* rt, const T (&u)[M], const T (&w)[M], uint32_t dst) {
         if constexpr (K < END) {
             constexpr int D = M - 2;
             constexpr int i = tri_row(D, K), j = tri_col(D, K);
-            const T v =
-                Arith<T>::rank2(u32_to_dd(rt[0], rt[1], rt[2], rt[3]), u[2 + i], u[2 + j], w[2 + i], w[2 + j]);
-            uint32_t r[4];
-            dd_to_u32(v, r);
-            tm_st4(dst + tm_col<D>(K), r[0], r[1], r[2], r[3]);
-            LtUpdTm<T, M, K + 1, END>::run(rt + 4, u, w, dst);
+            if constexpr (TOR_TM_LD16 && END - K >= 4) {
+                // four entries, one 16-column store (natural scratch layout)
+                uint32_t r[16];
+                LtQuad<T, M, K, 4>::run(rt, u, w, r);
+                tm_st16p(dst + tm_col<D>(K), r);
+                LtUpdTm<T, M, K + 4, END>::run(rt + 16, u, w, dst);
+            } else {
+                const T v = Arith<T>::rank2(u32_to_dd(rt[0], rt[1], rt[2], rt[3]), u[2 + i], u[2 + j], w[2 + i],
+                                            w[2 + j]);
+                uint32_t r[4];
+                dd_to_u32(v, r);
+                tm_st4(dst + tm_col<D>(K), r[0], r[1], r[2], r[3]);
+                LtUpdTm<T, M, K + 1, END>::run(rt + 4, u, w, dst);
+            }
         }
     }
 };
 template <int D, int K, int END> struct TmCopy {
     __device__ __forceinline__ static void run(const uint32_t* rt, uint32_t dst) {
         if constexpr (K < END) {
-            tm_st4(dst + tm_col<D - 2>(K), rt[0], rt[1], rt[2], rt[3]);
-            TmCopy<D, K + 1, END>::run(rt + 4, dst);
+            if constexpr (TOR_TM_LD16 && END - K >= 4) {
+                tm_st16p(dst + tm_col<D - 2>(K), rt);
+                TmCopy<D, K + 4, END>::run(rt + 16, dst);
+            } else {
+                tm_st4(dst + tm_col<D - 2>(K), rt[0], rt[1], rt[2], rt[3]);
+                TmCopy<D, K + 1, END>::run(rt + 4, dst);
+            }
         }
     }
 };
