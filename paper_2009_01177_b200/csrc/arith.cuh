@@ -475,7 +475,7 @@ TOR_HD_R2 qd qd_rank2_fused(qd s, qd a, qd b, qd c, qd d) {
 }
 // s - a*b, same scheme
 template <bool kNorm>
-TOR_HD_RNI qd qd_rank1_fused(qd s, qd a, qd b) {
+TOR_HD qd qd_rank1_body(const qd& s, const qd& a, const qd& b) {
     double p0, e0, pa, ea, pb, eb, r[3], re[3];
     two_prod(a.x[0], b.x[0], p0, e0);
     two_prod(a.x[0], b.x[1], pa, ea);
@@ -502,7 +502,11 @@ TOR_HD_RNI qd qd_rank1_fused(qd s, qd a, qd b) {
 // a*b by the same order-collected scheme (products have no cancellation: without the
 // final renormalisation the words are still ordered 2^-53k relative to |ab|)
 template <bool kNorm>
-TOR_HD_RNI qd qd_mul_fused(qd a, qd b) {
+TOR_HD_RNI qd qd_rank1_fused(qd s, qd a, qd b) {
+    return qd_rank1_body<kNorm>(s, a, b);
+}
+template <bool kNorm>
+TOR_HD qd qd_mul_body(const qd& a, const qd& b) {
     double p0, e0, pa, ea, pb, eb, r[3], re[3];
     two_prod(a.x[0], b.x[0], p0, e0);
     two_prod(a.x[0], b.x[1], pa, ea);
@@ -521,6 +525,10 @@ TOR_HD_RNI qd qd_mul_fused(qd a, qd b) {
     const double h3 = tree_add(t3);
     if constexpr (kNorm) return qd_renorm5_bf(p0, h1, h2, h3, 0.0);
     else return qd{{p0, h1, h2, h3}};
+}
+template <bool kNorm>
+TOR_HD_RNI qd qd_mul_fused(qd a, qd b) {
+    return qd_mul_body<kNorm>(a, b);
 }
 
 // Schur-state updates skip the final renormalisation (like the lazy DD products): every
@@ -548,7 +556,10 @@ TOR_HD_RNI qd qd_rank1_lazy(qd s, qd a, qd b) { return qd_sub(s, qd_mul(a, b)); 
 // y + y e / 2 with e = 1 - x y^2 by the fused rank-1 (y^2 formed exactly enough from
 // TwoProds of the DD words) and the correction as a DD product (e ~ 2^-104 needs only
 // ~2^-106 relative).  One renormalisation.
-TOR_HD_NI qd qd_rsqrt_fast(qd x) {
+// kInl: the residual's fused rank-1 inline (inside the out-of-line QD pivot / leaf) or as
+// its one out-of-line copy
+template <bool kInl>
+TOR_HD qd qd_rsqrt_body(const qd& x) {
     const dd y = dd_rsqrt(dd_norm(dd{x.x[0], x.x[1]}));
     // y^2 = p + (pe + q) + (qe + ll) + lle, words by order (2^-53k)
     double p, pe, q, qe, ll, lle, m1, m2, n2, n3, n4;
@@ -559,7 +570,10 @@ TOR_HD_NI qd qd_rsqrt_fast(qd x) {
     two_sum(m2, qe, n2, n3);
     two_sum(n2, ll, n2, n4);
     const qd y2{{p, m1, n2, (n3 + n4) + lle}};
-    const qd e = qd_rank1_fused<true>(qd{{1.0, 0.0, 0.0, 0.0}}, x, y2);
+    const qd one{{1.0, 0.0, 0.0, 0.0}};
+    qd e;
+    if constexpr (kInl) e = qd_rank1_body<true>(one, x, y2);
+    else e = qd_rank1_fused<true>(one, x, y2);
     // corr = (y/2) * (e0 + e1), DD product
     double c0, c1;
     two_prod(0.5 * y.hi, e.x[0], c0, c1);
@@ -567,6 +581,7 @@ TOR_HD_NI qd qd_rsqrt_fast(qd x) {
     c1 = fma_(0.5 * y.lo, e.x[0], c1);
     return qd_renorm5_bf(y.hi, y.lo, c0, c1, 0.0);
 }
+TOR_HD_NI qd qd_rsqrt_fast(qd x) { return qd_rsqrt_body<false>(x); }
 // 1/sqrt(x), x > 0: DD seed then one QD Newton step y + y(1 - x y^2)/2.
 TOR_HD_NI qd qd_rsqrt_slow(qd x) {
     const dd ys = dd_rsqrt(dd_norm(dd{x.x[0], x.x[1]}));
@@ -748,8 +763,31 @@ TOR_HD Piv<dd> pivot2<dd>(const dd& s00, const dd& s01, const dd& s11, const dd&
     return p;
 }
 // QD: det by one fused update
+// (one out-of-line body per pivot with its products, determinant and reciprocal square
+// roots inline: one call instead of ~8, and the two rsqrt chains schedule together)
+#ifndef TOR_QD_PIVOT_OOL
+#define TOR_QD_PIVOT_OOL 1
+#endif
+#if TOR_QD_PIVOT_OOL
+TOR_HD_RNI Piv<qd> qd_pivot_ool(qd s00, qd s01, qd s11, qd t) {
+    Piv<qd> p;
+    const qd a = qd_renorm5_bf(s00.x[0], s00.x[1], s00.x[2], s00.x[3], 0.0);
+    p.bad0 = nonpositive(a.x[0]);
+    p.r1 = qd_rsqrt_body<true>(a);
+    const qd det = qd_rank2_body<true>(qd{{0.0, 0.0, 0.0, 0.0}}, qd_neg(a), s11, s01, s01);
+    p.bad1 = nonpositive(det.x[0]);
+    const qd rd = qd_rsqrt_body<true>(det);
+    p.u1 = qd_mul_body<true>(s01, p.r1);
+    p.r2 = qd_mul_body<true>(qd_mul_body<true>(a, p.r1), rd);
+    p.tn = qd_mul_body<true>(t, rd);
+    return p;
+}
+#endif
 template <>
 TOR_HD Piv<qd> pivot2<qd>(const qd& s00, const qd& s01, const qd& s11, const qd& t) {
+#if TOR_QD_PIVOT_OOL
+    return qd_pivot_ool(s00, s01, s11, t);
+#else
     using A = Arith<qd>;
     Piv<qd> p;
     const qd a = A::norm(s00);
@@ -762,6 +800,7 @@ TOR_HD Piv<qd> pivot2<qd>(const qd& s00, const qd& s01, const qd& s11, const qd&
     p.r2 = A::mul(A::mul(a, p.r1), rd);
     p.tn = A::mul(t, rd);
     return p;
+#endif
 }
 // Term factor of a one-mode (leaf) state: t / sqrt(det).
 template <class T>
@@ -772,12 +811,28 @@ TOR_HD T leaf_term(const T& s00, const T& s01, const T& s11, const T& t, bool& b
     bad = nonpositive(A::hi(det));
     return A::mul(t, A::rsqrt(det));
 }
+#if TOR_QD_PIVOT_OOL
+struct QdLeaf {
+    qd v;
+    bool bad;
+};
+TOR_HD_RNI QdLeaf qd_leaf_ool(qd s00, qd s01, qd s11, qd t) {
+    const qd det = qd_rank2_body<true>(qd{{0.0, 0.0, 0.0, 0.0}}, qd_neg(s00), s11, s01, s01);
+    return QdLeaf{qd_mul_body<true>(t, qd_rsqrt_body<true>(det)), nonpositive(det.x[0])};
+}
+#endif
 template <>
 TOR_HD qd leaf_term<qd>(const qd& s00, const qd& s01, const qd& s11, const qd& t, bool& bad) {
+#if TOR_QD_PIVOT_OOL
+    const QdLeaf r = qd_leaf_ool(s00, s01, s11, t);
+    bad = r.bad;
+    return r.v;
+#else
     using A = Arith<qd>;
     const qd det = A::det2(s00, s01, s11);
     bad = nonpositive(det.x[0]);
     return A::mul(t, A::rsqrt(det));
+#endif
 }
 template <>
 TOR_HD dd leaf_term<dd>(const dd& s00, const dd& s01, const dd& s11, const dd& t, bool& bad) {
