@@ -619,6 +619,12 @@ template <> struct Arith<double> {
     TOR_HD static double rank1s(double s, double a, double b) { return fma_(-a, b, s); }
     TOR_HD static double rsqrt(double a) { return rsqrt_d(a); }
     TOR_HD static double unb(double a) { return a; }
+    // pivot-row vector pair: u = s0 r1, w = (s1 - u1 u) r2 (s0, s1 state entries; u, w may alias them)
+    TOR_HD static void vec(double s0, double s1, double r1, double u1, double r2, double& u, double& w) {
+        const double uu = s0 * r1;
+        w = fma_(-u1, uu, s1) * r2;
+        u = uu;
+    }
     TOR_HD static double neg(double a) { return -a; }
     TOR_HD static void words(double a, double* w) { w[0] = a; }
 };
@@ -653,6 +659,11 @@ template <> struct Arith<dd> {
     TOR_HD static dd rank1s(const dd& s, const dd& a, const dd& b) { return dd_rank1_grid(s, a, b); }
     // state entry -> value
     TOR_HD static dd unb(const dd& a) { return dd_unbias(a); }
+    TOR_HD static void vec(const dd& s0, const dd& s1, const dd& r1, const dd& u1, const dd& r2, dd& u, dd& w) {
+        const dd uu = mul(unb(s0), r1);
+        w = mul(rank1s(s1, u1, uu), r2);
+        u = uu;
+    }
 #else
     static constexpr bool kGrid = false;
     TOR_HD static dd rank2(const dd& s, const dd& a, const dd& b, const dd& c, const dd& d) {
@@ -660,6 +671,11 @@ template <> struct Arith<dd> {
     }
     TOR_HD static dd rank1s(const dd& s, const dd& a, const dd& b) { return dd_rank1(s, a, b); }
     TOR_HD static dd unb(const dd& a) { return a; }
+    TOR_HD static void vec(const dd& s0, const dd& s1, const dd& r1, const dd& u1, const dd& r2, dd& u, dd& w) {
+        const dd uu = mul(s0, r1);
+        w = mul(rank1s(s1, u1, uu), r2);
+        u = uu;
+    }
 #endif
     // general (non-state) s - a*b
     TOR_HD static dd rank1(const dd& s, const dd& a, const dd& b) { return dd_rank1(s, a, b); }
@@ -707,6 +723,7 @@ template <> struct Arith<qd> {
         return qd_rank2_fused<true>(qd{{0.0, 0.0, 0.0, 0.0}}, qd_neg(a), c, b, b);
     }
     TOR_HD static qd unb(const qd& a) { return a; }
+    TOR_HD static void vec(const qd& s0, const qd& s1, const qd& r1, const qd& u1, const qd& r2, qd& u, qd& w);
     TOR_HD static qd neg(const qd& a) { return qd_neg(a); }
     TOR_HD static void words(const qd& a, double* w) {
         for (int i = 0; i < 4; ++i) w[i] = a.x[i];
@@ -800,6 +817,25 @@ TOR_HD Piv<qd> pivot2<qd>(const qd& s00, const qd& s01, const qd& s11, const qd&
     p.r2 = A::mul(A::mul(a, p.r1), rd);
     p.tn = A::mul(t, rd);
     return p;
+#endif
+}
+// QD pivot-row vector pair in one out-of-line body (one call instead of three)
+struct QdPair {
+    qd u, w;
+};
+TOR_HD_RNI QdPair qd_vec_ool(qd s0, qd s1, qd r1, qd u1, qd r2) {
+    const qd u = qd_mul_body<true>(s0, r1);
+    return QdPair{u, qd_mul_body<true>(qd_rank1_body<!kQdLazy>(s1, u1, u), r2)};
+}
+TOR_HD void Arith<qd>::vec(const qd& s0, const qd& s1, const qd& r1, const qd& u1, const qd& r2, qd& u, qd& w) {
+#if TOR_QD_PIVOT_OOL
+    const QdPair p = qd_vec_ool(s0, s1, r1, u1, r2);
+    u = p.u;
+    w = p.w;
+#else
+    const qd uu = mul(s0, r1);
+    w = mul(rank1s(s1, u1, uu), r2);
+    u = uu;
 #endif
 }
 // Term factor of a one-mode (leaf) state: t / sqrt(det).

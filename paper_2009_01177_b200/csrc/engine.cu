@@ -236,8 +236,8 @@ __device__ void warp_elim(const T* S, int d, int sr, int q, T* dst, const T& t_i
     }
     const int m = 2 * q;
     for (int j = 2 + lane; j < m; j += 32) {
-        const T uj = A::mul(A::unb(S[tri_ix(d, sr, sr + j)]), r1);
-        const T wj = A::mul(A::rank1s(S[tri_ix(d, sr + 1, sr + j)], u1, uj), r2);
+        T uj, wj;
+        A::vec(S[tri_ix(d, sr, sr + j)], S[tri_ix(d, sr + 1, sr + j)], r1, u1, r2, uj, wj);
         uw[j] = uj;
         uw[m + j] = wj;
     }
@@ -350,9 +350,10 @@ __device__ void dfs_elim(const T* P, int q, T* slot, bool write_slot, T* root, c
     for (int r = 0; r < 2; ++r) {
         const int jv = 2 + lane + 32 * r;
         if (jv < m) {
-            const T uj = A::mul(A::unb(v0[r]), pv.r1);
+            T uj, wj;
+            A::vec(v0[r], v1[r], pv.r1, pv.u1, pv.r2, uj, wj);
             uw[jv] = uj;
-            uw[m + jv] = A::mul(A::rank1s(v1[r], pv.u1, uj), pv.r2);
+            uw[m + jv] = wj;
         }
     }
     __syncwarp();
@@ -545,8 +546,7 @@ __device__ __forceinline__ void elim_reg(const St<T, Q>& S, St<T, Q - 1>& out, c
     T u[M], w[M];
 #pragma unroll
     for (int j = 2; j < M; ++j) {
-        u[j] = A::mul(A::unb(S.e[cix<M>(0, j)]), r1);
-        w[j] = A::mul(A::rank1s(S.e[cix<M>(1, j)], u1, u[j]), r2);
+        A::vec(S.e[cix<M>(0, j)], S.e[cix<M>(1, j)], r1, u1, r2, u[j], w[j]);
     }
 #pragma unroll
     for (int i = 2; i < M; ++i)
@@ -632,8 +632,7 @@ __device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t,
             T u[M], w[M];
 #pragma unroll
             for (int j = 2; j < M; ++j) {
-                u[j] = A::mul(A::unb(S[tri_ix(d, sr, sr + j)]), r1);
-                w[j] = A::mul(A::rank1s(S[tri_ix(d, sr + 1, sr + j)], u1, u[j]), r2);
+                A::vec(S[tri_ix(d, sr, sr + j)], S[tri_ix(d, sr + 1, sr + j)], r1, u1, r2, u[j], w[j]);
             }
 #pragma unroll
             for (int i = 2; i < M; ++i)
@@ -1223,8 +1222,7 @@ template <class T, int E_LVL> struct FanLevel {
             }
 #pragma unroll
             for (int s = 0; s < NVS; ++s) {
-                a[s] = A::mul(A::unb(a[s]), pv.r1);
-                b[s] = A::mul(A::rank1s(b[s], pv.u1, a[s]), pv.r2);
+                A::vec(a[s], b[s], pv.r1, pv.u1, pv.r2, a[s], b[s]);
             }
 #pragma unroll
             for (int s = 0; s < NVS; ++s)
