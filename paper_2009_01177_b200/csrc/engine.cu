@@ -1185,6 +1185,14 @@ constexpr int kItemUnroll = TOR_ITEM_UNROLL;  // fan-out item batches per loop t
 #ifndef TOR_QD_UB
 #define TOR_QD_UB 1
 #endif
+#if TOR_QD_PIVOT_OOL
+// QD fan-out item: s - u_i u_j - w_i w_j with the operands loaded from shared memory here
+__device__ __noinline__ void qd_item_ool(const qd* sm, const qd* uwv, uint32_t w, int m, qd* dst) {
+    const int src = static_cast<int>(w & 0xfffu);
+    const int a = static_cast<int>((w >> 12) & 0x3ffu), b = static_cast<int>(w >> 22);
+    *dst = qd_rank2_body<!kQdLazy>(sm[src], uwv[a], uwv[b], uwv[a + m], uwv[b + m]);
+}
+#endif
 template <class T, int E_LVL> struct FanLevel {
     static constexpr int Q0 = WarpSmem<T>::Q0;
     static constexpr int E = 1 << (E_LVL - 1);
@@ -1275,6 +1283,23 @@ template <class T, int E_LVL> struct FanLevel {
         constexpr int UB = sizeof(T) == sizeof(qd) ? TOR_QD_UB : TOR_UB;  // items per batch (loads before stores)
         const uint32_t* itb = tabs + WarpSmem<T>::item_off(E_LVL) + lane;
         T* out = sm + WarpSmem<T>::lvl_off(E_LVL) + lane;
+#if TOR_QD_PIVOT_OOL && !defined(TOR_QD_ITEM_INLINE)
+        if constexpr (sizeof(T) == sizeof(qd)) {
+            // QD: one out-of-line call per item that loads its operands itself (pointer and
+            // index arguments instead of five QD values)
+#pragma unroll 1
+            for (int s = 0; s < NIT; ++s) {
+                if (s < NIT - 1 || lane + 32 * s < NE) {
+                    constexpr int kAdd = WarpSmem<T>::buf_stride(E_LVL) - tn;
+                    T* dst = out + 32 * s + (kAdd == 0 ? 0 : ((lane + 32 * s) / tn) * kAdd);
+                    qd_item_ool(reinterpret_cast<const qd*>(sm), reinterpret_cast<const qd*>(uwv), itb[32 * s], m,
+                                reinterpret_cast<qd*>(dst));
+                }
+            }
+            __syncwarp();
+            return;
+        }
+#endif
 #pragma unroll(kItemUnroll)
         for (int s0 = 0; s0 < NIT; s0 += UB) {
             T sv[UB], ui[UB], uj[UB], wi[UB], wj[UB];
