@@ -1185,6 +1185,9 @@ constexpr int kItemUnroll = TOR_ITEM_UNROLL;  // fan-out item batches per loop t
 #ifndef TOR_QD_UB
 #define TOR_QD_UB 1
 #endif
+#ifndef TOR_F64_UB
+#define TOR_F64_UB 5
+#endif
 #if TOR_QD_PIVOT_OOL
 // QD fan-out item: s - u_i u_j - w_i w_j with the operands loaded from shared memory here
 __device__ __noinline__ void qd_item_ool(const qd* sm, const qd* uwv, uint32_t w, int m, qd* dst) {
@@ -1280,7 +1283,8 @@ template <class T, int E_LVL> struct FanLevel {
         // trailing updates into the level-e buffers: item it = lane + 32 s (x-major)
         constexpr int NE = E * tn;
         constexpr int NIT = (NE + 31) / 32;
-        constexpr int UB = sizeof(T) == sizeof(qd) ? TOR_QD_UB : TOR_UB;  // items per batch (loads before stores)
+        constexpr int UB = sizeof(T) == sizeof(qd) ? TOR_QD_UB
+                           : (sizeof(T) == sizeof(double) ? TOR_F64_UB : TOR_UB);  // items per batch
         const uint32_t* itb = tabs + WarpSmem<T>::item_off(E_LVL) + lane;
         T* out = sm + WarpSmem<T>::lvl_off(E_LVL) + lane;
 #if TOR_QD_PIVOT_OOL && !defined(TOR_QD_ITEM_INLINE)
