@@ -355,3 +355,15 @@ def test_batch_beyond_grid_y_limit():
         want = singles[i % 8]
         ok, rel = within(words_value(rs[i]["words"]), words_value(want["words"]), want["sum_abs_terms"], "dd")
         assert ok, f"item {i}: {rel:.3g} sum|t|"
+
+
+def test_headline_n32_dd_vs_qd():
+    # the headline Torontonian itself (config 4's input, n = 32, 2^32 subsets): DD against
+    # the GPU's own QD, the full-size check the reference cannot run (2.4e5 s in fixed-128)
+    m = W.load_config_instance(4)
+    dd = T.torontonian(m, "128")
+    q = T.torontonian(m, "256")
+    ok, rel = within(words_value(dd["words"]), words_value(q["words"]), q["sum_abs_terms"], "dd")
+    assert ok, f"DD vs QD {rel:.3g} sum|t|"
+    assert rel < 2.0 ** -100
+    assert abs(float(words_value(dd["words"]) / words_value(q["words"])) - 1.0) < 1e-12
