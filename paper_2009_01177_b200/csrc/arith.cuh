@@ -315,6 +315,24 @@ TOR_HD qd qd_renorm5_bf(double c0, double c1, double c2, double c3, double c4) {
     return qd{{r0, r1, r2, r3}};
 }
 
+// Renormalisation when the leading word dominates (|h0| >= |h1 + h2 + h3|, e.g. an exact
+// leading product): a FastTwoSum for the top pair, TwoSums below.  Exact; the words come out
+// at most their nominal order 2^-53k (a word may be smaller when a lower sum cancels), which
+// is all the order-collected operations that consume them assume.
+#ifndef TOR_QD_LEAD_RENORM
+#define TOR_QD_LEAD_RENORM 1
+#endif
+TOR_HD qd qd_renorm_lead(double h0, double h1, double h2, double h3) {
+#if TOR_QD_LEAD_RENORM
+    double s0, e1, s1, e2, s2, s3;
+    fast_two_sum(h0, h1, s0, e1);
+    two_sum(e1, h2, s1, e2);
+    two_sum(e2, h3, s2, s3);
+    return qd{{s0, s1, s2, s3}};
+#else
+    return qd_renorm5_bf(h0, h1, h2, h3, 0.0);
+#endif
+}
 TOR_HD void three_sum(double& a, double& b, double& c) {
     double t1, t2, t3;
     two_sum(a, b, t1, t2);
@@ -523,7 +541,7 @@ TOR_HD qd qd_mul_body(const qd& a, const qd& b) {
     const double t3[10] = {re[0], re[1], re[2], l3[0], l3[1], l3[2], l3[3], l3[4], l3[5],
                            fma_(a.x[0], b.x[3], fma_(a.x[1], b.x[2], fma_(a.x[2], b.x[1], a.x[3] * b.x[0])))};
     const double h3 = tree_add(t3);
-    if constexpr (kNorm) return qd_renorm5_bf(p0, h1, h2, h3, 0.0);
+    if constexpr (kNorm) return qd_renorm_lead(p0, h1, h2, h3);
     else return qd{{p0, h1, h2, h3}};
 }
 template <bool kNorm>
@@ -579,7 +597,7 @@ TOR_HD qd qd_rsqrt_body(const qd& x) {
     two_prod(0.5 * y.hi, e.x[0], c0, c1);
     c1 = fma_(0.5 * y.hi, e.x[1], c1);
     c1 = fma_(0.5 * y.lo, e.x[0], c1);
-    return qd_renorm5_bf(y.hi, y.lo, c0, c1, 0.0);
+    return qd_renorm_lead(y.hi, y.lo, c0, c1);
 }
 TOR_HD_NI qd qd_rsqrt_fast(qd x) { return qd_rsqrt_body<false>(x); }
 // 1/sqrt(x), x > 0: DD seed then one QD Newton step y + y(1 - x y^2)/2.
