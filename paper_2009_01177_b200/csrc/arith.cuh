@@ -315,17 +315,19 @@ TOR_HD qd qd_renorm5_bf(double c0, double c1, double c2, double c3, double c4) {
     return qd{{r0, r1, r2, r3}};
 }
 
-// Renormalisation when the leading word dominates (|h0| >= |h1 + h2 + h3|, e.g. an exact
-// leading product): a FastTwoSum for the top pair, TwoSums below.  Exact; the words come out
-// at most their nominal order 2^-53k (a word may be smaller when a lower sum cancels), which
-// is all the order-collected operations that consume them assume.
+// One-pass renormalisation of order-collected words h0..h3 (h_k ~ 2^-53k of the operands'
+// scale): a chain of three TwoSums (exact for any ordering -- a lazy state-entry operand may
+// have cancelled its leading word).  The words come out at most their nominal order 2^-53k
+// of that scale, which is all the order-collected operations that consume them assume; the
+// full two-pass renormalisation is kept where a value must be normalised relative to ITSELF
+// (pivots, determinants, the rsqrt residual).
 #ifndef TOR_QD_LEAD_RENORM
 #define TOR_QD_LEAD_RENORM 1
 #endif
 TOR_HD qd qd_renorm_lead(double h0, double h1, double h2, double h3) {
 #if TOR_QD_LEAD_RENORM
     double s0, e1, s1, e2, s2, s3;
-    fast_two_sum(h0, h1, s0, e1);
+    two_sum(h0, h1, s0, e1);
     two_sum(e1, h2, s1, e2);
     two_sum(e2, h3, s2, s3);
     return qd{{s0, s1, s2, s3}};

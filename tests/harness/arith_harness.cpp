@@ -85,3 +85,10 @@ extern "C" void h_qd_acc(const double* t, const int* neg, int n, int flush, doub
     for (int i = 0; i < 4; ++i) o[i] = w[i];
     o[4] = a.abs_sum;
 }
+extern "C" void h_qd_vec(const double* s0, const double* s1, const double* r1, const double* u1,
+                         const double* r2, double* u, double* w) {
+    qd uu, ww;
+    Arith<qd>::vec(Q(s0), Q(s1), Q(r1), Q(u1), Q(r2), uu, ww);
+    put(uu, u);
+    put(ww, w);
+}

@@ -244,3 +244,22 @@ def test_qd_accumulator(lib):
     exact = sum(((-F(t)) if s else F(t) for t, s in zip(terms, negs)), Fraction(0))
     sabs = sum(abs(t[0]) for t in terms)
     assert abs(F(o[0:4]) - exact) <= 2.0 ** -200 * sabs
+
+
+def test_qd_products_of_cancelled_lazy_entries(lib):
+    # a lazy (unrenormalised) state entry whose leading word has cancelled -- words ordered by
+    # absolute scale, the second word larger than the first -- times normalised factors:
+    # the pivot-row vector pair stays exact to the ~2^-200 absolute level
+    rng = random.Random(10)
+    for _ in range(300):
+        small = rng.uniform(-1, 1) * 2.0 ** rng.randint(-70, -45)
+        s0 = D4(small, rng.uniform(-1, 1) * 2.0 ** -50, rng.uniform(-1, 1) * 2.0 ** -103,
+                rng.uniform(-1, 1) * 2.0 ** -156)
+        s1 = D4(*rand_qd(rng, -1.0, 1.0))
+        r1, u1, r2 = (D4(*rand_qd(rng, 0.5, 2.0)) for _ in range(3))
+        u, w = D4(), D4()
+        lib.h_qd_vec(s0, s1, r1, u1, r2, u, w)
+        eu = F(s0) * F(r1)
+        ew = (F(s1) - F(u1) * eu) * F(r2)
+        assert abs(F(u) - eu) <= 2.0 ** -200
+        assert abs(F(w) - ew) <= 2.0 ** -198
