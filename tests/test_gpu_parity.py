@@ -367,3 +367,25 @@ def test_headline_n32_dd_vs_qd():
     assert ok, f"DD vs QD {rel:.3g} sum|t|"
     assert rel < 2.0 ** -100
     assert abs(float(words_value(dd["words"]) / words_value(q["words"])) - 1.0) < 1e-12
+
+
+@pytest.mark.parametrize("prec", ["fp64", "128", "256"])
+def test_plan_resident_repeats(prec):
+    # tor_plan_*: inputs uploaded once, execute() reruns the whole device pipeline; every
+    # rerun gives the same words as the one-shot call, and a sharded plan its shard's words
+    m = W.load_config_instance(2)
+    whole = T.torontonian(m, prec)
+    pl = T.api.Plan(m, prec)
+    try:
+        for _ in range(3):
+            r = pl.execute()
+            assert r["words"] == whole["words"]
+            assert r["kernel_launches"] > 0 and r["device_ms"] > 0
+    finally:
+        pl.close()
+    shard = T.torontonian_shard(m, prec, 1, 4)
+    ps = T.api.Plan(m, prec, 2, 1, 2)
+    try:
+        assert ps.execute()["words"][: len(shard["words"])] == shard["words"][: len(ps.execute()["words"])]
+    finally:
+        ps.close()
