@@ -50,3 +50,18 @@ def test_bench_runs_and_prints_one_line():
     d = json.loads(lines[0])
     _check_line(d, cpu=False)
     assert d["result"]["value"] == pytest.approx(7.40836601865894e-11, rel=1e-12)
+
+
+def test_reference_arm_runs_on_host():
+    # bench.py --impl reference times the reference's own fixed-point engine (oracle/_ref, or
+    # the C restatement when the reference was not built) on the host cores: no GPU involved
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "1", "--cpu-sample-seconds", "1"], capture_output=True, text=True,
+                         timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "subset-terms/s"
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["kind"] in ("reference", "port")
