@@ -1189,11 +1189,19 @@ constexpr int kItemUnroll = TOR_ITEM_UNROLL;  // fan-out item batches per loop t
 #define TOR_F64_UB 5
 #endif
 #if TOR_QD_PIVOT_OOL
-// QD fan-out item: s - u_i u_j - w_i w_j with the operands loaded from shared memory here
-__device__ __noinline__ void qd_item_ool(const qd* sm, const qd* uwv, uint32_t w, int m, qd* dst) {
-    const int src = static_cast<int>(w & 0xfffu);
-    const int a = static_cast<int>((w >> 12) & 0x3ffu), b = static_cast<int>(w >> 22);
-    *dst = qd_rank2_body<!kQdLazy>(sm[src], uwv[a], uwv[b], uwv[a + m], uwv[b + m]);
+// QD fan-out level trailing update: one out-of-line loop over this lane's items
+// it = lane + 32 s (s < nit, it < ne), each s - u_i u_j - w_i w_j with the operands loaded
+// from shared memory inside (one call per level instead of one per item)
+__device__ __noinline__ void qd_items_ool(const qd* sm, const qd* uwv, const uint32_t* itb, qd* out, int nit, int ne,
+                                          int m, int lane) {
+#pragma unroll 1
+    for (int s = 0; s < nit; ++s) {
+        if (lane + 32 * s >= ne) break;
+        const uint32_t w = itb[32 * s];
+        const int src = static_cast<int>(w & 0xfffu);
+        const int a = static_cast<int>((w >> 12) & 0x3ffu), b = static_cast<int>(w >> 22);
+        out[32 * s] = qd_rank2_body<!kQdLazy>(sm[src], uwv[a], uwv[b], uwv[a + m], uwv[b + m]);
+    }
 }
 #endif
 template <class T, int E_LVL> struct FanLevel {
@@ -1289,17 +1297,10 @@ template <class T, int E_LVL> struct FanLevel {
         T* out = sm + WarpSmem<T>::lvl_off(E_LVL) + lane;
 #if TOR_QD_PIVOT_OOL && !defined(TOR_QD_ITEM_INLINE)
         if constexpr (sizeof(T) == sizeof(qd)) {
-            // QD: one out-of-line call per item that loads its operands itself (pointer and
-            // index arguments instead of five QD values)
-#pragma unroll 1
-            for (int s = 0; s < NIT; ++s) {
-                if (s < NIT - 1 || lane + 32 * s < NE) {
-                    constexpr int kAdd = WarpSmem<T>::buf_stride(E_LVL) - tn;
-                    T* dst = out + 32 * s + (kAdd == 0 ? 0 : ((lane + 32 * s) / tn) * kAdd);
-                    qd_item_ool(reinterpret_cast<const qd*>(sm), reinterpret_cast<const qd*>(uwv), itb[32 * s], m,
-                                reinterpret_cast<qd*>(dst));
-                }
-            }
+            // QD: the item loop as one out-of-line call that loads its operands itself
+            static_assert(WarpSmem<T>::buf_stride(E_LVL) == tn, "QD fan-out buffers are unpadded");
+            qd_items_ool(reinterpret_cast<const qd*>(sm), reinterpret_cast<const qd*>(uwv), itb,
+                         reinterpret_cast<qd*>(out), NIT, NE, m, lane);
             __syncwarp();
             return;
         }
