@@ -411,9 +411,6 @@ int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, i
                 throw HostError(TOR_E_INVALID, "torontonian/range", "batch instances must share N");
             if (prec == TOR_PREC_AUTO) {
                 cfgs[i] = select_precision(as[i], as[i].n, 3, 0.5);
-                if (cfgs[i].width_bits != 128)
-                    throw HostError(TOR_E_PRECISION, "precision/batch-width",
-                                    "batch AUTO requires every instance to select 128 bits");
             } else if (prec == TOR_PREC_FP64) {
                 cfgs[i] = PrecCfg{};
                 cfgs[i].width_bits = 64;
@@ -423,10 +420,59 @@ int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, i
         });
         const auto t1 = std::chrono::steady_clock::now();
         EngineStats st;
-        const auto res = run(device, mode, as, WorkRange{}, &st);
+        std::vector<int> modes(count, mode);
+        std::vector<EngineOut> res(count);
+        if (prec != TOR_PREC_AUTO) {
+            res = run(device, mode, as, WorkRange{}, &st);
+        } else {
+            // AUTO per instance, as tor_torontonian: the selected width picks DD or QD (one
+            // sub-batch each), then the posterior check re-runs in QD every DD instance whose
+            // cancellation leaves fewer than b_sgn bits
+            auto run_group = [&](int md, const std::vector<int>& idx) {
+                if (idx.empty()) return;
+                std::vector<Input> sub;
+                sub.reserve(idx.size());
+                for (int i : idx) sub.push_back(as[i]);
+                EngineStats gs;
+                const auto r = run(device, md, sub, WorkRange{}, &gs);
+                st.kernel_ms += gs.kernel_ms;
+                st.total_ms += gs.total_ms;
+                st.launches += gs.launches;
+                st.h2d_bytes += gs.h2d_bytes;
+                st.d2h_bytes += gs.d2h_bytes;
+                for (size_t k = 0; k < idx.size(); ++k) {
+                    res[idx[k]] = r[k];
+                    modes[idx[k]] = md;
+                }
+            };
+            std::vector<int> dd_idx, qd_idx;
+            for (int i = 0; i < count; ++i) (cfgs[i].width_bits == 128 ? dd_idx : qd_idx).push_back(i);
+            run_group(MODE_DD, dd_idx);
+            run_group(MODE_QD, qd_idx);
+            std::vector<int> esc;
+            for (int i : dd_idx) {
+                tor_result tmp;
+                fill_result(as[i], MODE_DD, cfgs[i], res[i], st, 0.0, 1, &tmp);
+                if (tmp.value != 0.0 && tmp.bits_left < cfgs[i].b_sgn) esc.push_back(i);
+            }
+            run_group(MODE_QD, esc);
+            for (int i : esc) {
+                tor_result tmp;
+                fill_result(as[i], MODE_QD, cfgs[i], res[i], st, 0.0, 1, &tmp);
+                if (tmp.bits_left < cfgs[i].b_sgn)
+                    throw HostError(TOR_E_PRECISION, "precision/insufficient",
+                                    "cancellation leaves fewer than b_sgn significant bits");
+            }
+            for (int i : esc) modes[i] = -modes[i] - 1;  // mark escalated (decoded below)
+        }
         const auto t2 = std::chrono::steady_clock::now();
         const double wall = std::chrono::duration<double>(t2 - t0).count();
-        for (int i = 0; i < count; ++i) fill_result(as[i], mode, cfgs[i], res[i], st, wall, 1, &outs[i]);
+        for (int i = 0; i < count; ++i) {
+            const bool escalated = modes[i] < 0;
+            const int md = escalated ? -modes[i] - 1 : modes[i];
+            fill_result(as[i], md, cfgs[i], res[i], st, wall, 1, &outs[i]);
+            outs[i].escalated = escalated ? 1 : 0;
+        }
         if (std::getenv("TOR_DEBUG_TIMING")) {
             auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
             std::fprintf(stderr, "[tor] batch: validate+precision %.2f ms, run %.2f ms, results %.2f ms\n",

@@ -389,3 +389,19 @@ def test_plan_resident_repeats(prec):
         assert ps.execute()["words"][: len(shard["words"])] == shard["words"][: len(ps.execute()["words"])]
     finally:
         ps.close()
+
+
+def test_batch_auto_mixed_widths():
+    # batch AUTO selects the width per instance like tor_torontonian: the near-singular
+    # instance needs 256 bits (QD sub-batch), the others 128 (DD sub-batch)
+    hard = diag_instance(6, [0.5] * 6, [0.5 - 2.0 ** -20] * 6)
+    ms = [W.generate_instance(6, 0.16, 0.06, s) for s in (1, 2)] + [hard] + [W.generate_instance(6, 0.16, 0.06, 3)]
+    rs = T.torontonian_batch(ms, "auto")
+    assert [r["mode"] for r in rs] == ["dd", "dd", "qd", "dd"]
+    for m, r in zip(ms, rs):
+        single = T.torontonian(m, "auto")
+        assert r["mode"] == single["mode"] and r["config"] == single["config"]
+        ok, rel = within(words_value(r["words"]), words_value(single["words"]), single["sum_abs_terms"], r["mode"])
+        assert ok, rel
+    closed = (1.0 / math.sqrt((1 - 0.5) ** 2 - (0.5 - 2.0 ** -20) ** 2) - 1.0) ** 6
+    assert abs(rs[2]["value"] / closed - 1) < 1e-9
