@@ -166,7 +166,9 @@ int tor_torontonian(const tor_input* in, tor_precision prec, const int* devices,
  * on the device by the same engine in fp64. */
 int tor_torontonian_reference(const tor_input* in, double* value, tor_error* err);
 
-/* `count` instances of equal N in one device pass (BASELINE config 3). */
+/* `count` instances of equal N in one device pass (BASELINE config 3).  AUTO selects the
+ * width per instance exactly as tor_torontonian (DD and QD sub-batches) including the
+ * posterior escalation; validation errors report the first bad instance in index order. */
 int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, int device,
                           tor_result* outs, tor_error* err);
 
