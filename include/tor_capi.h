@@ -192,6 +192,10 @@ int tor_fold_partials(const tor_partial* parts, int count, const tor_input* in, 
 /* p(S) = Tor(A_S) sqrt(det(I - A)) (torontonian.cpp:202-209); pattern bit k = mode k. */
 int tor_probability(const tor_input* full, uint64_t pattern_bits, tor_precision prec, int device,
                     double* p, tor_error* err);
+/* The same with the click pattern as an ascending list of mode indices: no 64-mode limit on
+ * the full state (the reference's ClickPattern is one u64, matrix_io.hpp:29-34). */
+int tor_probability_modes(const tor_input* full, const int* modes, int nmodes, tor_precision prec, int device,
+                          double* p, tor_error* err);
 
 /* Prepared evaluation with device-resident inputs (the exact R is uploaded once):
  * create -> execute (repeatable; runs the whole device pipeline and reads back the

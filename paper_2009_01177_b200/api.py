@@ -62,7 +62,7 @@ class TorPartial(C.Structure):
 EXPORTS = ("tor_abi_version", "tor_check_symmetries", "tor_check_dense", "tor_det_i_minus_a",
            "tor_select_precision", "tor_force_width", "tor_torontonian", "tor_torontonian_reference",
            "tor_torontonian_batch", "tor_torontonian_slice", "tor_torontonian_shard", "tor_fold_partials",
-           "tor_probability", "tor_device_count", "tor_plan_create", "tor_plan_execute", "tor_plan_destroy",
+           "tor_probability", "tor_probability_modes", "tor_device_count", "tor_plan_create", "tor_plan_execute", "tor_plan_destroy",
            "tor_release_device_cache")
 
 _lib = None
@@ -92,6 +92,8 @@ def lib():
         L.tor_check_dense.argtypes = [C.c_int, P(C.c_double), P(C.c_double), P(C.c_int), P(TorError)]
         L.tor_det_i_minus_a.argtypes = [P(TorInput), P(C.c_double), P(TorError)]
         L.tor_probability.argtypes = [P(TorInput), C.c_uint64, C.c_int, C.c_int, P(C.c_double), P(TorError)]
+        L.tor_probability_modes.argtypes = [P(TorInput), P(C.c_int), C.c_int, C.c_int, C.c_int, P(C.c_double),
+                                            P(TorError)]
         L.tor_plan_create.argtypes = [P(TorInput), C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int,
                                       P(C.c_void_p), P(TorError)]
         L.tor_plan_execute.argtypes = [C.c_void_p, P(TorResult), P(TorError)]
@@ -290,14 +292,22 @@ def det_i_minus_a(matrix: InputMatrix) -> float:
     return v.value
 
 
-def probability(matrix: InputMatrix, pattern_bits: int, workers: int = 0, precision="auto",
+def probability(matrix: InputMatrix, pattern_bits, workers: int = 0, precision="auto",
                 device: int = 0) -> float:
-    """p(S) = Tor(A_S) sqrt(det(I - A)) (torontonian.cpp:202-209); bit k = mode k."""
+    """p(S) = Tor(A_S) sqrt(det(I - A)) (torontonian.cpp:202-209).  pattern_bits: an int
+    (bit k = mode k, the reference's ClickPattern) or a sequence of mode indices (no 64-mode
+    limit: tor_probability_modes)."""
     inp = _In(matrix)
     v = C.c_double()
     err = TorError()
-    _check(lib().tor_probability(C.byref(inp.s), pattern_bits, _prec(precision), device, C.byref(v),
-                                 C.byref(err)), err)
+    if isinstance(pattern_bits, (int, np.integer)):
+        _check(lib().tor_probability(C.byref(inp.s), int(pattern_bits), _prec(precision), device, C.byref(v),
+                                     C.byref(err)), err)
+    else:
+        modes = sorted(int(k) for k in pattern_bits)
+        arr = (C.c_int * max(len(modes), 1))(*modes)
+        _check(lib().tor_probability_modes(C.byref(inp.s), arr, len(modes), _prec(precision), device, C.byref(v),
+                                           C.byref(err)), err)
     return v.value
 
 

@@ -623,32 +623,51 @@ int tor_plan_execute(tor_plan* plan, tor_result* out, tor_error* err) {
 
 void tor_plan_destroy(tor_plan* plan) { delete plan; }
 
+namespace {
+int probability_of(const tor_input* full, const std::vector<int>* modes, uint64_t pattern_bits,
+                   tor_precision prec, int device, double* p, tor_error* err) {
+    if (!full || full->n < 1) throw HostError(TOR_E_INVALID, "matrixio/dim", "matrix has no modes");
+    const Input a = make_input(full->n, full->a00_upper, full->a01_upper);
+    const double det = det_i_minus_a_float(a);  // torontonian.cpp:203
+    if (!(det > 0.0)) throw HostError(TOR_E_ERROR, "torontonian/invalid-state", "det(I - A) must be positive");
+    if (modes ? modes->empty() : pattern_bits == 0) {
+        *p = std::sqrt(det);
+        return TOR_OK;
+    }
+    const Input sub = modes ? extract_modes(a, *modes) : extract_submatrix(a, pattern_bits);
+    std::vector<double> w00(sub.a00.size() * 2), w01(sub.a01.size() * 2);
+    for (size_t i = 0; i < sub.a00.size(); ++i) {
+        w00[2 * i] = sub.a00[i].real();
+        w00[2 * i + 1] = sub.a00[i].imag();
+        w01[2 * i] = sub.a01[i].real();
+        w01[2 * i + 1] = sub.a01[i].imag();
+    }
+    const tor_input si{sub.n, w00.data(), w01.data()};
+    tor_result r;
+    const int st = tor_torontonian(&si, prec, &device, 1, &r, err);
+    if (st) return st;
+    *p = r.value * std::sqrt(det);
+    return TOR_OK;
+}
+}  // namespace
+
 int tor_probability(const tor_input* full, uint64_t pattern_bits, tor_precision prec, int device, double* p,
                     tor_error* err) {
     try {
         clear_err(err);
-        if (!full || full->n < 1) throw HostError(TOR_E_INVALID, "matrixio/dim", "matrix has no modes");
-        const Input a = make_input(full->n, full->a00_upper, full->a01_upper);
-        const double det = det_i_minus_a_float(a);  // torontonian.cpp:203
-        if (!(det > 0.0)) throw HostError(TOR_E_ERROR, "torontonian/invalid-state", "det(I - A) must be positive");
-        if (pattern_bits == 0) {
-            *p = std::sqrt(det);
-            return TOR_OK;
-        }
-        const Input sub = extract_submatrix(a, pattern_bits);
-        std::vector<double> w00(sub.a00.size() * 2), w01(sub.a01.size() * 2);
-        for (size_t i = 0; i < sub.a00.size(); ++i) {
-            w00[2 * i] = sub.a00[i].real();
-            w00[2 * i + 1] = sub.a00[i].imag();
-            w01[2 * i] = sub.a01[i].real();
-            w01[2 * i + 1] = sub.a01[i].imag();
-        }
-        const tor_input si{sub.n, w00.data(), w01.data()};
-        tor_result r;
-        const int st = tor_torontonian(&si, prec, &device, 1, &r, err);
-        if (st) return st;
-        *p = r.value * std::sqrt(det);
-        return TOR_OK;
+        return probability_of(full, nullptr, pattern_bits, prec, device, p, err);
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+int tor_probability_modes(const tor_input* full, const int* modes, int nmodes, tor_precision prec, int device,
+                          double* p, tor_error* err) {
+    try {
+        clear_err(err);
+        if (nmodes < 0 || (nmodes > 0 && !modes)) throw HostError(TOR_E_INVALID, "matrixio/pattern", "bad mode list");
+        const std::vector<int> sel(modes, modes + nmodes);
+        return probability_of(full, &sel, 0, prec, device, p, err);
     } catch (const HostError& h) {
         return fail(err, h);
     }

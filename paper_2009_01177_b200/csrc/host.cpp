@@ -292,11 +292,20 @@ void op_counts(int n, uint64_t& mults, uint64_t& adds, uint64_t& recips, uint64_
 
 Input extract_submatrix(const Input& full, uint64_t bits) {  // matrix_io.cpp:360-382
     std::vector<int> sel;
-    for (int k = 0; k < full.n; ++k)
+    for (int k = 0; k < full.n && k < 64; ++k)
         if (bits >> k & 1) sel.push_back(k);
     if (full.n < 64 && (bits >> full.n) != 0)
         throw HostError(TOR_E_INVALID, "matrixio/dim", "pattern mode count mismatch");
+    return extract_modes(full, sel);
+}
+
+// Submatrix on an explicit ascending mode list: no 64-mode limit on the full state (the
+// reference's ClickPattern is one u64, matrix_io.hpp:29-34).
+Input extract_modes(const Input& full, const std::vector<int>& sel) {
     if (sel.empty()) throw HostError(TOR_E_INVALID, "matrixio/pattern", "empty click pattern");
+    for (size_t k = 0; k < sel.size(); ++k)
+        if (sel[k] < 0 || sel[k] >= full.n || (k > 0 && sel[k] <= sel[k - 1]))
+            throw HostError(TOR_E_INVALID, "matrixio/pattern", "modes must be ascending and within the state");
     Input out;
     out.n = static_cast<int>(sel.size());
     const size_t t = static_cast<size_t>(out.n) * (out.n + 1) / 2;

@@ -57,5 +57,6 @@ void op_counts(int n, uint64_t& mults, uint64_t& adds, uint64_t& recips, uint64_
 unsigned __int128 total_op_count(int n);
 
 Input extract_submatrix(const Input& full, uint64_t pattern_bits);
+Input extract_modes(const Input& full, const std::vector<int>& ascending_modes);
 
 }  // namespace tor

@@ -405,3 +405,19 @@ def test_batch_auto_mixed_widths():
         assert ok, rel
     closed = (1.0 / math.sqrt((1 - 0.5) ** 2 - (0.5 - 2.0 ** -20) ** 2) - 1.0) ** 6
     assert abs(rs[2]["value"] / closed - 1) < 1e-9
+
+
+def test_probability_beyond_64_modes():
+    # p(S) on config 3's m = 100 state (the reference's u64 ClickPattern cannot address it):
+    # the mode-list entry point equals Tor(O_S) sqrt(det(I - O)) of the extracted instance,
+    # and on config 2's m = 50 state the mode list and the bit pattern agree exactly
+    st3 = W.full_state(3)
+    sel = W.click_set(3, 0)
+    p = T.probability(st3, sel, precision="128")
+    want = T.torontonian(W.instance(3, 0, st3), "128")["value"] * math.sqrt(T.det_i_minus_a(st3))
+    assert p == pytest.approx(want, rel=1e-12)
+    st2 = W.full_state(2)
+    sel2 = W.click_set(2)
+    assert T.probability(st2, sel2, precision="128") == T.probability(st2, W.pattern_bits(sel2), precision="128")
+    with pytest.raises(T.InvalidArgument):
+        T.probability(st3, [3, 200], precision="128")  # mode outside the state
