@@ -158,7 +158,10 @@ int tor_select_precision(const tor_input* in, int N, int sig_decimal_digits, dou
 int tor_force_width(const tor_input* in, int width_bits, tor_precision_config* out, tor_error* err);
 
 /* Full evaluation (validation N in [1,40], symmetry gate, precision selection,
- * adaptive escalation, device evaluation).  devices == NULL / ndev <= 0: device 0. */
+ * adaptive escalation, device evaluation).  devices == NULL / ndev <= 0: device 0.  With
+ * ndev > 1 the prefix classes split into P = 2^k aligned shards (P = the largest power of
+ * two <= ndev), one host thread per listed device, folded along the fixed tree:
+ * bit-identical to one device; out->devices = P (the reference's `workers` fan-out). */
 int tor_torontonian(const tor_input* in, tor_precision prec, const int* devices, int ndev,
                     tor_result* out, tor_error* err);
 

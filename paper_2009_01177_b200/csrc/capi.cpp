@@ -42,6 +42,25 @@ void clear_err(tor_error* e) {
     if (e) set_err(e, "", "");
 }
 
+// One host thread per index (a thread per device); the first failure in index order is
+// rethrown.
+template <class F>
+void parallel_for_n(int n, F f) {
+    std::vector<std::exception_ptr> errs(n);
+    std::vector<std::thread> th;
+    for (int t = 0; t < n; ++t)
+        th.emplace_back([&, t] {
+            try {
+                f(t);
+            } catch (...) {
+                errs[t] = std::current_exception();
+            }
+        });
+    for (auto& x : th) x.join();
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+}
+
 // Host-side preparation of many instances (validation, precision bounds, exact R) in
 // parallel chunks; the first failure in index order is rethrown (deterministic).
 template <class F>
@@ -172,6 +191,50 @@ void fill_result(const Input& a, int mode, const PrecCfg& cfg, const EngineOut& 
     r->kernel_launches = st.launches;
     r->h2d_bytes = st.h2d_bytes;
     r->d2h_bytes = st.d2h_bytes;
+}
+
+// One Torontonian on several devices of this process: the prefix classes are split into
+// P = 2^k aligned shards (P = the largest power of two <= the device count), one host thread
+// per device, and the shard partials fold along the engine's fixed tree -- bit-identical to
+// a single-device run (the reference's `workers` fan-out, torontonian.cpp:112-147).
+EngineOut run_devices(const std::vector<int>& devs, int mode, const Input& a, EngineStats* stats, int* used) {
+    int P = 1;
+    while (2 * P <= static_cast<int>(devs.size())) P *= 2;
+    if (used) *used = P;
+    if (P == 1) return run(devs[0], mode, {a}, WorkRange{}, stats)[0];
+    int k = 0;
+    while ((1 << k) < P) ++k;
+    std::vector<EngineOut> parts(P);
+    std::vector<EngineStats> sts(P);
+    parallel_for_n(P, [&](int r) {
+        WorkRange wr;
+        wr.class_bits = k;
+        wr.class_lo = static_cast<uint64_t>(r);
+        wr.class_hi = static_cast<uint64_t>(r) + 1;
+        parts[r] = run(devs[r], mode, {a}, wr, &sts[r])[0];
+    });
+    std::vector<double> buf(static_cast<size_t>(P) * 5);
+    EngineOut o;
+    for (int r = 0; r < P; ++r) {
+        for (int x = 0; x < 4; ++x) buf[r * 5 + x] = parts[r].words[x];
+        buf[r * 5 + 4] = parts[r].sum_abs;
+        o.terms += parts[r].terms;
+    }
+    double w5[5];
+    fold_words(mode, buf.data(), P, w5);
+    for (int x = 0; x < 4; ++x) o.words[x] = w5[x];
+    o.sum_abs = w5[4];
+    if (stats) {
+        *stats = EngineStats{};
+        for (const auto& t : sts) {  // the slowest device bounds the call
+            stats->kernel_ms = std::max(stats->kernel_ms, t.kernel_ms);
+            stats->total_ms = std::max(stats->total_ms, t.total_ms);
+            stats->launches += t.launches;
+            stats->h2d_bytes += t.h2d_bytes;
+            stats->d2h_bytes += t.d2h_bytes;
+        }
+    }
+    return o;
 }
 
 // Exact fixed-point validation mode: the reference's algorithm on the GPU (fixed.cu).
@@ -333,7 +396,10 @@ int tor_torontonian(const tor_input* in, tor_precision prec, const int* devices,
         const Input a = checked_input(in, 40);
         if (prec < TOR_PREC_AUTO || prec > TOR_PREC_FIXED256)
             throw HostError(TOR_E_INVALID, "precision/range", "unknown precision mode");
-        const int dev = (devices && ndev > 0) ? devices[0] : 0;
+        std::vector<int> devs;
+        if (devices && ndev > 0) devs.assign(devices, devices + ndev);
+        else devs.push_back(0);
+        const int dev = devs[0];
         if (prec == TOR_PREC_FIXED128 || prec == TOR_PREC_FIXED256) {
             fixed_mode(a, prec == TOR_PREC_FIXED128 ? 128 : 256, dev, out);
             out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -353,7 +419,8 @@ int tor_torontonian(const tor_input* in, tor_precision prec, const int* devices,
             mode = mode_of(prec);
         }
         EngineStats st;
-        auto res = run(dev, mode, {a}, WorkRange{}, &st);
+        int used = 1;
+        std::vector<EngineOut> res{run_devices(devs, mode, a, &st, &used)};
         int escalated = 0;
         if (prec == TOR_PREC_AUTO) {
             // posterior check: keep >= b_sgn significant bits after cancellation
@@ -363,7 +430,7 @@ int tor_torontonian(const tor_input* in, tor_precision prec, const int* devices,
                 if (mode == MODE_DD) {
                     mode = MODE_QD;
                     escalated = 1;
-                    res = run(dev, mode, {a}, WorkRange{}, &st);
+                    res = {run_devices(devs, mode, a, &st, &used)};
                     fill_result(a, mode, cfg, res[0], st, 0.0, 1, &tmp);
                 }
                 if (tmp.bits_left < cfg.b_sgn)
@@ -372,7 +439,7 @@ int tor_torontonian(const tor_input* in, tor_precision prec, const int* devices,
             }
         }
         const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        fill_result(a, mode, cfg, res[0], st, wall, 1, out);
+        fill_result(a, mode, cfg, res[0], st, wall, used, out);
         out->escalated = escalated;
         return TOR_OK;
     } catch (const HostError& h) {

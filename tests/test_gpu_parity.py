@@ -421,3 +421,17 @@ def test_probability_beyond_64_modes():
     assert T.probability(st2, sel2, precision="128") == T.probability(st2, W.pattern_bits(sel2), precision="128")
     with pytest.raises(T.InvalidArgument):
         T.probability(st3, [3, 200], precision="128")  # mode outside the state
+
+
+@pytest.mark.parametrize("prec", ["128", "256", "fp64"])
+def test_device_list_folds_bit_identical(prec):
+    # tor_torontonian with a device list (the reference's `workers`): 2^k prefix-class shards,
+    # one host thread per device, folded along the fixed tree -- bit-identical to one device.
+    # (On a one-GPU box the list repeats device 0: the shards run concurrently there.)
+    m = W.load_config_instance(2)
+    one = T.torontonian(m, prec)
+    for devs in ([0, 0], [0, 0, 0, 0], [0, 0, 0]):
+        r = T.torontonian(m, prec, devices=devs)
+        assert r["words"] == one["words"], devs
+        assert r["sum_abs_terms"] == one["sum_abs_terms"]
+        assert r["devices"] == (2 if len(devs) == 3 else len(devs))
