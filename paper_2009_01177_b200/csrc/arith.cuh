@@ -940,6 +940,9 @@ template <> struct Acc<double> {
     }
 };
 
+#ifndef TOR_ACC_NOBR
+#define TOR_ACC_NOBR 0
+#endif
 template <> struct Acc<dd> {
     // running sum s (accurate DD) + a lazily renormalised block (h, c): per term one
     // TwoSum on the leading words and one plain add for the low words; the block is
@@ -950,11 +953,19 @@ template <> struct Acc<dd> {
     double abs_sum = 0.0;
     int sc = 0;
     TOR_HD void add(dd t, bool negative, int z) {
+#if TOR_ACC_NOBR
+        {  // branch-free: pow2i(0) = 1 exactly
+            const double f = pow2i(-sc * z);
+            t.hi *= f;
+            t.lo *= f;
+        }
+#else
         if (sc) {
             const double f = pow2i(-sc * z);
             t.hi *= f;
             t.lo *= f;
         }
+#endif
         const double th = negative ? -t.hi : t.hi;
         const double tl = negative ? -t.lo : t.lo;
         double nh, e;

@@ -166,6 +166,22 @@ __device__ __forceinline__ void report_breakdown(unsigned long long* err, uint64
     // smallest failing mask wins (deterministic); row in the low byte
     atomicMin(err, (static_cast<unsigned long long>(mask) << 8) | static_cast<unsigned long long>(row & 0xff));
 }
+// Per-thread breakdown sink of the lane-level code: the same min key kept in a register
+// and published once per warp lifetime (flush), so the pivot checks are selects instead
+// of branches around an atomic (no basic-block split between consecutive pivot chains).
+#ifndef TOR_BAD_DEFER
+#define TOR_BAD_DEFER 1
+#endif
+struct LocalErr {
+    unsigned long long v = ~0ull;
+    __device__ __forceinline__ void flush(unsigned long long* err) const {
+        if (v != ~0ull) atomicMin(err, v);
+    }
+};
+__device__ __forceinline__ void report_breakdown(LocalErr* err, uint64_t mask, int row) {
+    const unsigned long long key = (static_cast<unsigned long long>(mask) << 8) | static_cast<unsigned long long>(row & 0xff);
+    err->v = key < err->v ? key : err->v;
+}
 
 template <class T> __device__ __forceinline__ T shfl_xor_t(const T& v, int m);
 template <> __device__ __forceinline__ double shfl_xor_t<double>(const double& v, int m) {
@@ -534,9 +550,9 @@ template <class T, int Q> struct St {
 template <int D> __device__ __forceinline__ constexpr int cix(int i, int j) { return i * D - (i * (i + 1)) / 2 + j; }
 
 // Eliminate mode 0 of a Q-mode register state into a (Q-1)-mode state.
-template <class T, int Q>
+template <class T, int Q, class E>
 __device__ __forceinline__ void elim_reg(const St<T, Q>& S, St<T, Q - 1>& out, const T& t, T& tout, uint64_t mask,
-                                         int nsel, unsigned long long* err) {
+                                         int nsel, E* err) {
     using A = Arith<T>;
     constexpr int M = 2 * Q;
     const Piv<T> pv = piv_lt<T>(S.e[cix<M>(0, 0)], S.e[cix<M>(0, 1)], S.e[cix<M>(1, 1)], t);
@@ -570,8 +586,9 @@ constexpr int kLoopQ = TOR_LOOPQ;
 constexpr int kLoopQQd = TOR_QD_LOOPQ;
 
 template <class T, int Q> struct SubReg {
+    template <class E>
     __device__ __forceinline__ static void branch(const St<T, Q>& S, int br, const T& t, bool neg, uint64_t mask,
-                                                  int nsel, Acc<T>& acc, unsigned long long* err) {
+                                                  int nsel, Acc<T>& acc, E* err) {
         constexpr int M = 2 * Q;
         const uint64_t bit = 1ull << (Q - 1);
         St<T, Q - 1> Sn;
@@ -589,8 +606,9 @@ template <class T, int Q> struct SubReg {
         SubReg<T, Q - 1>::run(Sn, tn, br == 0 ? !neg : neg, br == 0 ? (mask | bit) : mask, nsel + (br == 0),
                               acc, err);
     }
+    template <class E>
     __device__ __forceinline__ static void run(const St<T, Q>& S, const T& t, bool neg, uint64_t mask, int nsel,
-                                               Acc<T>& acc, unsigned long long* err) {
+                                               Acc<T>& acc, E* err) {
         if constexpr (Q >= (sizeof(T) == sizeof(qd) ? kLoopQQd : kLoopQ)) {
 #pragma unroll 1
             for (int br = 0; br < 2; ++br) branch(S, br, t, neg, mask, nsel, acc, err);
@@ -601,11 +619,14 @@ template <class T, int Q> struct SubReg {
     }
 };
 template <class T> struct SubReg<T, 1> {
+    template <class E>
     __device__ __forceinline__ static void run(const St<T, 1>& S, const T& t, bool neg, uint64_t mask, int nsel,
-                                               Acc<T>& acc, unsigned long long* err) {
+                                               Acc<T>& acc, E* err) {
         bool bad;
         const T tn = leaf_term<T>(S.e[0], S.e[1], S.e[2], t, bad);
-        if (bad) report_breakdown(err, mask | 1ull, 2 * nsel + 1);
+        // both pivots of the last mode: a negative-definite 2x2 block has det > 0
+        const bool bad0 = nonpositive(Arith<T>::hi(Arith<T>::unb(S.e[0])));
+        if (bad || bad0) report_breakdown(err, mask | 1ull, 2 * nsel + (bad0 ? 0 : 1));
         acc.add(tn, !neg, nsel + 1);
     }
 };
@@ -613,9 +634,9 @@ template <class T> struct SubReg<T, 1> {
 // Lane subtree rooted at an L-mode view in shared memory: emits the node's own
 // term and all 2^L - 1 extensions.  Branch 0 includes the first view mode (its
 // elimination reads shared memory), branch 1 excludes it (loads the trailing block).
-template <class T, int L>
+template <class T, int L, class E>
 __device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t, bool neg, uint64_t mask, int nsel,
-                                          Acc<T>& acc, unsigned long long* err) {
+                                          Acc<T>& acc, E* err) {
     using A = Arith<T>;
     constexpr int M = 2 * L;
     acc.add(t, neg, nsel);
@@ -818,9 +839,9 @@ __device__ __forceinline__ void lt_wave(uint32_t row, const T (&u)[M], const T (
 // Lane subtree whose L-mode root state sits in this lane's TMEM row (entry k of the
 // packed 2L-row triangle at columns tm_col(k)..+3, DD words).  Same arithmetic as
 // lane_tree; only the source of the root entries differs.
-template <class T, int L>
+template <class T, int L, class E>
 __device__ __forceinline__ void lane_tree_tmem(uint32_t row, const T& t, bool neg, uint64_t mask, int nsel,
-                                               Acc<T>& acc, unsigned long long* err) {
+                                               Acc<T>& acc, E* err) {
     using A = Arith<T>;
     constexpr int M = 2 * L;
     constexpr int K01 = 2 * M - 1;  // entries of rows 0 and 1
@@ -928,9 +949,14 @@ template <int D, int K, int END> struct TmCopy {
         }
     }
 };
-template <class T, int L>
+// kPre: the include branch's pivot was computed by the parent (pre), overlapping the
+// parent's trailing update instead of starting after it.
+#ifndef TOR_PIV_AHEAD
+#define TOR_PIV_AHEAD 0
+#endif
+template <class T, int L, class E, bool kPre = false>
 __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t, bool neg, uint64_t mask, int nsel,
-                                         Acc<T>& acc, unsigned long long* err) {
+                                         Acc<T>& acc, E* err, const Piv<T>* pre = nullptr) {
     using A = Arith<T>;
     constexpr int M = 2 * L;
     constexpr int K01 = 2 * M - 1;  // entries of rows 0 and 1
@@ -940,6 +966,7 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
     for (int br = 0; br < 2; ++br) {
         T tn;
         if constexpr (L >= 4) {
+            Piv<T> cpiv;
             if (br == 0) {
                 uint32_t r0[4 * K01];
                 tm_ld_entries<M, 0, K01>(row, r0);
@@ -962,6 +989,18 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
                     tm_ld_entries<M, K01, H>(row, rt);
                     tm_wait_ld();
                     LtUpdTm<T, M, 0, H>::run(rt, u, w, scr);
+#if TOR_PIV_AHEAD
+                    if constexpr (L == 4) {
+                        // the child's pivot entries (0,0), (0,1), (1,1) = trailing entries 0, 1, M-2
+                        static_assert(M - 2 < H, "child pivot entries in the first wave");
+                        const T c00 = A::rank2(u32_to_dd(rt[0], rt[1], rt[2], rt[3]), u[2], u[2], w[2], w[2]);
+                        const T c01 = A::rank2(u32_to_dd(rt[4], rt[5], rt[6], rt[7]), u[2], u[3], w[2], w[3]);
+                        const T c11 = A::rank2(u32_to_dd(rt[4 * (M - 2)], rt[4 * (M - 2) + 1], rt[4 * (M - 2) + 2],
+                                                         rt[4 * (M - 2) + 3]),
+                                               u[3], u[3], w[3], w[3]);
+                        cpiv = piv_lt<T>(c00, c01, c11, tn);
+                    }
+#endif
                 }
                 {
                     uint32_t rt[4 * H];
@@ -983,6 +1022,14 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
                     tm_ld_entries<M, K01, H>(row, rt);
                     tm_wait_ld();
                     TmCopy<M, 0, H>::run(rt, scr);
+#if TOR_PIV_AHEAD
+                    if constexpr (L == 4) {
+                        cpiv = piv_lt<T>(u32_to_dd(rt[0], rt[1], rt[2], rt[3]), u32_to_dd(rt[4], rt[5], rt[6], rt[7]),
+                                         u32_to_dd(rt[4 * (M - 2)], rt[4 * (M - 2) + 1], rt[4 * (M - 2) + 2],
+                                                   rt[4 * (M - 2) + 3]),
+                                         t);
+                    }
+#endif
                 }
                 {
                     uint32_t rt[4 * (NT - H)];
@@ -993,8 +1040,9 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
                 tn = t;
             }
             tm_wait_st();
-            tmem_ext<T, L - 1>(scr, scr, tn, br == 0 ? !neg : neg, br == 0 ? (mask | bit) : mask, nsel + (br == 0),
-                               acc, err);
+            tmem_ext<T, L - 1, E, TOR_PIV_AHEAD && L == 4>(scr, scr, tn, br == 0 ? !neg : neg,
+                                                             br == 0 ? (mask | bit) : mask, nsel + (br == 0), acc,
+                                                             err, &cpiv);
         } else {
             St<T, L - 1> Sn;
             if (br == 0) {
@@ -1004,7 +1052,9 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
                 T e0[K01];
 #pragma unroll
                 for (int k = 0; k < K01; ++k) e0[k] = u32_to_dd(r0[4 * k], r0[4 * k + 1], r0[4 * k + 2], r0[4 * k + 3]);
-                const Piv<T> pv = piv_lt<T>(e0[0], e0[1], e0[M], t);
+                Piv<T> pv;
+                if constexpr (kPre) pv = *pre;
+                else pv = piv_lt<T>(e0[0], e0[1], e0[M], t);
                 if (pv.bad0 || pv.bad1) report_breakdown(err, mask | bit, 2 * nsel + (pv.bad0 ? 0 : 1));
                 tn = pv.tn;
                 T u[M], w[M];
@@ -1212,8 +1262,9 @@ template <class T, int E_LVL> struct FanLevel {
     static constexpr int m = 2 * q;
     static constexpr int dn = m - 2;
     static constexpr int tn = tri_sz(dn);
+    template <class ErrSink>
     __device__ __forceinline__ static void run(T* sm, T* tvals, T* uwv, const uint32_t* tabs, uint64_t leaf_mask,
-                                               int leaf_sel, unsigned long long* err, uint32_t tm_row) {
+                                               int leaf_sel, ErrSink* err, uint32_t tm_row) {
         using A = Arith<T>;
         const int lane = threadIdx.x & 31;
         const int x = (Cfg<T>::TMEM && E_LVL == FAN) ? l5_map(kL5VecMap, lane & (E - 1)) : lane & (E - 1);
@@ -1595,15 +1646,21 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
             T* cuw = csm + SM::kUwOff;
             Acc<T> acc;
             acc.sc = tsc;
+#if TOR_BAD_DEFER
+            LocalErr lerr;
+            LocalErr* cerr = &lerr;
+#else
+            unsigned long long* cerr = err;
+#endif
             for (uint32_t k = 0;; ++k) {
                 mb_wait(c, k & 1);
                 const unsigned long long leaf_mask = meta[c].mask;
                 const unsigned long long job = meta[c].job;
                 const int leaf_sel = meta[c].sel, flags = meta[c].flags;
                 if (flags & 2) break;
-                if constexpr (kConsFirst <= 3) FanLevel<T, 3>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
-                FanLevel<T, 4>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
-                FanLevel<T, FAN>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
+                if constexpr (kConsFirst <= 3) FanLevel<T, 3>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, cerr, crow);
+                FanLevel<T, 4>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, cerr, crow);
+                FanLevel<T, FAN>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, cerr, crow);
                 const int node = l5_lane_node(lane);  // the level-5 node in this lane's TMEM row
                 const T vt = ctv[node_ref<T>(tabs, FAN, node).tix];
                 __syncwarp();
@@ -1612,7 +1669,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 const int lsel = leaf_sel + __popc(node);
                 const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
                 acc.add(vt, nodeneg, lsel);
-                tmem_ext<T, L>(crow, crow + 4 * tri_sz(2 * L), vt, nodeneg, lmask, lsel, acc, err);
+                tmem_ext<T, L>(crow, crow + 4 * tri_sz(2 * L), vt, nodeneg, lmask, lsel, acc, cerr);
                 acc.flush();
                 if (flags & 1) {
                     write_partial(acc, job);
@@ -1620,6 +1677,9 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                     acc.sc = tsc;
                 }
             }
+#if TOR_BAD_DEFER
+            lerr.flush(err);
+#endif
         }
     } else if constexpr (Cfg<T>::WS) {
         // ---- warp-specialised: producer warp p (0-3) runs the DFS and fan-out levels

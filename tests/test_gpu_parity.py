@@ -227,6 +227,48 @@ def test_indefinite_breakdown_reports_mask():
         T.torontonian(m, "128")
 
 
+@pytest.mark.parametrize("prec", ["fp64", "128", "256"])
+def test_breakdown_mask_at_every_tree_level(prec):
+    """Two indefinite modes in an n = 24 instance (det(I - O) > 0 overall): the engine reports
+    a single-mode subset (smallest failing mask, one of its two pivot rows) whichever tree level
+    evaluates those modes -- prefix levels, producer DFS / fan-out, or the consumers' lane
+    subtrees, where the key is kept per thread and published once."""
+    n = 24
+    masks, rows = [], set()
+    for k in (0, 4, 9, 14, 22):
+        a = [0.1] * n
+        c = [0.05] * n
+        for j in (k, k + 1):
+            a[j], c[j] = 0.5, 0.7  # det of I - O_{j} = 0.25 - 0.49 < 0
+        with pytest.raises(T.BreakdownError) as e:
+            T.torontonian(diag_instance(n, a, c), prec)
+        assert bin(e.value.subset_mask).count("1") == 1, (k, e.value.subset_mask)
+        rows.add(e.value.pivot_row)
+        masks.append(e.value.subset_mask)
+    assert len(set(masks)) == len(masks)
+    assert len(rows) == 1 and rows <= {0, 1}, rows  # the same pivot row of a one-mode subset
+
+
+@pytest.mark.parametrize("prec", ["fp64", "128", "256"])
+def test_negative_definite_block_breaks_down_at_every_level(prec):
+    """A mode whose 2x2 block of I - O is negative definite (det > 0, so det(I - O) > 0 and
+    the one-mode Torontonian term is finite) must still break down at the first pivot, as the
+    reference's Cholesky does -- including when that mode is the last one eliminated (the
+    leaf term, which otherwise needs only the determinant)."""
+    n = 24
+    masks = []
+    for k in (0, 4, 9, 14, 22, 23):
+        a = [0.1] * n
+        c = [0.05] * n
+        a[k], c[k] = 1.5, 0.1  # eigenvalues of the block: -0.6, -0.4
+        with pytest.raises(T.BreakdownError) as e:
+            T.torontonian(diag_instance(n, a, c), prec)
+        assert bin(e.value.subset_mask).count("1") == 1, (k, e.value.subset_mask)
+        assert e.value.pivot_row == 0, (k, e.value.pivot_row)
+        masks.append(e.value.subset_mask)
+    assert len(set(masks)) == len(masks)
+
+
 def test_probabilities():
     """test_torontonian.cpp:246-268."""
     a = diag_instance(1, [0.3], [0.1])
