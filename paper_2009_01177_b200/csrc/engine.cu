@@ -172,6 +172,9 @@ __device__ __forceinline__ void report_breakdown(unsigned long long* err, uint64
 #ifndef TOR_BAD_DEFER
 #define TOR_BAD_DEFER 1
 #endif
+#ifndef TOR_BAD_DEFER_P
+#define TOR_BAD_DEFER_P 0
+#endif
 struct LocalErr {
     unsigned long long v = ~0ull;
     __device__ __forceinline__ void flush(unsigned long long* err) const {
@@ -1474,6 +1477,12 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
     // DFS step + root + fan-out of one leaf of job J into the fan area fsm (buffers +
     // t values): all FAN levels, or (warp-specialised) levels 1..FAN-1 -- the level-FAN
     // states in shared memory, or in TMEM at tm_slot for the TMEM types
+#if TOR_BAD_DEFER_P
+    LocalErr perr_l;  // fan-out breakdown keys of this warp, published at kernel end
+    LocalErr* perr = &perr_l;
+#else
+    unsigned long long* perr = err;
+#endif
     auto produce_leaf = [&](const Job<T>& J, uint64_t leaf, uint32_t tm_slot, T* fsm, T* dfs_t, T* slots) {
         T* ftv = fsm + SM::kTOff;
         PHASE_T0();
@@ -1527,12 +1536,12 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         const uint64_t leaf_mask = J.mask | (leaf << Q0);
         const int leaf_sel = J.nsel + __popcll(leaf);
         PHASE_MARK(1);
-        FanLevel<T, 1>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
-        FanLevel<T, 2>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
+        FanLevel<T, 1>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
+        FanLevel<T, 2>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
         if constexpr (Cfg<T>::WS_MODE != 2 || kConsFirst > 3)
-            FanLevel<T, 3>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
-        if constexpr (Cfg<T>::WS_MODE != 2) FanLevel<T, 4>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
-        if constexpr (!Cfg<T>::WS) FanLevel<T, 5>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, err, tm_slot);
+            FanLevel<T, 3>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
+        if constexpr (Cfg<T>::WS_MODE != 2) FanLevel<T, 4>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
+        if constexpr (!Cfg<T>::WS) FanLevel<T, 5>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
     };
     auto write_partial = [&](Acc<T>& acc, unsigned long long job) {
         warp_fold<T>(acc);
@@ -1783,6 +1792,9 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
             write_partial(acc, job);
         }
     }
+#if TOR_BAD_DEFER_P
+    perr_l.flush(err);
+#endif
     if constexpr (Cfg<T>::TMEM) {
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         __syncthreads();
