@@ -97,7 +97,10 @@ typedef struct {
     char code[48];      /* "module/kind", as the reference's Error::code() */
     char message[200];
     int64_t pivot_row;  /* BreakdownError::pivot_row (pair order 2k: x_k, 2k+1: p_k), -1 n/a */
-    uint64_t subset_mask; /* BreakdownError::subset_mask (reference convention), 0 n/a */
+    uint64_t subset_mask; /* BreakdownError::subset_mask (reference convention), 0 n/a.  The engine
+                             checks both pivots of every eliminated mode (leaf modes included) and
+                             reports the numerically smallest failing mask, independent of the
+                             schedule, the device count and the shard layout */
 } tor_error;
 
 /* TorontonianResult (torontonian.hpp:21-29) extended with the multi-word value and
