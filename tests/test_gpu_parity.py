@@ -477,3 +477,21 @@ def test_device_list_folds_bit_identical(prec):
         assert r["words"] == one["words"], devs
         assert r["sum_abs_terms"] == one["sum_abs_terms"]
         assert r["devices"] == (2 if len(devs) == 3 else len(devs))
+
+
+@pytest.mark.gpu
+def test_device_list_breakdown_reports_smallest_mask():
+    # Breakdowns in several shards: the call reports the same (smallest) failing subset as one
+    # device -- shard r covers prefix class r, and the first failing shard in class order wins.
+    n = 24
+    a = [0.1] * n
+    c = [0.05] * n
+    for j in (1, 2, 20, 21):  # four indefinite modes spread over the prefix classes
+        a[j], c[j] = 0.5, 0.7
+    m = diag_instance(n, a, c)
+    with pytest.raises(T.BreakdownError) as one:
+        T.torontonian(m, "128")
+    for devs in ([0, 0], [0, 0, 0, 0], [0] * 8):
+        with pytest.raises(T.BreakdownError) as e:
+            T.torontonian(m, "128", devices=devs)
+        assert (e.value.subset_mask, e.value.pivot_row) == (one.value.subset_mask, one.value.pivot_row), devs
