@@ -128,8 +128,11 @@ typedef struct {
     uint64_t kernel_launches; /* device kernels launched by the call */
     uint64_t h2d_bytes;       /* host->device bytes copied by the call */
     uint64_t d2h_bytes;       /* device->host bytes copied by the call */
-    uint64_t raw_limbs[4];    /* FixedValue limbs (exact in FIXED modes; DD/QD words
-                                 re-quantised at config.frac_bits otherwise: 0) */
+    uint64_t raw_limbs[4];    /* FixedValue limbs (torontonian.hpp:14-29), low limb first:
+                                 FIXED modes: the exact accumulator (identical to the
+                                 reference's); DD/QD: round(sum(words) * 2^config.frac_bits)
+                                 (ties toward +inf, exact) as width_bits two's complement;
+                                 fp64: 0 */
 } tor_result;
 
 /* Shard partial for multi-GPU / multi-process folds: a contiguous, power-of-two
@@ -162,36 +165,74 @@ int tor_force_width(const tor_input* in, int width_bits, tor_precision_config* o
 
 /* Full evaluation (validation N in [1,40], symmetry gate, precision selection,
  * adaptive escalation, device evaluation).  devices == NULL / ndev <= 0: device 0.  With
- * ndev > 1 the prefix classes split into P = 2^k aligned shards (P = the largest power of
- * two <= ndev), one host thread per listed device, folded along the fixed tree:
- * bit-identical to one device; out->devices = P (the reference's `workers` fan-out). */
+ * ndev > 1 the 64 top-level prefix classes split into ndev contiguous ranges (any device
+ * count <= 64; sizes differ by at most one class), one host thread per listed device, and
+ * the per-class partials fold along the fixed tree: bit-identical to one device;
+ * out->devices = the devices used (the reference's `workers` fan-out).  Instances with
+ * fewer than 6 prefix levels (N < 15 in DD, 16 in fp64, 14 in QD) run on the first device.
+ * AUTO: the width select_precision picks (128 -> DD, 256 -> QD), then the posterior check:
+ * if fewer than b_sgn bits survive the cancellation (bits_left < b_sgn; a sum that cancels
+ * to exactly 0 counts as no bits left unless the input is exactly zero), DD re-runs in QD
+ * (escalated = 1), and a QD result that still fails raises PrecisionError
+ * "precision/insufficient". */
 int tor_torontonian(const tor_input* in, tor_precision prec, const int* devices, int ndev,
                     tor_result* out, tor_error* err);
 
 /* fp64 oracle semantics (N <= 20, PrecisionError "torontonian/nonfinite"), computed
- * on the device by the same engine in fp64. */
+ * on the device by the same engine in fp64.  Like the reference there is no pivot check:
+ * a non-positive pivot makes the sum non-finite ("torontonian/nonfinite").  Difference: on
+ * an input whose I - A_Z has a negative-definite 2x2 mode block (det > 0) the reference's
+ * LU-style elimination returns a finite number, this Cholesky-based path "nonfinite"; such
+ * inputs are not physical states (I - A must be positive definite). */
 int tor_torontonian_reference(const tor_input* in, double* value, tor_error* err);
 
-/* `count` instances of equal N in one device pass (BASELINE config 3).  AUTO selects the
- * width per instance exactly as tor_torontonian (DD and QD sub-batches) including the
- * posterior escalation; validation errors report the first bad instance in index order. */
+/* `count` instances of equal N in one device pass (BASELINE config 3); prec AUTO, 128, 256 or
+ * fp64.  AUTO selects the width per instance exactly as tor_torontonian (DD and QD
+ * sub-batches) including the posterior check: failing DD instances re-run in QD, and a QD
+ * instance that fails it raises "precision/insufficient" naming the instance; validation
+ * errors report the first bad instance in index order. */
 int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, int device,
                           tor_result* outs, tor_error* err);
 
 /* Partial sum over prefix classes [class_lo, class_hi) of the top class_bits mask
  * bits on one device (the subset of torontonian_partial's masks with those
- * prefixes).  prec must not be AUTO.  N in [1, 50] (beyond the reference's 40: the
+ * prefixes).  prec: 128, 256 or fp64.  N in [1, 50] (beyond the reference's 40: the
  * paper's n = 50 case as checkpointable class ranges); slices, shards and plans only. */
 int tor_torontonian_slice(const tor_input* in, tor_precision prec, int class_bits, uint64_t class_lo,
                           uint64_t class_hi, int device, tor_partial* out, tor_error* err);
+
+/* Schedule hints for tor_torontonian_classes (0 = the default schedule).  prefix_jobs sets
+ * the prefix depth c (the smallest c with 2^c >= prefix_jobs, capped by the problem), and so
+ * the depth of the producer DFS below it; blocks_per_sm overrides the subtree kernel's CTAs
+ * per SM.  Results stay within the mode's tolerance; they are bit-identical only between
+ * runs with the same prefix_jobs.  Replaces round-1's TOR_WANT_JOBS / TOR_BLOCKS_PER_SM
+ * environment knobs (the library reads no environment variable that changes results;
+ * TOR_DEBUG_TIMING=1 only prints host/device timings to stderr). */
+typedef struct {
+    uint64_t prefix_jobs;
+    int blocks_per_sm;
+    int reserved;
+} tor_schedule;
+
+/* One partial per prefix class of [class_lo, class_hi) (class_hi - class_lo <= 2^24 entries in
+ * outs, in class order) from ONE device pass.  Each class partial is an aligned subtree of
+ * the engine's fixed fold tree, so any assignment of classes to devices or processes folds
+ * bit-identically with tor_fold_partials (this is how N devices that are not a power of two
+ * split a Torontonian).  sched may be NULL. */
+int tor_torontonian_classes(const tor_input* in, tor_precision prec, int class_bits, uint64_t class_lo,
+                            uint64_t class_hi, int device, const tor_schedule* sched, tor_partial* outs,
+                            tor_error* err);
 
 /* Rank `rank` of `world` (power of two) evaluates its aligned share of the 2^k
  * top-level classes. */
 int tor_torontonian_shard(const tor_input* in, tor_precision prec, int rank, int world, int device,
                           tor_partial* out, tor_error* err);
 
-/* Fold shard partials (sorted by class_lo, contiguous, power-of-two aligned) along
- * the engine's fixed tree; bit-identical to a single-device run. */
+/* Fold shard partials along the engine's fixed tree; bit-identical to a single-device run.
+ * The partials must share mode and class_bits, be sorted and contiguous, cover every class
+ * [0, 2^class_bits), each span an aligned power-of-two class range (lo % width == 0), and
+ * their term counts must add up to 2^N; otherwise TOR_E_INVALID "torontonian/shard"
+ * (e.g. a rank missing from an all-gather). */
 int tor_fold_partials(const tor_partial* parts, int count, const tor_input* in, tor_result* out,
                       tor_error* err);
 
@@ -206,7 +247,7 @@ int tor_probability_modes(const tor_input* full, const int* modes, int nmodes, t
 /* Prepared evaluation with device-resident inputs (the exact R is uploaded once):
  * create -> execute (repeatable; runs the whole device pipeline and reads back the
  * result words) -> destroy.  The range is [class_lo, class_hi) of the top class_bits
- * mask bits ([0,1) of 0 bits = the whole Torontonian).  prec must not be AUTO. */
+ * mask bits ([0,1) of 0 bits = the whole Torontonian).  prec: 128, 256 or fp64. */
 typedef struct tor_plan tor_plan;
 int tor_plan_create(const tor_input* in, tor_precision prec, int class_bits, uint64_t class_lo,
                     uint64_t class_hi, int device, tor_plan** out, tor_error* err);

@@ -6,7 +6,7 @@
 """
 from .api import (device_count, det_i_minus_a, fold_partials, force_width, probability,
                   probability_reference, select_precision, torontonian, torontonian_batch,
-                  torontonian_reference, torontonian_shard, torontonian_slice)
+                  torontonian_classes, torontonian_reference, torontonian_shard, torontonian_slice)
 from .errors import (BreakdownError, DeviceError, InvalidArgument, ParseError, PrecisionError,
                      ResourceError, TorfpError)
 from .matrix import (InputMatrix, check_symmetries, dequantize, extract_submatrix, from_dense,
@@ -21,7 +21,7 @@ __all__ = [
     "factorization_op_count", "from_dense", "generate_instance", "get_kth_mask", "get_next_mask",
     "load_matrix", "partition", "prefix_classes", "probability", "probability_reference", "quantize",
     "select_precision", "force_width", "det_i_minus_a", "torontonian", "torontonian_reference",
-    "torontonian_batch", "torontonian_slice", "torontonian_shard", "fold_partials", "total_op_count",
+    "torontonian_batch", "torontonian_slice", "torontonian_classes", "torontonian_shard", "fold_partials", "total_op_count",
     "device_count",
 ]
 

@@ -58,10 +58,15 @@ class TorPartial(C.Structure):
                 ("words", C.c_double * 4), ("sum_abs", C.c_double), ("term_count", C.c_uint64)]
 
 
+class TorSchedule(C.Structure):
+    _fields_ = [("prefix_jobs", C.c_uint64), ("blocks_per_sm", C.c_int), ("reserved", C.c_int)]
+
+
 # every symbol include/tor_capi.h declares (checked by tests/test_capi.py)
 EXPORTS = ("tor_abi_version", "tor_check_symmetries", "tor_check_dense", "tor_det_i_minus_a",
            "tor_select_precision", "tor_force_width", "tor_torontonian", "tor_torontonian_reference",
-           "tor_torontonian_batch", "tor_torontonian_slice", "tor_torontonian_shard", "tor_fold_partials",
+           "tor_torontonian_batch", "tor_torontonian_slice", "tor_torontonian_classes", "tor_torontonian_shard",
+           "tor_fold_partials",
            "tor_probability", "tor_probability_modes", "tor_device_count", "tor_plan_create", "tor_plan_execute", "tor_plan_destroy",
            "tor_release_device_cache")
 
@@ -82,6 +87,8 @@ def lib():
         L.tor_torontonian_batch.argtypes = [P(TorInput), C.c_int, C.c_int, C.c_int, P(TorResult), P(TorError)]
         L.tor_torontonian_slice.argtypes = [P(TorInput), C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int,
                                             P(TorPartial), P(TorError)]
+        L.tor_torontonian_classes.argtypes = [P(TorInput), C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int,
+                                              P(TorSchedule), P(TorPartial), P(TorError)]
         L.tor_torontonian_shard.argtypes = [P(TorInput), C.c_int, C.c_int, C.c_int, C.c_int, P(TorPartial),
                                             P(TorError)]
         L.tor_fold_partials.argtypes = [P(TorPartial), C.c_int, P(TorInput), P(TorResult), P(TorError)]
@@ -161,8 +168,7 @@ def _result_dict(r: TorResult, workers: int) -> dict:
     return {
         # reference keys (bindings.cpp:69-85)
         "value": r.value,
-        "raw_limbs": (tuple(int(x) for x in r.raw_limbs) if r.mode in (PREC_FIXED128, PREC_FIXED256)
-                      else raw_limbs(words, r.width_bits, cfg["frac_bits"])),
+        "raw_limbs": tuple(int(x) for x in r.raw_limbs),
         "width_bits": r.width_bits,
         "config": cfg,
         "term_count": r.term_count,
@@ -224,6 +230,21 @@ def torontonian_slice(matrix: InputMatrix, precision, class_bits: int, class_lo:
     _check(lib().tor_torontonian_slice(C.byref(inp.s), _prec(precision), class_bits, class_lo, class_hi, device,
                                        C.byref(p), C.byref(err)), err)
     return _partial_dict(p)
+
+
+def torontonian_classes(matrix: InputMatrix, precision, class_bits: int, class_lo: int, class_hi: int,
+                        device: int = 0, prefix_jobs: int = 0, blocks_per_sm: int = 0) -> list[dict]:
+    """One partial per prefix class of [class_lo, class_hi) from one device pass
+    (tor_torontonian_classes); ``prefix_jobs`` / ``blocks_per_sm`` are the schedule hints
+    (0 = default)."""
+    inp = _In(matrix)
+    cnt = class_hi - class_lo
+    arr = (TorPartial * max(cnt, 1))()
+    sch = TorSchedule(prefix_jobs, blocks_per_sm, 0)
+    err = TorError()
+    _check(lib().tor_torontonian_classes(C.byref(inp.s), _prec(precision), class_bits, class_lo, class_hi, device,
+                                         C.byref(sch), arr, C.byref(err)), err)
+    return [_partial_dict(arr[i]) for i in range(cnt)]
 
 
 def torontonian_shard(matrix: InputMatrix, precision, rank: int, world: int, device: int = 0) -> dict:

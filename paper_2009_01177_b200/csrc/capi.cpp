@@ -129,6 +129,73 @@ double mantissa_bits(int mode) { return mode == MODE_FP64 ? 52.0 : (mode == MODE
 
 double words_value(const double* w) { return ((w[3] + w[2]) + w[1]) + w[0]; }
 
+// FixedValue limbs of a multi-word value: round(sum(words) * 2^frac_bits) (ties toward +inf)
+// as width_bits two's complement, low limb first -- the reference's raw accumulator
+// format (torontonian.hpp:14-29) at its own scaling.  Exact: the words are summed in a
+// 2176-bit integer at scale 2^1100 (every finite double is an integer multiple of 2^-1074).
+void requantise(const double* words, int nwords, int width_bits, unsigned frac_bits, uint64_t* limbs4) {
+    for (int i = 0; i < 4; ++i) limbs4[i] = 0;
+    if (width_bits != 128 && width_bits != 256) return;
+    constexpr int kL = 34, kScale = 1100;
+    uint64_t acc[kL] = {};
+    auto add_shifted = [&](uint64_t m, int sh, bool neg) {  // acc += (neg ? -1 : 1) * m * 2^sh
+        uint64_t t[kL] = {};
+        const int li = sh / 64, bi = sh % 64;
+        if (li < kL) t[li] = m << bi;
+        if (bi && li + 1 < kL) t[li + 1] = m >> (64 - bi);
+        if (neg) {  // two's complement of t
+            uint64_t c = 1;
+            for (int i = 0; i < kL; ++i) {
+                const uint64_t v = ~t[i] + c;
+                c = (c && v == 0) ? 1 : 0;
+                t[i] = v;
+            }
+        }
+        unsigned __int128 c = 0;
+        for (int i = 0; i < kL; ++i) {
+            c += static_cast<unsigned __int128>(acc[i]) + t[i];
+            acc[i] = static_cast<uint64_t>(c);
+            c >>= 64;
+        }
+    };
+    for (int k = 0; k < nwords; ++k) {
+        const double w = words[k];
+        if (w == 0.0 || !std::isfinite(w)) continue;
+        int e = 0;
+        const double fr = std::frexp(std::fabs(w), &e);           // |w| = fr * 2^e, fr in [0.5, 1)
+        const uint64_t m = static_cast<uint64_t>(std::ldexp(fr, 53));  // |w| = m * 2^(e-53), exact
+        const int sh = e - 53 + kScale;
+        if (sh < 0) continue;  // below 2^-1100: cannot occur for finite doubles
+        add_shifted(m, sh, w < 0);
+    }
+    // + 2^(kScale - f - 1), then arithmetic shift right by kScale - f
+    const int rs = kScale - static_cast<int>(frac_bits);
+    if (rs <= 0 || rs > 64 * (kL - 4)) return;
+    add_shifted(1, rs - 1, false);
+    for (int i = 0; i < 4; ++i) {
+        const int bit = rs + 64 * i, li = bit / 64, bi = bit % 64;
+        uint64_t v = li < kL ? acc[li] >> bi : ~0ull;
+        if (bi && li + 1 < kL) v |= acc[li + 1] << (64 - bi);
+        limbs4[i] = i < width_bits / 64 ? v : 0;
+    }
+}
+
+// Tor(0) = 0 exactly (every term is +-1): the only input whose zero sum is exempt from the
+// posterior cancellation check.
+bool zero_input(const Input& a) {
+    for (const auto* v : {&a.a00, &a.a01})
+        for (const auto& x : *v)
+            if (x.real() != 0.0 || x.imag() != 0.0) return false;
+    return true;
+}
+
+// AUTO's posterior check (precision.cpp:80-121 sizes the width a priori; the budget's
+// lower bound is blind on pure states, a_repr = 0): at least b_sgn significant bits must
+// survive the cancellation sum|t| / |Tor| after the growth allowance.
+bool posterior_ok(const Input& a, const tor_result& r, const PrecCfg& cfg) {
+    return zero_input(a) || r.bits_left >= cfg.b_sgn;
+}
+
 void device_check(int device) {
     int cnt = 0;
     const cudaError_t e = cudaGetDeviceCount(&cnt);
@@ -140,7 +207,7 @@ void device_check(int device) {
 
 // Runs the engine and maps its failures onto the error taxonomy.
 std::vector<EngineOut> run(int device, int mode, const std::vector<Input>& ins, const WorkRange& range,
-                           EngineStats* stats) {
+                           EngineStats* stats, bool check_breakdown = true) {
     const auto t0 = std::chrono::steady_clock::now();
     device_check(device);
     const auto t1 = std::chrono::steady_clock::now();
@@ -159,7 +226,7 @@ std::vector<EngineOut> run(int device, int mode, const std::vector<Input>& ins, 
     const int st = engine_run(device, mode, prep, range, out, stats, err);
     if (st != 0) throw HostError(TOR_E_DEVICE, "device/cuda", err);
     for (const auto& o : out)
-        if (o.breakdown) {
+        if (check_breakdown && o.breakdown) {
             HostError h(TOR_E_BREAKDOWN, "linalg/breakdown", "non-positive pivot in elimination");
             h.pivot_row = o.bad_row;
             h.subset_mask = o.bad_mask;
@@ -191,37 +258,42 @@ void fill_result(const Input& a, int mode, const PrecCfg& cfg, const EngineOut& 
     r->kernel_launches = st.launches;
     r->h2d_bytes = st.h2d_bytes;
     r->d2h_bytes = st.d2h_bytes;
+    if (mode != MODE_FP64) requantise(o.words, mode_words(mode), r->width_bits, cfg.frac_bits, r->raw_limbs);
 }
 
-// One Torontonian on several devices of this process: the prefix classes are split into
-// P = 2^k aligned shards (P = the largest power of two <= the device count), one host thread
-// per device, and the shard partials fold along the engine's fixed tree -- bit-identical to
-// a single-device run (the reference's `workers` fan-out, torontonian.cpp:112-147).
+// One Torontonian on several devices of this process (the reference's `workers` fan-out,
+// torontonian.cpp:112-147): the 2^kShardBits top-level prefix classes are split into P
+// contiguous ranges (P = the device count, any P <= 2^kShardBits; ranges differ by at most
+// one class), one host thread per device; each device returns one partial per class (an
+// aligned subtree of the engine's fixed fold tree) and the host folds all classes along the
+// same tree -- bit-identical to a single-device run.  Instances too small to have
+// kShardBits prefix levels run on the first device.
+constexpr int kShardBits = 6;
 EngineOut run_devices(const std::vector<int>& devs, int mode, const Input& a, EngineStats* stats, int* used) {
-    int P = 1;
-    while (2 * P <= static_cast<int>(devs.size())) P *= 2;
+    const int ncls = 1 << kShardBits;
+    int P = std::min(static_cast<int>(devs.size()), ncls);
+    if (a.n < engine_tree_min_n(mode) + kShardBits) P = 1;
     if (used) *used = P;
     if (P == 1) return run(devs[0], mode, {a}, WorkRange{}, stats)[0];
-    int k = 0;
-    while ((1 << k) < P) ++k;
     std::vector<EngineOut> parts(P);
     std::vector<EngineStats> sts(P);
     parallel_for_n(P, [&](int r) {
         WorkRange wr;
-        wr.class_bits = k;
-        wr.class_lo = static_cast<uint64_t>(r);
-        wr.class_hi = static_cast<uint64_t>(r) + 1;
+        wr.class_bits = kShardBits;
+        wr.class_lo = static_cast<uint64_t>(ncls) * r / P;
+        wr.class_hi = static_cast<uint64_t>(ncls) * (r + 1) / P;
+        wr.class_partials = true;
         parts[r] = run(devs[r], mode, {a}, wr, &sts[r])[0];
     });
-    std::vector<double> buf(static_cast<size_t>(P) * 5);
+    std::vector<double> buf;
     EngineOut o;
     for (int r = 0; r < P; ++r) {
-        for (int x = 0; x < 4; ++x) buf[r * 5 + x] = parts[r].words[x];
-        buf[r * 5 + 4] = parts[r].sum_abs;
+        buf.insert(buf.end(), parts[r].class_parts.begin(), parts[r].class_parts.end());
         o.terms += parts[r].terms;
     }
+    if (buf.size() != static_cast<size_t>(ncls) * 5) throw HostError(TOR_E_DEVICE, "device/cuda", "missing class partials");
     double w5[5];
-    fold_words(mode, buf.data(), P, w5);
+    fold_words(mode, buf.data(), ncls, w5);
     for (int x = 0; x < 4; ++x) o.words[x] = w5[x];
     o.sum_abs = w5[4];
     if (stats) {
@@ -426,14 +498,14 @@ int tor_torontonian(const tor_input* in, tor_precision prec, const int* devices,
             // posterior check: keep >= b_sgn significant bits after cancellation
             tor_result tmp;
             fill_result(a, mode, cfg, res[0], st, 0.0, 1, &tmp);
-            if (tmp.value != 0.0 && tmp.bits_left < cfg.b_sgn) {
+            if (!posterior_ok(a, tmp, cfg)) {
                 if (mode == MODE_DD) {
                     mode = MODE_QD;
                     escalated = 1;
                     res = {run_devices(devs, mode, a, &st, &used)};
                     fill_result(a, mode, cfg, res[0], st, 0.0, 1, &tmp);
                 }
-                if (tmp.bits_left < cfg.b_sgn)
+                if (!posterior_ok(a, tmp, cfg))
                     throw HostError(TOR_E_PRECISION, "precision/insufficient",
                                     "cancellation leaves fewer than b_sgn significant bits");
             }
@@ -452,7 +524,9 @@ int tor_torontonian_reference(const tor_input* in, double* value, tor_error* err
         clear_err(err);
         const Input a = checked_input(in, 20);
         EngineStats st;
-        const auto res = run(0, MODE_FP64, {a}, WorkRange{}, &st);
+        // torontonian_reference (torontonian.cpp:179-200) has no pivot check: a breakdown
+        // surfaces as a non-finite sum (the Cholesky pivots of an indefinite block are NaN)
+        const auto res = run(0, MODE_FP64, {a}, WorkRange{}, &st, /*check_breakdown=*/false);
         const double v = words_value(res[0].words);
         if (!std::isfinite(v))
             throw HostError(TOR_E_PRECISION, "torontonian/nonfinite", "non-finite term in reference summation");
@@ -468,6 +542,8 @@ int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, i
     try {
         clear_err(err);
         if (count < 1 || !ins) throw HostError(TOR_E_INVALID, "torontonian/range", "empty batch");
+        if (prec < TOR_PREC_AUTO || prec > TOR_PREC_FP64)
+            throw HostError(TOR_E_INVALID, "precision/range", "batch supports auto, 128, 256 and fp64");
         const auto t0 = std::chrono::steady_clock::now();
         std::vector<Input> as(count);
         const int mode = prec == TOR_PREC_AUTO ? MODE_DD : mode_of(prec);
@@ -520,15 +596,21 @@ int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, i
             for (int i : dd_idx) {
                 tor_result tmp;
                 fill_result(as[i], MODE_DD, cfgs[i], res[i], st, 0.0, 1, &tmp);
-                if (tmp.value != 0.0 && tmp.bits_left < cfgs[i].b_sgn) esc.push_back(i);
+                if (!posterior_ok(as[i], tmp, cfgs[i])) esc.push_back(i);
             }
             run_group(MODE_QD, esc);
-            for (int i : esc) {
+            // every QD result (selected a priori or escalated) passes the same check as
+            // tor_torontonian; the first failing instance in index order is reported
+            std::vector<int> qd_all(qd_idx);
+            qd_all.insert(qd_all.end(), esc.begin(), esc.end());
+            std::sort(qd_all.begin(), qd_all.end());
+            for (int i : qd_all) {
                 tor_result tmp;
                 fill_result(as[i], MODE_QD, cfgs[i], res[i], st, 0.0, 1, &tmp);
-                if (tmp.bits_left < cfgs[i].b_sgn)
+                if (!posterior_ok(as[i], tmp, cfgs[i]))
                     throw HostError(TOR_E_PRECISION, "precision/insufficient",
-                                    "cancellation leaves fewer than b_sgn significant bits");
+                                    "instance " + std::to_string(i) +
+                                        ": cancellation leaves fewer than b_sgn significant bits");
             }
             for (int i : esc) modes[i] = -modes[i] - 1;  // mark escalated (decoded below)
         }
@@ -551,29 +633,81 @@ int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, i
     }
 }
 
+namespace {
+// explicit evaluation modes of slices, shards, class partials and plans
+int explicit_mode(tor_precision prec, const char* what) {
+    if (prec != TOR_PREC_W128_DD && prec != TOR_PREC_W256_QD && prec != TOR_PREC_FP64)
+        throw HostError(TOR_E_INVALID, "precision/range", std::string(what) + " needs prec 128, 256 or fp64");
+    return mode_of(prec);
+}
+
+WorkRange class_range(const Input& a, int class_bits, uint64_t class_lo, uint64_t class_hi) {
+    if (class_bits < 0 || class_bits > a.n || class_bits > 62 || class_hi <= class_lo ||
+        class_hi > (1ull << class_bits))
+        throw HostError(TOR_E_INVALID, "torontonian/slice", "bad class range");
+    WorkRange wr;
+    wr.class_bits = class_bits;
+    wr.class_lo = class_lo;
+    wr.class_hi = class_hi;
+    return wr;
+}
+
+void put_partial(tor_precision prec, const WorkRange& wr, const double* w5, uint64_t terms, tor_partial* out) {
+    std::memset(out, 0, sizeof(*out));
+    out->mode = prec;
+    out->class_bits = wr.class_bits;
+    out->class_lo = wr.class_lo;
+    out->class_hi = wr.class_hi;
+    for (int i = 0; i < 4; ++i) out->words[i] = w5[i];
+    out->sum_abs = w5[4];
+    out->term_count = terms;
+}
+}  // namespace
+
 int tor_torontonian_slice(const tor_input* in, tor_precision prec, int class_bits, uint64_t class_lo,
                           uint64_t class_hi, int device, tor_partial* out, tor_error* err) {
     try {
         clear_err(err);
         const Input a = checked_input(in, kMaxSliceModes);
-        if (prec == TOR_PREC_AUTO) throw HostError(TOR_E_INVALID, "precision/range", "slice needs an explicit mode");
-        if (class_bits < 0 || class_bits > a.n || class_hi <= class_lo || class_hi > (1ull << class_bits))
-            throw HostError(TOR_E_INVALID, "torontonian/slice", "bad class range");
-        const int mode = mode_of(prec);
-        WorkRange wr;
-        wr.class_bits = class_bits;
-        wr.class_lo = class_lo;
-        wr.class_hi = class_hi;
+        const int mode = explicit_mode(prec, "slice");
+        const WorkRange wr = class_range(a, class_bits, class_lo, class_hi);
         EngineStats st;
         const auto res = run(device, mode, {a}, wr, &st);
-        std::memset(out, 0, sizeof(*out));
-        out->mode = prec;
-        out->class_bits = class_bits;
-        out->class_lo = class_lo;
-        out->class_hi = class_hi;
-        for (int i = 0; i < 4; ++i) out->words[i] = res[0].words[i];
-        out->sum_abs = res[0].sum_abs;
-        out->term_count = res[0].terms;
+        double w5[5] = {res[0].words[0], res[0].words[1], res[0].words[2], res[0].words[3], res[0].sum_abs};
+        put_partial(prec, wr, w5, res[0].terms, out);
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+int tor_torontonian_classes(const tor_input* in, tor_precision prec, int class_bits, uint64_t class_lo,
+                            uint64_t class_hi, int device, const tor_schedule* sched, tor_partial* outs,
+                            tor_error* err) {
+    try {
+        clear_err(err);
+        const Input a = checked_input(in, kMaxSliceModes);
+        const int mode = explicit_mode(prec, "class partials");
+        WorkRange wr = class_range(a, class_bits, class_lo, class_hi);
+        if (!outs) throw HostError(TOR_E_INVALID, "torontonian/slice", "null output array");
+        if (class_hi - class_lo > (1ull << 24))
+            throw HostError(TOR_E_INVALID, "torontonian/slice", "at most 2^24 class partials per call");
+        wr.class_partials = true;
+        if (sched) {
+            wr.prefix_jobs = sched->prefix_jobs;
+            wr.blocks_per_sm = sched->blocks_per_sm;
+        }
+        EngineStats st;
+        const auto res = run(device, mode, {a}, wr, &st);
+        const uint64_t ncls = class_hi - class_lo;
+        if (res[0].class_parts.size() != ncls * 5) throw HostError(TOR_E_DEVICE, "device/cuda", "class partials lost");
+        const uint64_t per = res[0].terms / ncls;
+        for (uint64_t c = 0; c < ncls; ++c) {
+            WorkRange one = wr;
+            one.class_lo = class_lo + c;
+            one.class_hi = class_lo + c + 1;
+            put_partial(prec, one, &res[0].class_parts[5 * c], per, &outs[c]);
+        }
         return TOR_OK;
     } catch (const HostError& h) {
         return fail(err, h);
@@ -603,18 +737,33 @@ int tor_fold_partials(const tor_partial* parts, int count, const tor_input* in, 
         clear_err(err);
         if (count < 1 || !parts) throw HostError(TOR_E_INVALID, "torontonian/shard", "no partials");
         const Input a = checked_input(in, kMaxSliceModes);
-        const int mode = mode_of(static_cast<tor_precision>(parts[0].mode));
+        const tor_precision prec = static_cast<tor_precision>(parts[0].mode);
+        const int mode = explicit_mode(prec, "fold");
+        const int k = parts[0].class_bits;
+        if (k < 0 || k > a.n || k > 62) throw HostError(TOR_E_INVALID, "torontonian/shard", "bad class bits");
         std::vector<double> buf(static_cast<size_t>(count) * 5);
+        std::vector<uint64_t> lo(count), wd(count);
         uint64_t terms = 0;
         for (int i = 0; i < count; ++i) {
-            if (i > 0 && (parts[i].class_bits != parts[0].class_bits || parts[i].class_lo != parts[i - 1].class_hi))
+            const tor_partial& p = parts[i];
+            if (p.mode != parts[0].mode || p.class_bits != k)
+                throw HostError(TOR_E_INVALID, "torontonian/shard", "partials of mixed modes or class bits");
+            if (p.class_hi <= p.class_lo || (i > 0 && p.class_lo != parts[i - 1].class_hi))
                 throw HostError(TOR_E_INVALID, "torontonian/shard", "partials must be contiguous and sorted");
-            for (int x = 0; x < 4; ++x) buf[i * 5 + x] = parts[i].words[x];
-            buf[i * 5 + 4] = parts[i].sum_abs;
-            terms += parts[i].term_count;
+            for (int x = 0; x < 4; ++x) buf[i * 5 + x] = p.words[x];
+            buf[i * 5 + 4] = p.sum_abs;
+            lo[i] = p.class_lo;
+            wd[i] = p.class_hi - p.class_lo;
+            terms += p.term_count;
         }
+        if (parts[0].class_lo != 0 || parts[count - 1].class_hi != (1ull << k))
+            throw HostError(TOR_E_INVALID, "torontonian/shard", "partials must cover every class (a missing rank?)");
+        if (a.n < 64 && terms != (1ull << a.n))
+            throw HostError(TOR_E_INVALID, "torontonian/shard", "partial term counts do not add up to 2^N");
         double w5[5];
-        fold_words(mode, buf.data(), count, w5);
+        if (!fold_blocks(mode, buf.data(), lo.data(), wd.data(), count, k, w5))
+            throw HostError(TOR_E_INVALID, "torontonian/shard",
+                            "every partial must span an aligned power-of-two class range");
         EngineOut o;
         for (int x = 0; x < 4; ++x) o.words[x] = w5[x];
         o.sum_abs = w5[4];
@@ -635,23 +784,17 @@ int tor_plan_create(const tor_input* in, tor_precision prec, int class_bits, uin
         clear_err(err);
         *out = nullptr;
         const Input a = checked_input(in, kMaxSliceModes);
-        if (prec == TOR_PREC_AUTO || prec < TOR_PREC_AUTO || prec > TOR_PREC_FP64)
-            throw HostError(TOR_E_INVALID, "precision/range", "plan needs an explicit mode");
-        if (class_bits < 0 || class_bits > a.n || class_hi <= class_lo || class_hi > (1ull << class_bits))
-            throw HostError(TOR_E_INVALID, "torontonian/slice", "bad class range");
+        const int mode = explicit_mode(prec, "plan");
+        const WorkRange wr = class_range(a, class_bits, class_lo, class_hi);
         device_check(device);
         auto* p = new tor_plan();
         p->in = a;
-        p->mode = mode_of(prec);
+        p->mode = mode;
         if (p->mode == MODE_FP64) p->cfg.width_bits = 64;
         else p->cfg = force_width(a, p->mode == MODE_DD ? 128 : 256);
         PreparedInput pi;
         pi.n = a.n;
         pi.R = build_R(a, mode_words(p->mode), p->mode == MODE_DD, &pi.tscale_log2);
-        WorkRange wr;
-        wr.class_bits = class_bits;
-        wr.class_lo = class_lo;
-        wr.class_hi = class_hi;
         std::string e;
         if (plan_create(device, p->mode, {pi}, wr, &p->plan, e) != 0) {
             delete p;

@@ -28,6 +28,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "arith.cuh"
@@ -1879,8 +1880,11 @@ template <class T> __host__ __device__ inline void merge_words(double* a, const 
 // kFoldB, kFoldB^2, ... reproduce the whole tree exactly (bit-identical to a single
 // sequential fold, and to fold_words on the host).
 constexpr int kFoldB = 512;
+// G (a power of two <= kFoldB): groups of G elements fold separately, stopping the tree at
+// subtrees of G*S partials (the per-class partials of WorkRange::class_partials).
 template <class T>
-__global__ void __launch_bounds__(kFoldB / 2) fold_pass_kernel(double* partials, uint64_t per, uint64_t S, int inst0) {
+__global__ void __launch_bounds__(kFoldB / 2) fold_pass_kernel(double* partials, uint64_t per, uint64_t S, int inst0,
+                                                               int G) {
     __shared__ double sh[kFoldB * 5];
     double* p = partials + (inst0 + static_cast<uint64_t>(blockIdx.y)) * per * 5;
     const uint64_t cnt = (per + S - 1) / S;
@@ -1890,12 +1894,15 @@ __global__ void __launch_bounds__(kFoldB / 2) fold_pass_kernel(double* partials,
         sh[x] = k < cnt ? p[(k * S) * 5 + x % 5] : 0.0;
     }
     __syncthreads();
-    for (int s = 1; s < kFoldB; s <<= 1) {
+    for (int s = 1; s < G; s <<= 1) {
         const int i = threadIdx.x * 2 * s;
         if (i < kFoldB && k0 + i + s < cnt) merge_words<T>(sh + i * 5, sh + (i + s) * 5);
         __syncthreads();
     }
-    if (threadIdx.x < 5) p[(k0 * S) * 5 + threadIdx.x] = sh[threadIdx.x];
+    for (int x = threadIdx.x; x < (kFoldB / G) * 5; x += blockDim.x) {
+        const uint64_t k = k0 + static_cast<uint64_t>(x / 5) * G;
+        if (k < cnt) p[(k * S) * 5 + x % 5] = sh[(x / 5) * G * 5 + x % 5];
+    }
 }
 
 // ------------------------------------------------------------ host side ----
@@ -2015,8 +2022,8 @@ class PlanImpl final : public Plan {
         // gives bit-identical results.  kWantJobs whole-problem jobs keep the dynamic
         // schedule's tail short even for the 1/8 shard of an 8-GPU run; job states are
         // <= kMaxJobModes modes.
-        uint64_t want_jobs = kWantJobs;
-        if (const char* wj = std::getenv("TOR_WANT_JOBS")) want_jobs = std::strtoull(wj, nullptr, 10);
+        const uint64_t want_jobs = range.prefix_jobs ? range.prefix_jobs : kWantJobs;
+        class_partials_ = range.class_partials;
         c_ = 0;
         if (n_ >= Q0) {
             int cw = 0;
@@ -2085,7 +2092,7 @@ class PlanImpl final : public Plan {
             // CTAs (256 TMEM columns each = the SM's 512) fit by registers and shared memory
             // and do run concurrently (measured: 264 -> 173 ms at n=32 DD).
             if (Cfg<T>::TMEM && Cfg<T>::WPB == 4 && 2 * (smem_ + 1024) <= 233472) bps = std::max(bps, 2);
-            if (const char* ov = std::getenv("TOR_BLOCKS_PER_SM")) bps = std::max(1, std::atoi(ov));
+            if (range.blocks_per_sm > 0) bps = range.blocks_per_sm;
             if (std::getenv("TOR_DEBUG_TIMING")) {
                 cudaFuncAttributes fa;
                 cudaFuncGetAttributes(&fa, subtree_kernel<T>);
@@ -2194,12 +2201,15 @@ class PlanImpl final : public Plan {
         ++launches;
         CK(cudaGetLastError());
         CK(cudaEventRecord(ev_[2], st_));
-        for (uint64_t S = 1; S < per_; S *= kFoldB) {
+        // jobs per output partial: the whole range, or one class (a power of two)
+        const uint64_t chunk = class_partials_ ? per_ / (chi_ - clo_) : per_;
+        for (uint64_t S = 1; S < chunk; S *= kFoldB) {
             const uint64_t cnt = (per_ + S - 1) / S;
+            const int G = class_partials_ ? static_cast<int>(std::min<uint64_t>(kFoldB, chunk / S)) : kFoldB;
             for (int i0 = 0; i0 < ninst_; i0 += 65535) {
                 const int ni = std::min(ninst_ - i0, 65535);
                 fold_pass_kernel<T><<<dim3(static_cast<unsigned>((cnt + kFoldB - 1) / kFoldB), ni), kFoldB / 2, 0,
-                                      st_>>>(parts, per_, S, i0);
+                                      st_>>>(parts, per_, S, i0, G);
                 ++launches;
             }
         }
@@ -2208,6 +2218,15 @@ class PlanImpl final : public Plan {
         std::vector<double> res(static_cast<size_t>(ninst_) * 5);
         CK(cudaMemcpy2DAsync(res.data(), 5 * sizeof(double), parts, per_ * 5 * sizeof(double), 5 * sizeof(double),
                              ninst_, cudaMemcpyDeviceToHost, st_));
+        std::vector<double> cls;
+        if (class_partials_) {
+            const uint64_t ncls = chi_ - clo_;
+            cls.resize(static_cast<size_t>(ninst_) * ncls * 5);
+            for (int i = 0; i < ninst_; ++i)
+                CK(cudaMemcpy2DAsync(cls.data() + i * ncls * 5, 5 * sizeof(double), parts + i * per_ * 5,
+                                     chunk * 5 * sizeof(double), 5 * sizeof(double), ncls, cudaMemcpyDeviceToHost,
+                                     st_));
+        }
         unsigned long long herr = 0;
         CK(cudaMemcpyAsync(&herr, errw, sizeof(herr), cudaMemcpyDeviceToHost, st_));
         CK(cudaStreamSynchronize(st_));
@@ -2235,6 +2254,16 @@ class PlanImpl final : public Plan {
             for (int x = 0; x < 4; ++x) out[i].words[x] = res[i * 5 + x];
             out[i].sum_abs = res[i * 5 + 4];
             out[i].terms = terms;
+            if (class_partials_) {
+                // the classes, and the range's total folded from them on the host
+                const size_t ncls = chi_ - clo_;
+                out[i].class_parts.assign(cls.begin() + i * ncls * 5, cls.begin() + (i + 1) * ncls * 5);
+                double w5[5];
+                fold_words(std::is_same<T, qd>::value ? MODE_QD : MODE_DD, out[i].class_parts.data(),
+                           static_cast<int>(ncls), w5);
+                for (int x = 0; x < 4; ++x) out[i].words[x] = w5[x];
+                out[i].sum_abs = w5[4];
+            }
             if (herr != ~0ull) {
                 out[i].breakdown = true;
                 out[i].bad_mask = herr >> 8;
@@ -2251,7 +2280,7 @@ class PlanImpl final : public Plan {
             stats->prefix_depth = cj_;
             stats->jobs = njobs_;
             stats->h2d_bytes = h2d_bytes_;
-            stats->d2h_bytes = res.size() * sizeof(double) + sizeof(herr);
+            stats->d2h_bytes = (res.size() + cls.size()) * sizeof(double) + sizeof(herr);
         }
         return 0;
     }
@@ -2261,7 +2290,7 @@ class PlanImpl final : public Plan {
     T* tpool() { return static_cast<T*>(tpool_.p); }
     int device_ = 0, ninst_ = 0, n_ = 0, kbits_ = 0, sm_count_ = 0, c_ = 0, cj_ = 0, rjob_ = 0, tsc_ = 0;
     uint64_t clo_ = 0, chi_ = 1, per_ = 0, njobs_ = 0, blocks_ = 0;
-    bool use_levels_ = true;
+    bool use_levels_ = true, class_partials_ = false;
     PrefixGeom g_{};
     size_t smem_ = 0, scr_stride_ = 1, work_stride_ = 0, h2d_bytes_ = 0;
     cudaStream_t st_ = nullptr;
@@ -2300,7 +2329,7 @@ void release_device_cache() {
 }
 
 int engine_tree_min_n(int mode) {
-    return mode == MODE_QD ? Cfg<qd>::L + FAN : Cfg<dd>::L + FAN;
+    return mode == MODE_QD ? Cfg<qd>::L + FAN : (mode == MODE_DD ? Cfg<dd>::L + FAN : Cfg<double>::L + FAN);
 }
 
 int plan_create(int device, int mode, const std::vector<PreparedInput>& inputs, const WorkRange& range, Plan** out,
@@ -2344,6 +2373,35 @@ int engine_run(int device, int mode, const std::vector<PreparedInput>& inputs, c
                      ms(t1, t2), ms(t2, t3));
     }
     return rs;
+}
+
+namespace {
+// fold of the aligned blocks covering classes [a, a + w) along the fixed tree
+bool fold_range(int mode, const double* parts, const uint64_t* lo, const uint64_t* width, int count, uint64_t a,
+                uint64_t w, int& next, double* out5) {
+    if (next >= count || lo[next] < a) return false;
+    if (lo[next] == a && width[next] == w) {
+        for (int x = 0; x < 5; ++x) out5[x] = parts[5 * next + x];
+        ++next;
+        return true;
+    }
+    if (w == 1 || lo[next] != a || width[next] > w) return false;
+    double r[5];
+    if (!fold_range(mode, parts, lo, width, count, a, w / 2, next, out5)) return false;
+    if (!fold_range(mode, parts, lo, width, count, a + w / 2, w / 2, next, r)) return false;
+    if (mode == MODE_QD) merge_words<qd>(out5, r);
+    else merge_words<dd>(out5, r);
+    return true;
+}
+}  // namespace
+
+bool fold_blocks(int mode, const double* parts, const uint64_t* lo, const uint64_t* width, int count,
+                 int class_bits, double* out5) {
+    if (count < 1 || class_bits < 0 || class_bits > 62) return false;
+    for (int i = 0; i < count; ++i)
+        if (width[i] == 0 || (width[i] & (width[i] - 1)) || lo[i] % width[i]) return false;
+    int next = 0;
+    return fold_range(mode, parts, lo, width, count, 0, 1ull << class_bits, next, out5) && next == count;
 }
 
 void fold_words(int mode, const double* parts, int count, double* out5) {

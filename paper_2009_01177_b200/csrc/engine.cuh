@@ -34,6 +34,15 @@ struct WorkRange {
     int class_bits = 0;
     uint64_t class_lo = 0;
     uint64_t class_hi = 1;
+    // one partial per class of the range (EngineOut::class_parts) instead of one folded
+    // partial: each class is an aligned subtree of the fixed fold tree, so any split of the
+    // classes across devices folds bit-identically on the host (fold_blocks)
+    bool class_partials = false;
+    // schedule (0 = default): prefix jobs of the whole problem (sets the prefix depth c and
+    // so the producer DFS depth n - c - Q0; results stay within the mode's tolerance but are
+    // bit-identical only between runs of equal prefix_jobs), subtree-kernel CTAs per SM
+    uint64_t prefix_jobs = 0;
+    int blocks_per_sm = 0;
 };
 
 // Per-instance outcome.
@@ -44,6 +53,7 @@ struct EngineOut {
     bool breakdown = false;
     uint64_t bad_mask = 0;           // reference mask convention
     int bad_row = -1;                // pair-order pivot row (2k: x_k, 2k+1: p_k)
+    std::vector<double> class_parts; // WorkRange::class_partials: 5 doubles per class
 };
 
 struct EngineStats {
@@ -75,6 +85,14 @@ int engine_run(int device, int mode, const std::vector<PreparedInput>& inputs, c
 // identical to the device reduction tree so results are bit-identical for any
 // shard count.  `parts` are `count` x 5 doubles (4 words + sum_abs).
 void fold_words(int mode, const double* parts, int count, double* out5);
+
+// Fold of partials over aligned power-of-two class blocks that tile [0, 2^class_bits):
+// block i covers classes [lo[i], lo[i] + width[i]) (sorted, width a power of two,
+// lo % width == 0).  Each block's partial is the fixed tree's subtree over its classes, so
+// folding the blocks along the same tree is bit-identical to a single-device run.
+// Returns false if the blocks do not tile the range that way.
+bool fold_blocks(int mode, const double* parts, const uint64_t* lo, const uint64_t* width, int count,
+                 int class_bits, double* out5);
 
 // Exact fixed-point validation mode (fixed.cu): the reference's per-subset algorithm on
 // the GPU; limbs4 receives the raw accumulator (identical to the reference's).

@@ -1,0 +1,73 @@
+"""Reference goldens for the deep Schur-tree paths (multi-level producer DFS, shard-width classes).
+
+Run here (where /root/reference exists and oracle/_ref/libtorfp_ref.so is built):
+
+    make -C oracle ref && python tests/golden/make_golden_deep.py
+
+Input: config 4's instance restricted to its first 30 click modes (n = 30).  The values are
+raw fixed-point class sums of the unmodified reference engine (torfp, per-mask templates of
+torontonian_partial<W>, torontonian.cpp:72-103) over prefix classes of the top k mask bits
+(bit N-1-j = mode j):
+
+  k = 12, class 0xFFF (modes 0..11 all in, 2^18 subsets, the largest determinants' subtree),
+         fixed-128 and fixed-256: with a one-job schedule the GPU runs this class as ONE job
+         with rjob = 18, i.e. 9 levels of producer DFS;
+  k = 6,  classes 0 and 0x2A (2^24 subsets each), fixed-128: shard-width classes, which the
+         default n = 30 schedule (c = 18) runs as 4096 jobs each with 3 DFS levels.
+
+Writes tests/golden/reference_deep.json.  Takes ~1.5 h on 8 cores.
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import ref  # noqa: E402
+from paper_2009_01177_b200 import matrix as M  # noqa: E402
+from paper_2009_01177_b200 import workloads as W  # noqa: E402
+
+THREADS = os.cpu_count() or 1
+OUT = os.path.join(HERE, "reference_deep.json")
+
+
+def n30():
+    return M.select_modes(W.load_config_instance(4), list(range(30)))
+
+
+def slice_case(m, k, cls, widths):
+    out = {"n": m.n_modes, "k": k, "cls": cls, "widths": {}}
+    for w in widths:
+        cfg = ref.force_width(m, w)
+        t0 = time.time()
+        tot, per, sabs = ref.slice(m, w, cfg["frac_bits"], k, cls, cls + 1, THREADS)
+        out["widths"][str(w)] = dict(frac_bits=cfg["frac_bits"], raw=str(per[0]), sum_abs=sabs[0],
+                                     seconds=round(time.time() - t0, 1), threads=THREADS)
+        print(f"  n={m.n_modes} k={k} cls={cls:#x} w={w}: {time.time() - t0:.1f}s", flush=True)
+    return out
+
+
+def main():
+    m = n30()
+    gold = {"generator": "tests/golden/make_golden_deep.py", "reference": "torfp (oracle/_ref, unmodified sources)",
+            "instance": "config 4 (tests/golden/cfg4.gbsa.txt), click modes 0..29", "cases": {}}
+    if os.path.exists(OUT):
+        gold = json.load(open(OUT))
+    C = gold["cases"]
+    todo = [("n30_k12_fff", 12, 0xFFF, (128, 256)), ("n30_k6_00", 6, 0x00, (128,)), ("n30_k6_2a", 6, 0x2A, (128,))]
+    for name, k, cls, widths in todo:
+        if name in C:
+            continue
+        C[name] = slice_case(m, k, cls, widths)
+        with open(OUT, "w") as f:
+            json.dump(gold, f, indent=1, sort_keys=True)
+    print("wrote", OUT)
+
+
+if __name__ == "__main__":
+    main()
