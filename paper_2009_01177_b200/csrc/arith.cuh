@@ -630,6 +630,8 @@ template <> struct Arith<double> {
     TOR_HD static double from(double x) { return x; }
     TOR_HD static double hi(double a) { return a; }
     TOR_HD static double norm(double a) { return a; }
+    // a double with the sign of the (possibly unnormalised) value: for sign tests
+    TOR_HD static double sign_val(double a) { return a; }
     TOR_HD static double mul(double a, double b) { return a * b; }
     TOR_HD static double rank2(double s, double a, double b, double c, double d) {
         return fma_(-c, d, fma_(-a, b, s));
@@ -656,6 +658,7 @@ template <> struct Arith<dd> {
     TOR_HD static dd from(double x) { return dd{x, 0.0}; }
     TOR_HD static double hi(const dd& a) { return a.hi; }
     TOR_HD static dd norm(const dd& a) { return dd_norm(a); }
+    TOR_HD static double sign_val(const dd& a) { return a.hi + a.lo; }
 #ifndef TOR_DD_NORMMUL
     // Products feed further products, rank updates or the accumulator, all of which use
     // both words: the final renormalisation is skipped (|lo| <= 2 ulp(hi)); values are
@@ -717,6 +720,7 @@ template <> struct Arith<qd> {
     TOR_HD static qd from(double x) { return qd{{x, 0.0, 0.0, 0.0}}; }
     TOR_HD static double hi(const qd& a) { return a.x[0]; }
     TOR_HD static qd norm(const qd& a) { return qd_renorm5_bf(a.x[0], a.x[1], a.x[2], a.x[3], 0.0); }
+    TOR_HD static double sign_val(const qd& a) { return (a.x[0] + a.x[1]) + (a.x[2] + a.x[3]); }
 #ifndef TOR_QD_UNFUSED
     TOR_HD static qd mul(const qd& a, const qd& b) { return qd_mul_fused<true>(a, b); }
 #else

@@ -628,8 +628,10 @@ template <class T> struct SubReg<T, 1> {
                                                Acc<T>& acc, E* err) {
         bool bad;
         const T tn = leaf_term<T>(S.e[0], S.e[1], S.e[2], t, bad);
-        // both pivots of the last mode: a negative-definite 2x2 block has det > 0
-        const bool bad0 = nonpositive(Arith<T>::hi(Arith<T>::unb(S.e[0])));
+        // both pivots of the last mode: a negative-definite 2x2 block has det > 0.  The state
+        // word may be unnormalised (DD grid leading word a multiple of 2^-49, lazy QD words):
+        // the sign comes from the word sum, not the leading word alone
+        const bool bad0 = nonpositive(Arith<T>::sign_val(Arith<T>::unb(S.e[0])));
         if (bad || bad0) report_breakdown(err, mask | 1ull, 2 * nsel + (bad0 ? 0 : 1));
         acc.add(tn, !neg, nsel + 1);
     }

@@ -496,3 +496,19 @@ def test_device_list_breakdown_reports_smallest_mask():
         with pytest.raises(T.BreakdownError) as e:
             T.torontonian(m, "128", devices=devs)
         assert (e.value.subset_mask, e.value.pivot_row) == (one.value.subset_mask, one.value.pivot_row), devs
+
+
+@pytest.mark.parametrize("n", [9, 10, 12])
+def test_tiny_positive_last_pivot_is_not_a_breakdown(n):
+    """Tiny positive last-mode pivots (1 - a = 2^-44: det 2^-88) are eliminated, not reported
+    as breakdowns.  The leaf's first-pivot test takes the sign of the word sum of the
+    unnormalised state entry (round-1 advisor: the biased-grid DD leading word is a multiple
+    of 2^-49, lazy QD leading words may cancel).  Diagonal A00 (closed form prod a/(1-a),
+    test_torontonian.cpp:72-77).  DD's grid states carry ~2^-100 absolute error, so a 2x2
+    block with det below that is indistinguishable from a breakdown in DD (as in fixed-128)."""
+    a = [0.1] * (n - 1) + [1.0 - 2.0 ** -44]
+    m = diag_instance(n, a)
+    want = (1.0 / 9.0) ** (n - 1) * (2.0 ** 44 - 1.0)
+    for prec in ("128", "256"):
+        r = T.torontonian(m, prec)
+        assert r["value"] == pytest.approx(want, rel=1e-9), prec
