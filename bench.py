@@ -5,10 +5,11 @@
 
 Headline (BASELINE.json metric): Torontonian subset-terms/sec, n=32, double-double, on
 config 4's input (the headline row in DD on config 4's input).  One step =
-one full Torontonian (2^32 subset-terms) evaluated on the GPU.  Under torchrun each
-rank evaluates its power-of-two share of the top-level prefix classes (strong scaling:
-total work fixed), the per-rank partial words are all-gathered over NCCL and folded in
-the engine's fixed order (bit-identical for any rank count).
+one full Torontonian (2^32 subset-terms) evaluated on the GPU.  With --gpus N > 1 (run under
+torchrun, or self-launched through torch.distributed.run when WORLD_SIZE is unset) rank r
+evaluates the top-level prefix classes [64r/N, 64(r+1)/N) of the top 6 mask bits (strong
+scaling: total work fixed; any N <= 64), the per-class partials are all-gathered over NCCL
+and every rank folds all 64 along the engine's fixed tree (bit-identical for any N).
 
 value  : terms/s with the exact R resident in HBM (tor_plan_execute), device-timed with
          CUDA events, max over ranks.
@@ -52,6 +53,59 @@ def parse():
     return ap.parse_args()
 
 
+# ------------------------------------------------------------- multi-rank ----
+KBITS = 6  # top-level prefix classes split across ranks (tor_torontonian_classes)
+
+
+def split_classes(rank: int, world: int) -> tuple[int, int]:
+    """Contiguous class range of `rank` (sizes differ by at most one class)."""
+    n = 1 << KBITS
+    if not 1 <= world <= n or not 0 <= rank < world:
+        raise SystemExit(f"bench.py: world size must be in [1, {n}] (got {world})")
+    return n * rank // world, n * (rank + 1) // world
+
+
+def gather_fold(parts: list[dict], world: int, m, dist, device=None) -> dict:
+    """All-gather this rank's per-class partials (10 doubles each, padded to the largest
+    rank's count) and fold all 2^KBITS classes along the fixed tree (tor_fold_partials,
+    host code): every rank returns the same words."""
+    import torch
+    from paper_2009_01177_b200 import api
+    import paper_2009_01177_b200 as T
+    width = (1 << KBITS) // world + 1
+    buf = torch.full((width, 10), -1.0, dtype=torch.float64)
+    for i, p in enumerate(parts):
+        buf[i] = torch.from_numpy(api.partial_to_array(p))
+    if device is not None:
+        buf = buf.to(f"cuda:{device}")
+    allb = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(allb, buf)
+    got = []
+    for b in allb:
+        for row in b.cpu().numpy():
+            if row[3] >= 0:  # class_hi of a real record (padding rows are -1)
+                got.append(api.array_to_partial(row))
+    return T.fold_partials(sorted(got, key=lambda p: p["class_lo"]), m)
+
+
+def self_launch(args) -> int:
+    """--gpus N > 1 without torchrun: relaunch this script as N NCCL ranks (the driver's own
+    launch form); refuse (exit 2) when the node has fewer than N GPUs."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} requested but {have} CUDA device(s) visible"}), flush=True)
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 WORKLOADS = {
     "cfg4-n32-dd": (4, "128", "dd"),
     "cfg4-n32-qd": (4, "256", "qd"),
@@ -59,6 +113,7 @@ WORKLOADS = {
     "cfg1-n16-fp64": (1, "fp64", "fp64"),
     "cfg5-n40-dd": (5, "128", "dd"),
 }
+DATA = "synthetic (seeded pure Gaussian state, SURVEY 8(d) recipe; committed input tests/golden/cfg{}.gbsa.txt)"
 
 
 # ------------------------------------------------------------------ clocks --
@@ -162,9 +217,13 @@ def ref_sample(m, precision: str, seconds: float):
 def main():
     args = parse()
     cfg, prec, dtype = WORKLOADS[args.workload]
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "engine":
+        sys.exit(self_launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "engine" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     from paper_2009_01177_b200 import workloads as W
     m = W.load_config_instance(cfg)
@@ -180,10 +239,14 @@ def main():
             if s >= args.warmup:
                 vals.append(r["value"])
         v = statistics.median(vals)
-        line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        line = {"metric": METRIC if args.workload == "cfg4-n32-dd" else f"Torontonian subset-terms/sec ({args.workload})",
+                "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": terms_total / v * 1e3, "higher_is_better": True,
+                "ms_per_step_note": "derived, not timed: 2^n / value -- each step times a bounded sample "
+                                    "(cpu_baseline.sample) of the same Torontonian, the full sum would take "
+                                    f"{terms_total / v / 3600:.0f} h on these cores",
                 "scaling": "strong", "vs_baseline": None, "dtype": "fixed-128" if dtype == "dd" else dtype,
-                "data": "synthetic (seeded pure Gaussian state, tests/golden)", "impl": "reference",
+                "data": DATA.format(cfg), "impl": "reference",
                 "config": {"workload": args.workload, "n": n, "precision": prec},
                 "cpu_baseline": dict(r, value=v),
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -199,12 +262,12 @@ def main():
         dist.init_process_group("nccl", init_method="env://")
     device = local if world > 1 else 0
     torch.cuda.set_device(device)
-    if world & (world - 1):
-        raise SystemExit("world size must be a power of two")
-    k = world.bit_length() - 1
-
-    # resident-input plan for this rank's share
-    plan = T.api.Plan(m, prec, k, rank, rank + 1, device=device)
+    # resident-input plan for this rank's share of the top-level prefix classes
+    if world > 1:
+        k, (clo, chi) = KBITS, split_classes(rank, world)
+    else:
+        k, clo, chi = 0, 0, 1
+    plan = T.api.Plan(m, prec, k, clo, chi, device=device)
     flush = torch.empty(64 << 20, dtype=torch.int32, device=f"cuda:{device}")  # 256 MiB > 126 MB L2
 
     def barrier():
@@ -244,12 +307,8 @@ def main():
         barrier()
         t0 = time.perf_counter()
         if world > 1:
-            p = T.torontonian_shard(m, prec, rank, world, device=device)
-            buf = torch.tensor(T.api.partial_to_array(p), device=f"cuda:{device}")
-            allb = [torch.empty_like(buf) for _ in range(world)]
-            dist.all_gather(allb, buf)
-            parts_l = [T.api.array_to_partial(x.cpu().numpy()) for x in allb]
-            result = T.fold_partials(parts_l, m)
+            mine = T.torontonian_classes(m, prec, KBITS, clo, chi, device=device)
+            result = gather_fold(mine, world, m, dist, device)
         else:
             result = T.torontonian(m, prec)
         barrier()
@@ -262,15 +321,17 @@ def main():
             e2e_ms.append(dt)
     e2e_step = statistics.median(e2e_ms)
     # bytes moved per step, all ranks: each rank uploads the exact R (the single-device
-    # call reports its own counts) and reads back its partial; with N > 1 each rank also
-    # uploads its 10-double partial for the all-gather and reads the N gathered ones back
+    # call reports its own counts) and reads back its class partials (5 doubles each + the
+    # error word); with N > 1 each rank also uploads its padded partial records for the
+    # all-gather and reads the N gathered blocks back
     words = {"fp64": 1, "dd": 2, "qd": 4}[dtype]
     r_bytes = (2 * n) * (2 * n + 1) // 2 * words * 8
     if world == 1:
         h2d_step, d2h_step = int(result.get("h2d_bytes", r_bytes)), int(result.get("d2h_bytes", 48))
     else:
-        h2d_step = world * (r_bytes + 80)
-        d2h_step = world * (48 + world * 80)
+        rec = ((1 << KBITS) // world + 1) * 80
+        h2d_step = world * (r_bytes + rec)
+        d2h_step = (1 << KBITS) * 40 + world * 8 + world * world * rec
 
     if rank == 0:
         def _load(name):
@@ -282,7 +343,8 @@ def main():
         ipt = fmodel.get("fp64_instr")
         roof = None
         if fpt and peak:
-            terms_rank = terms_total / world
+            # the most loaded rank bounds the max-over-ranks kernel time
+            terms_rank = terms_total * (-(-(1 << KBITS) // world) if world > 1 else 1) / ((1 << KBITS) if world > 1 else 1)
             achieved = terms_rank * fpt / (kstep_ms * 1e-3) / 1e12
             roof = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": sass.get("dram_bytes_per_launch", {}).get(dtype),
@@ -312,9 +374,10 @@ def main():
             "metric": METRIC if args.workload == "cfg4-n32-dd" else f"Torontonian subset-terms/sec ({args.workload})",
             "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": dtype, "data": "synthetic (seeded pure Gaussian state, committed tests/golden/cfg4.gbsa.txt)",
+            "dtype": dtype, "data": DATA.format(cfg),
             "config": {"workload": args.workload, "n": n, "precision": prec, "terms_per_step": terms_total,
-                       "l2": "flushed between steps (256 MiB write)", "prefix_classes_per_rank": f"2^{k} split",
+                       "l2": "flushed between steps (256 MiB write)",
+                       "prefix_classes_per_rank": f"{chi - clo} of 2^{k}" if world > 1 else "all",
                        "parallelism": f"prefix-class shards x{world}"},
             "e2e": {"value": terms_total / (e2e_step * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": h2d_step, "d2h_bytes_per_step": d2h_step, "ms_per_step": e2e_step},
