@@ -254,6 +254,22 @@ int tor_plan_create(const tor_input* in, tor_precision prec, int class_bits, uin
 int tor_plan_execute(tor_plan* plan, tor_result* out, tor_error* err);
 void tor_plan_destroy(tor_plan* plan);
 
+/* GBSA instance files (load_matrix_file / save_matrix, matrix_io.cpp:109-263; SURVEY 8(f)
+ * rank 3).  Binary: "GBSA", u16 version 1, u32 N, u8 bits (16/32), then the A00 and A01 upper
+ * triangles as (re, im) signed little-endian integers x 2^-(bits-1).  Text: "GBSA text 1",
+ * "modes N", one "re im" line per entry.  tor_load_matrix sniffs the format from the magic
+ * as the reference does; *n (and *quant_bits: 16/32 binary, 0 text) are always set, and the
+ * triangles are written when both pointers are non-NULL (capacity >= N(N+1)/2 complex
+ * entries; call once with NULL to size).  Parse errors: TOR_E_PARSE with the reference's
+ * codes ("matrixio/magic|version|format|dim|truncated|entry|range") and the position (byte
+ * offset / 1-based line) in err->pivot_row.  tor_save_matrix: format 0 text, 1 binary
+ * (quant_bits 16/32, entries must satisfy |x| < 1); *len = the full size, min(len, capacity)
+ * bytes are copied to buf (buf may be NULL). */
+int tor_load_matrix(const void* bytes, size_t len, int* n, int* quant_bits, double* a00_upper, double* a01_upper,
+                    size_t capacity, tor_error* err);
+int tor_save_matrix(const tor_input* in, int format, int quant_bits, void* buf, size_t capacity, size_t* len,
+                    tor_error* err);
+
 /* Number of CUDA devices visible (0 without a GPU). */
 int tor_device_count(void);
 

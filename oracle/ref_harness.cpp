@@ -18,6 +18,10 @@
 //                                 (torontonian.hpp:36-38, linalg.hpp:67, fixed_point.hpp:178)
 //                                 over the masks of prefix classes, i.e. exactly the
 //                                 per-mask body of torontonian_partial (torontonian.cpp:83-96)
+//   ref_save_matrix            -> torfp::save_matrix            (matrix_io.cpp:109)
+//   ref_load_matrix            -> torfp::load_matrix_file       (matrix_io.cpp:253; the bytes
+//                                 go through a temporary file so the reference's own format
+//                                 sniffing is used)
 //   ref_partial_sample         -> torfp::torontonian_partial<W> over partition(N, rank, P)
 //                                 (torontonian.cpp:72, subsets.cpp:66), threaded; the
 //                                 bounded CPU-baseline sample of bench.py
@@ -28,7 +32,9 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <fstream>
 #include <string>
+#include <unistd.h>
 #include <thread>
 #include <vector>
 
@@ -77,6 +83,7 @@ int report(const ErrOut& e) {
     } catch (const ParseError& x) {
         put(e.code, e.code_len, x.code());
         put(e.msg, e.msg_len, x.what());
+        if (e.row) *e.row = static_cast<std::int64_t>(x.position());
         return 4;
     } catch (const ResourceError& x) {
         put(e.code, e.code_len, x.code());
@@ -447,6 +454,59 @@ int ref_total_op_count(int n, std::uint64_t* lo, std::uint64_t* hi, ERR_ARGS) {
         *hi = static_cast<std::uint64_t>(v >> 64);
         return 0;
     } catch (...) {
+        return report(e);
+    }
+}
+
+// binary: 0 text, 1 binary (bits 16/32).  *len = full size; copies min(len, cap) bytes.
+int ref_save_matrix(int n, const double* a00, const double* a01, int binary, int bits, unsigned char* buf,
+                    std::size_t cap, std::size_t* len, ERR_ARGS) {
+    ERR_INIT;
+    try {
+        const InputMatrix m = make_input(n, a00, a01);
+        const auto b = save_matrix(m, binary ? MatrixFormat::Binary : MatrixFormat::Text, bits);
+        *len = b.size();
+        if (buf) std::memcpy(buf, b.data(), std::min(cap, b.size()));
+        return 0;
+    } catch (...) {
+        return report(e);
+    }
+}
+
+// bytes -> load_matrix_file (format sniffed by the reference); triangles copied when
+// cap >= n(n+1)/2 entries.
+int ref_load_matrix(const unsigned char* bytes, std::size_t len, int* n, int* bits, double* a00, double* a01,
+                    std::size_t cap, ERR_ARGS) {
+    ERR_INIT;
+    char path[] = "/tmp/ref_gbsa_XXXXXX";
+    const int fd = mkstemp(path);
+    if (fd < 0) {
+        put(code, code_len, "harness/tmp");
+        return 8;
+    }
+    if (len && write(fd, bytes, len) != static_cast<ssize_t>(len)) {
+        close(fd);
+        unlink(path);
+        put(code, code_len, "harness/tmp");
+        return 8;
+    }
+    close(fd);
+    try {
+        const InputMatrix m = load_matrix_file(path);
+        unlink(path);
+        *n = m.n_modes;
+        *bits = m.quant_bits;
+        if (a00 && a01 && cap >= m.a00.size()) {
+            for (std::size_t i = 0; i < m.a00.size(); ++i) {
+                a00[2 * i] = m.a00[i].real();
+                a00[2 * i + 1] = m.a00[i].imag();
+                a01[2 * i] = m.a01[i].real();
+                a01[2 * i + 1] = m.a01[i].imag();
+            }
+        }
+        return 0;
+    } catch (...) {
+        unlink(path);
         return report(e);
     }
 }

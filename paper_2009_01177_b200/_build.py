@@ -69,12 +69,14 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
          os.path.join(BUILD, "host.log")),
         (["g++"] + CXX_FLAGS + inc + ["-c", os.path.join(CSRC, "capi.cpp"), "-o", os.path.join(BUILD, "capi.o")],
          os.path.join(BUILD, "capi.log")),
+        (["g++"] + CXX_FLAGS + inc + ["-c", os.path.join(CSRC, "gbsa.cpp"), "-o", os.path.join(BUILD, "gbsa.o")],
+         os.path.join(BUILD, "gbsa.log")),
     ]
     with ThreadPoolExecutor(len(jobs)) as ex:
         list(ex.map(lambda j: _run(*j), jobs))
     tmp = lib_path + ".tmp"
     _run([nvcc] + ARCH + ["-shared", "-o", tmp, os.path.join(BUILD, "engine.o"), os.path.join(BUILD, "fixed.o"),
-                          os.path.join(BUILD, "host.o"),
+                          os.path.join(BUILD, "host.o"), os.path.join(BUILD, "gbsa.o"),
                           os.path.join(BUILD, "capi.o"), "-lcudart_static", "-lrt", "-lpthread", "-ldl"],
          os.path.join(BUILD, "link.log"))
     os.replace(tmp, lib_path)

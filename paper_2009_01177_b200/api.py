@@ -68,7 +68,7 @@ EXPORTS = ("tor_abi_version", "tor_check_symmetries", "tor_check_dense", "tor_de
            "tor_torontonian_batch", "tor_torontonian_slice", "tor_torontonian_classes", "tor_torontonian_shard",
            "tor_fold_partials",
            "tor_probability", "tor_probability_modes", "tor_device_count", "tor_plan_create", "tor_plan_execute", "tor_plan_destroy",
-           "tor_release_device_cache")
+           "tor_release_device_cache", "tor_load_matrix", "tor_save_matrix")
 
 _lib = None
 
@@ -106,6 +106,10 @@ def lib():
         L.tor_plan_execute.argtypes = [C.c_void_p, P(TorResult), P(TorError)]
         L.tor_plan_destroy.argtypes = [C.c_void_p]
         L.tor_plan_destroy.restype = None
+        L.tor_load_matrix.argtypes = [C.c_char_p, C.c_size_t, P(C.c_int), P(C.c_int), P(C.c_double),
+                                      P(C.c_double), C.c_size_t, P(TorError)]
+        L.tor_save_matrix.argtypes = [P(TorInput), C.c_int, C.c_int, C.c_char_p, C.c_size_t, P(C.c_size_t),
+                                      P(TorError)]
         L.tor_release_device_cache.argtypes = []
         L.tor_release_device_cache.restype = None
         _lib = L
@@ -373,3 +377,33 @@ def device_count() -> int:
 def release_device_cache() -> None:
     """Free the device memory pooled between calls (tor_release_device_cache)."""
     lib().tor_release_device_cache()
+
+
+def load_matrix_bytes(b: bytes) -> InputMatrix:
+    """GBSA bytes -> InputMatrix through tor_load_matrix (load_matrix_file's format sniffing,
+    matrix_io.cpp:253-263)."""
+    b = bytes(b)
+    n, qb = C.c_int(), C.c_int()
+    err = TorError()
+    _check(lib().tor_load_matrix(b, len(b), C.byref(n), C.byref(qb), None, None, 0, C.byref(err)), err)
+    t = n.value * (n.value + 1) // 2
+    a00 = np.zeros(2 * t)
+    a01 = np.zeros(2 * t)
+    P = C.POINTER(C.c_double)
+    _check(lib().tor_load_matrix(b, len(b), C.byref(n), C.byref(qb), a00.ctypes.data_as(P), a01.ctypes.data_as(P), t,
+                                 C.byref(err)), err)
+    return InputMatrix(n.value, a00.view(np.complex128), a01.view(np.complex128), quant_bits=qb.value)
+
+
+def save_matrix_bytes(matrix: InputMatrix, format: str = "text", quant_bits: int = 16) -> bytes:
+    """InputMatrix -> GBSA bytes through tor_save_matrix (save_matrix, matrix_io.cpp:109-143)."""
+    if format not in ("text", "binary"):
+        raise E.InvalidArgument("matrixio/format", "format must be 'text' or 'binary'")
+    inp = _In(matrix)
+    size = C.c_size_t()
+    err = TorError()
+    fmt = 1 if format == "binary" else 0
+    _check(lib().tor_save_matrix(C.byref(inp.s), fmt, quant_bits, None, 0, C.byref(size), C.byref(err)), err)
+    buf = C.create_string_buffer(size.value)
+    _check(lib().tor_save_matrix(C.byref(inp.s), fmt, quant_bits, buf, size.value, C.byref(size), C.byref(err)), err)
+    return buf.raw[: size.value]

@@ -883,4 +883,46 @@ int tor_probability_modes(const tor_input* full, const int* modes, int nmodes, t
     }
 }
 
+int tor_load_matrix(const void* bytes, size_t len, int* n, int* quant_bits, double* a00_upper, double* a01_upper,
+                    size_t capacity, tor_error* err) {
+    try {
+        clear_err(err);
+        if (!bytes && len) throw HostError(TOR_E_INVALID, "matrixio/io", "null buffer");
+        if (!n) throw HostError(TOR_E_INVALID, "matrixio/io", "null output");
+        int qb = 0;
+        const Input a = load_gbsa(static_cast<const uint8_t*>(bytes), len, &qb);
+        *n = a.n;
+        if (quant_bits) *quant_bits = qb;
+        if (a00_upper && a01_upper) {
+            if (capacity < a.a00.size())
+                throw HostError(TOR_E_INVALID, "matrixio/dim", "output triangles smaller than N(N+1)/2 entries");
+            for (size_t i = 0; i < a.a00.size(); ++i) {
+                a00_upper[2 * i] = a.a00[i].real();
+                a00_upper[2 * i + 1] = a.a00[i].imag();
+                a01_upper[2 * i] = a.a01[i].real();
+                a01_upper[2 * i + 1] = a.a01[i].imag();
+            }
+        }
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
+int tor_save_matrix(const tor_input* in, int format, int quant_bits, void* buf, size_t capacity, size_t* len,
+                    tor_error* err) {
+    try {
+        clear_err(err);
+        if (!in || in->n < 1 || !in->a00_upper || !in->a01_upper)
+            throw HostError(TOR_E_INVALID, "matrixio/dim", "matrix has no modes");
+        if (format != 0 && format != 1) throw HostError(TOR_E_INVALID, "matrixio/format", "format: 0 text, 1 binary");
+        const std::string s = save_gbsa(make_input(in->n, in->a00_upper, in->a01_upper), format == 1, quant_bits);
+        if (len) *len = s.size();
+        if (buf) std::memcpy(buf, s.data(), std::min(capacity, s.size()));
+        return TOR_OK;
+    } catch (const HostError& h) {
+        return fail(err, h);
+    }
+}
+
 }  // extern "C"

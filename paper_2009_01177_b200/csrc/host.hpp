@@ -59,4 +59,11 @@ unsigned __int128 total_op_count(int n);
 Input extract_submatrix(const Input& full, uint64_t pattern_bits);
 Input extract_modes(const Input& full, const std::vector<int>& ascending_modes);
 
+// GBSA instance files (gbsa.cpp; matrix_io.cpp:92-263): format sniffed from the magic on
+// load (*quant_bits = 16/32 for binary, 0 for text); save as text or binary (16/32 bits).
+Input load_gbsa(const uint8_t* bytes, size_t len, int* quant_bits);
+std::string save_gbsa(const Input& a, bool binary, int quant_bits);
+int64_t quantize(double x, int bits);
+double quant_unit(int bits);
+
 }  // namespace tor

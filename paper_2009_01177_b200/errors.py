@@ -81,4 +81,6 @@ def raise_for_status(status: int, code: str, message: str, pivot_row: int = -1,
         return
     if status == TOR_E_BREAKDOWN:
         raise BreakdownError(code, message, pivot_row, subset_mask)
+    if status == TOR_E_PARSE:  # the C ABI reports ParseError::position() in pivot_row
+        raise ParseError(code, message, max(pivot_row, 0))
     raise _BY_STATUS.get(status, TorfpError)(code, message)

@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .errors import InvalidArgument, ParseError, TorfpError
+from .errors import InvalidArgument, TorfpError
 
 SYMMETRY_TOL = 1e-12  # matrix_io.hpp:62
 
@@ -151,7 +151,6 @@ def select_modes(a: InputMatrix, sel) -> InputMatrix:
 
 
 # ----------------------------------------------------------------- formats --
-_TEXT_MAGIC = "GBSA text 1"
 
 
 def quantize(x: float, bits: int) -> int:
@@ -174,29 +173,16 @@ def dequantize(q: int, bits: int) -> float:
 
 
 def save_matrix(a: InputMatrix, format: str = "text", quant_bits: int = 16) -> bytes:
-    if format == "text":
-        lines = [_TEXT_MAGIC, f"modes {a.n_modes}"]
-        for tri in (a.a00, a.a01):
-            for v in tri:
-                lines.append(f"{v.real:.17g} {v.imag:.17g}")
-        return ("\n".join(lines) + "\n").encode()
-    if quant_bits not in (16, 32):
-        raise InvalidArgument("matrixio/bits", "binary format stores 16- or 32-bit entries")
-    out = bytearray(b"GBSA")
-    out += (1).to_bytes(2, "little") + int(a.n_modes).to_bytes(4, "little") + bytes([quant_bits])
-    nb = quant_bits // 8
-    for tri in (a.a00, a.a01):
-        for v in tri:
-            for x in (v.real, v.imag):
-                out += int(quantize(float(x), quant_bits)).to_bytes(nb, "little", signed=True)
-    return bytes(out)
+    """save_matrix (matrix_io.cpp:109-143) through the C ABI (tor_save_matrix)."""
+    from .api import save_matrix_bytes
+    return save_matrix_bytes(a, format, quant_bits)
 
 
 def load_matrix_bytes(b: bytes) -> InputMatrix:
-    """Format sniffed from the magic (matrix_io.cpp:254-263)."""
-    if len(b) >= 4 and b[:4] == b"GBSA" and not (len(b) >= 5 and b[4:5] == b" "):
-        return _load_binary(b)
-    return _load_text(b)
+    """Format sniffed from the magic (matrix_io.cpp:253-263), through the C ABI
+    (tor_load_matrix)."""
+    from .api import load_matrix_bytes as _load
+    return _load(b)
 
 
 def load_matrix(path: str) -> InputMatrix:
@@ -204,57 +190,3 @@ def load_matrix(path: str) -> InputMatrix:
         raise TorfpError("matrixio/io", f"cannot open for reading: {path}")
     with open(path, "rb") as f:
         return load_matrix_bytes(f.read())
-
-
-def _load_binary(b: bytes) -> InputMatrix:
-    if len(b) < 6:
-        raise ParseError("matrixio/truncated", "file ends inside the version field", 4)
-    if int.from_bytes(b[4:6], "little") != 1:
-        raise ParseError("matrixio/version", "unsupported format version", 4)
-    if len(b) < 11:
-        raise ParseError("matrixio/truncated", "file ends inside the header", len(b))
-    n = int.from_bytes(b[6:10], "little")
-    bits = b[10]
-    if bits not in (16, 32):
-        raise ParseError("matrixio/format", "entry width must be 16 or 32 bits", 10)
-    if n < 1 or n > 4096:
-        raise ParseError("matrixio/dim", "mode count out of range", 6)
-    t = tri_size(n)
-    nb = bits // 8
-    need = 11 + t * 4 * nb
-    if len(b) < need:
-        raise ParseError("matrixio/truncated", "file ends inside the entry data", len(b))
-    raw = np.frombuffer(b[11:need], dtype=np.dtype(f"<i{nb}")).astype(np.float64)
-    vals = raw * math.ldexp(1.0, -(bits - 1))
-    c = vals[0::2] + 1j * vals[1::2]
-    return InputMatrix(n, c[:t], c[t:2 * t], quant_bits=bits)
-
-
-def _load_text(b: bytes) -> InputMatrix:
-    lines = [ln.rstrip("\r") for ln in b.decode().split("\n")]
-    lines = [(i + 1, ln) for i, ln in enumerate(lines) if ln]
-    if not lines or lines[0][1] != _TEXT_MAGIC:
-        raise ParseError("matrixio/magic", "first line must be 'GBSA text 1'", 1)
-    if len(lines) < 2:
-        raise ParseError("matrixio/truncated", "missing 'modes N' line", 2)
-    parts = lines[1][1].split()
-    if len(parts) != 2 or parts[0] != "modes" or not parts[1].isdigit() or not 1 <= int(parts[1]) <= 4096:
-        raise ParseError("matrixio/dim", "expected 'modes N' with 1 <= N <= 4096", lines[1][0])
-    n = int(parts[1])
-    t = tri_size(n)
-    body = lines[2:]
-    if len(body) < 2 * t:
-        raise ParseError("matrixio/truncated", "file ends inside the entry list",
-                         (body[-1][0] + 1) if body else lines[1][0] + 1)
-    vals = np.empty(2 * t, dtype=np.complex128)
-    for k in range(2 * t):
-        ln, s = body[k]
-        p = s.split()
-        try:
-            re, im = float(p[0]), float(p[1])
-        except (ValueError, IndexError):
-            raise ParseError("matrixio/entry", "expected 're im' pair", ln) from None
-        if not (abs(re) < 1.0 and abs(im) < 1.0):
-            raise ParseError("matrixio/range", "entry magnitudes must be < 1", ln)
-        vals[k] = complex(re, im)
-    return InputMatrix(n, vals[:t], vals[t:])
