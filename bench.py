@@ -177,13 +177,14 @@ def fp64_peak_tflops(device: int):
             out = subprocess.run([exe], capture_output=True, text=True, timeout=60,
                                  env=dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "")))
             d = json.loads(out.stdout.strip().splitlines()[-1])
-            return d["dfma_tflops"], "measured: tools/fp64_peak DFMA microbenchmark (burst, this box)"
+            return d["dfma_tflops"], ("measured: tools/fp64_peak DFMA microbenchmark (best of 8-32 independent "
+                                      "chains x 4/8 CTAs per SM, this box)")
         except Exception as e:  # pragma: no cover
             why = f"fp64_peak failed: {e}"
     # fallback: the committed measurement of the same microbenchmark on this pool's B200s
-    rec = os.path.join(ROOT, "profiles", "r01_fp64_peak.json")
+    rec = os.path.join(ROOT, "profiles", "r02_fp64_peak.json")
     if os.path.exists(rec):
-        return json.load(open(rec))["dfma_tflops"], f"recorded: profiles/r01_fp64_peak.json ({why})"
+        return json.load(open(rec))["dfma_tflops"], f"recorded: profiles/r02_fp64_peak.json ({why})"
     return None, why
 
 
@@ -353,6 +354,13 @@ def main():
                                              "primitive costs (tools/flops_model.py), useful work only",
                     "kappa": fmodel.get("kappa"), "rho": fmodel.get("rho_leaf_bundle_flops"),
                     "peak_source": peak_src}
+            # nominal 64 DFMA/clk/SM x SMs x max clock x 2 flops (the microbenchmark sustains
+            # ~58.5/clk/SM at any chain count: profiles/r02_fp64_peak.json)
+            import torch
+            sms = torch.cuda.get_device_properties(device).multi_processor_count
+            mhz = clk.summary().get("sm_max_mhz") or 1965
+            roof["peak_nominal"] = 2 * 64 * sms * mhz * 1e6 / 1e12
+            roof["frac_nominal"] = achieved / roof["peak_nominal"]
             if ipt:
                 # FP64 pipe issue utilisation: DD arithmetic is DADD-heavy, so the flop
                 # fraction caps well below 1 even at a saturated pipe (peak = 2 flops/instr)
