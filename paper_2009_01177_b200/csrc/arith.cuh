@@ -20,15 +20,12 @@
 #if defined(__CUDACC__)
 #define TOR_UNROLL _Pragma("unroll")
 #define TOR_HD __host__ __device__ __forceinline__
-// large QD routines: inline by default (measured faster than out-of-line calls even
-// though the QD kernel's SASS is ~60K instructions); -DTOR_QD_NOINLINE for experiments
-#ifdef TOR_QD_NOINLINE
-#define TOR_HD_NI __host__ __device__ __noinline__
-#else
+// large QD routines: inline (measured faster than out-of-line calls even though the QD
+// kernel's SASS is ~60K instructions)
 #define TOR_HD_NI TOR_HD
-#endif
 // QD rank-1/rank-2 entry updates as out-of-line calls (one copy each): measured
-// 407 -> 352 ms at n=28 QD (instruction-cache bound kernel); -DTOR_QD_RANK_INLINE to undo
+// 407 -> 352 ms at n=28 QD (instruction-cache bound kernel); -DTOR_QD_RANK_INLINE inlines
+// them (used only by the arithmetic probes of tools/probes/prims.cu, which count the bodies)
 #ifndef TOR_QD_RANK_INLINE
 #define TOR_HD_RNI __host__ __device__ __noinline__
 #else
@@ -88,26 +85,13 @@ TOR_HD double rsqrt_seed(double x) {
 // Two fp64 Newton steps from the seed y ~ 1/sqrt(x) -> ~1 ulp.  The seed may come from
 // an approximation of x (e.g. an unnormalised leading word): the steps converge to
 // 1/sqrt(x) for any seed within a few 2^-20 of it.
-#ifndef TOR_RSQRT_HOUSEHOLDER
-#define TOR_RSQRT_HOUSEHOLDER 1
-#endif
 TOR_HD double rsqrt_newton(double x, double y) {
-#if TOR_RSQRT_HOUSEHOLDER
     // one third-order step y (1 + r/2 + 3 r^2 / 8), r = 1 - x y^2: from a 2^-20 seed the
     // truncation error is ~(5/16) r^3 < 2^-58, i.e. the result is fp64-rounding-limited
     // (~1 ulp) after 4 dependent operations instead of 6 for two Newton steps
     const double r = fma_(-x, y * y, 1.0);
     const double p = fma_(0.375, r, 0.5);
     return fma_(y * r, p, y);
-#else
-    double h = x * y;
-    double r = fma_(-h, y, 1.0);
-    y = fma_(0.5 * y, r, y);
-    h = x * y;
-    r = fma_(-h, y, 1.0);
-    y = fma_(0.5 * y, r, y);
-    return y;
-#endif
 }
 // Full-precision fp64 reciprocal square root for x > 0.
 TOR_HD double rsqrt_d(double x) { return rsqrt_newton(x, rsqrt_seed(x)); }
@@ -265,19 +249,7 @@ TOR_HD dd dd_det2(const dd& a, const dd& b, const dd& c, double& h) {
     two_sum(p, -q, h, he);
     double t = fma_(a.hi, c.lo, a.lo * c.hi);
     t = fma_(-2.0 * b.hi, b.lo, t);
-#ifndef TOR_DET2_LOLO
-#define TOR_DET2_LOLO 0
-#endif
-#if TOR_DET2_LOLO == 1
-    // grid state entries are un-normalised (|lo| up to 2^-50 absolute): the low*low
-    // products are <= 2^-100 of the O(1) state scale, the order of the grid updates' own
-    // rounding; keeping them cost 1.2 ms of 90.5 at n=32 (register pressure), so off
-    // (a separate short chain, joined at the end)
-    const double t2 = fma_(a.lo, c.lo, -(b.lo * b.lo));
-    const double lo = (he + (pe - qe)) + (t + t2);
-#else
     const double lo = (he + (pe - qe)) + t;
-#endif
     dd r;
     fast_two_sum(h, lo, r.hi, r.lo);
     return r;
@@ -321,19 +293,12 @@ TOR_HD qd qd_renorm5_bf(double c0, double c1, double c2, double c3, double c4) {
 // of that scale, which is all the order-collected operations that consume them assume; the
 // full two-pass renormalisation is kept where a value must be normalised relative to ITSELF
 // (pivots, determinants, the rsqrt residual).
-#ifndef TOR_QD_LEAD_RENORM
-#define TOR_QD_LEAD_RENORM 1
-#endif
 TOR_HD qd qd_renorm_lead(double h0, double h1, double h2, double h3) {
-#if TOR_QD_LEAD_RENORM
     double s0, e1, s1, e2, s2, s3;
     two_sum(h0, h1, s0, e1);
     two_sum(e1, h2, s1, e2);
     two_sum(e2, h3, s2, s3);
     return qd{{s0, s1, s2, s3}};
-#else
-    return qd_renorm5_bf(h0, h1, h2, h3, 0.0);
-#endif
 }
 TOR_HD void three_sum(double& a, double& b, double& c) {
     double t1, t2, t3;
@@ -410,10 +375,7 @@ TOR_HD qd qd_mul_d(const qd& a, double b) {
 // order 0..2 products by TwoProd, order 3 plainly; each order is summed exactly with
 // TwoSums whose errors drop to the next order; order 3 is summed plainly.  Error
 // ~2^-208 of max(|s|, |ab|, |cd|) (tests/test_arith.py).
-#ifndef TOR_QD_LAZY
-#define TOR_QD_LAZY 1
-#endif
-constexpr bool kQdLazy = TOR_QD_LAZY;
+constexpr bool kQdLazy = true;
 // Exact pairwise (tree) sum of N doubles: the rounded total, and the N - 1 TwoSum errors
 // in a fixed order.  ceil(log2 N) dependent TwoSums instead of N - 1 for a running sum --
 // the QD kernel runs one warp per SM sub-partition, so its time is these chains.
@@ -444,11 +406,7 @@ TOR_HD double tree_add(const double (&t)[N]) {
         return tree_add<N - H>(u);
     }
 }
-#ifndef TOR_QD_R2_INLINE
 #define TOR_HD_R2 TOR_HD_RNI
-#else
-#define TOR_HD_R2 TOR_HD
-#endif
 template <bool kNorm>
 TOR_HD qd qd_rank2_body(const qd& s, const qd& a, const qd& b, const qd& c, const qd& d) {
     double p0, e0, q0, f0;
@@ -556,21 +514,12 @@ TOR_HD_RNI qd qd_mul_fused(qd a, qd b) {
 // ABSOLUTE scale 2^-53k keep the fused algorithm's error at ~2^-208 of that scale even
 // when the leading word has cancelled; entries are renormalised where they become
 // pivots, and the products that consume them renormalise their results.
-#ifndef TOR_QD_UNFUSED
 // (thin inline wrappers: one out-of-line call per update, to the fused body)
 TOR_HD qd qd_rank2(const qd& s, const qd& a, const qd& b, const qd& c, const qd& d) {
     return qd_rank2_fused<!kQdLazy>(s, a, b, c, d);
 }
 TOR_HD qd qd_rank1(const qd& s, const qd& a, const qd& b) { return qd_rank1_fused<true>(s, a, b); }
 TOR_HD qd qd_rank1_lazy(const qd& s, const qd& a, const qd& b) { return qd_rank1_fused<!kQdLazy>(s, a, b); }
-#else
-// s - a*b - c*d.
-TOR_HD_RNI qd qd_rank2(qd s, qd a, qd b, qd c, qd d) {
-    return qd_sub(qd_sub(s, qd_mul(a, b)), qd_mul(c, d));
-}
-TOR_HD_RNI qd qd_rank1(qd s, qd a, qd b) { return qd_sub(s, qd_mul(a, b)); }
-TOR_HD_RNI qd qd_rank1_lazy(qd s, qd a, qd b) { return qd_sub(s, qd_mul(a, b)); }
-#endif
 
 // 1/sqrt(x), x > 0 normalised: DD value y = (y0, y1) (~2^-104), then one Newton step
 // y + y e / 2 with e = 1 - x y^2 by the fused rank-1 (y^2 formed exactly enough from
@@ -613,11 +562,7 @@ TOR_HD_NI qd qd_rsqrt_slow(qd x) {
     return qd_add(y, corr);
 }
 
-#ifndef TOR_QD_SLOW_RSQRT
 TOR_HD qd qd_rsqrt(const qd& x) { return qd_rsqrt_fast(x); }
-#else
-TOR_HD qd qd_rsqrt(const qd& x) { return qd_rsqrt_slow(x); }
-#endif
 
 // ================================================================ traits ==
 // Uniform interface used by the kernels.  Word type W, number of doubles K.
@@ -659,7 +604,6 @@ template <> struct Arith<dd> {
     TOR_HD static double hi(const dd& a) { return a.hi; }
     TOR_HD static dd norm(const dd& a) { return dd_norm(a); }
     TOR_HD static double sign_val(const dd& a) { return a.hi + a.lo; }
-#ifndef TOR_DD_NORMMUL
     // Products feed further products, rank updates or the accumulator, all of which use
     // both words: the final renormalisation is skipped (|lo| <= 2 ulp(hi)); values are
     // renormalised explicitly where it matters (pivots before rsqrt).
@@ -670,10 +614,6 @@ template <> struct Arith<dd> {
         e = fma_(a.lo, b.hi, e);
         return dd{p, e};
     }
-#else
-    TOR_HD static dd mul(const dd& a, const dd& b) { return dd_mul(a, b); }
-#endif
-#ifndef TOR_DD_NOGRID
     static constexpr bool kGrid = true;
     // Schur-state updates: fixed-exponent (grid) DD
     TOR_HD static dd rank2(const dd& s, const dd& a, const dd& b, const dd& c, const dd& d) {
@@ -687,19 +627,6 @@ template <> struct Arith<dd> {
         w = mul(rank1s(s1, u1, uu), r2);
         u = uu;
     }
-#else
-    static constexpr bool kGrid = false;
-    TOR_HD static dd rank2(const dd& s, const dd& a, const dd& b, const dd& c, const dd& d) {
-        return dd_rank2(s, a, b, c, d);
-    }
-    TOR_HD static dd rank1s(const dd& s, const dd& a, const dd& b) { return dd_rank1(s, a, b); }
-    TOR_HD static dd unb(const dd& a) { return a; }
-    TOR_HD static void vec(const dd& s0, const dd& s1, const dd& r1, const dd& u1, const dd& r2, dd& u, dd& w) {
-        const dd uu = mul(s0, r1);
-        w = mul(rank1s(s1, u1, uu), r2);
-        u = uu;
-    }
-#endif
     // general (non-state) s - a*b
     TOR_HD static dd rank1(const dd& s, const dd& a, const dd& b) { return dd_rank1(s, a, b); }
     TOR_HD static dd rank2_item(const dd& s, const dd& a, const dd& b, const dd& c, const dd& d) {
@@ -721,24 +648,13 @@ template <> struct Arith<qd> {
     TOR_HD static double hi(const qd& a) { return a.x[0]; }
     TOR_HD static qd norm(const qd& a) { return qd_renorm5_bf(a.x[0], a.x[1], a.x[2], a.x[3], 0.0); }
     TOR_HD static double sign_val(const qd& a) { return (a.x[0] + a.x[1]) + (a.x[2] + a.x[3]); }
-#ifndef TOR_QD_UNFUSED
     TOR_HD static qd mul(const qd& a, const qd& b) { return qd_mul_fused<true>(a, b); }
-#else
-    TOR_HD static qd mul(const qd& a, const qd& b) { return qd_mul(a, b); }
-#endif
     TOR_HD static qd rank2(const qd& s, const qd& a, const qd& b, const qd& c, const qd& d) {
         return qd_rank2(s, a, b, c, d);
     }
-#ifdef TOR_QD_ITEM_INLINE
-    // the fan-out item loops' update, inlined (one copy per fan-out level)
-    TOR_HD static qd rank2_item(const qd& s, const qd& a, const qd& b, const qd& c, const qd& d) {
-        return qd_rank2_body<!kQdLazy>(s, a, b, c, d);
-    }
-#else
     TOR_HD static qd rank2_item(const qd& s, const qd& a, const qd& b, const qd& c, const qd& d) {
         return rank2(s, a, b, c, d);
     }
-#endif
     TOR_HD static qd rank1(const qd& s, const qd& a, const qd& b) { return qd_rank1(s, a, b); }
     TOR_HD static qd rank1s(const qd& s, const qd& a, const qd& b) { return qd_rank1_lazy(s, a, b); }
     TOR_HD static qd rsqrt(const qd& a) { return qd_rsqrt(a); }
@@ -806,10 +722,6 @@ TOR_HD Piv<dd> pivot2<dd>(const dd& s00, const dd& s01, const dd& s11, const dd&
 // QD: det by one fused update
 // (one out-of-line body per pivot with its products, determinant and reciprocal square
 // roots inline: one call instead of ~8, and the two rsqrt chains schedule together)
-#ifndef TOR_QD_PIVOT_OOL
-#define TOR_QD_PIVOT_OOL 1
-#endif
-#if TOR_QD_PIVOT_OOL
 TOR_HD_RNI Piv<qd> qd_pivot_ool(qd s00, qd s01, qd s11, qd t) {
     Piv<qd> p;
     const qd a = qd_renorm5_bf(s00.x[0], s00.x[1], s00.x[2], s00.x[3], 0.0);
@@ -823,25 +735,9 @@ TOR_HD_RNI Piv<qd> qd_pivot_ool(qd s00, qd s01, qd s11, qd t) {
     p.tn = qd_mul_body<true>(t, rd);
     return p;
 }
-#endif
 template <>
 TOR_HD Piv<qd> pivot2<qd>(const qd& s00, const qd& s01, const qd& s11, const qd& t) {
-#if TOR_QD_PIVOT_OOL
     return qd_pivot_ool(s00, s01, s11, t);
-#else
-    using A = Arith<qd>;
-    Piv<qd> p;
-    const qd a = A::norm(s00);
-    p.bad0 = nonpositive(a.x[0]);
-    p.r1 = A::rsqrt(a);
-    const qd det = A::det2(a, s01, s11);
-    p.bad1 = nonpositive(det.x[0]);
-    const qd rd = A::rsqrt(det);
-    p.u1 = A::mul(s01, p.r1);
-    p.r2 = A::mul(A::mul(a, p.r1), rd);
-    p.tn = A::mul(t, rd);
-    return p;
-#endif
 }
 // QD pivot-row vector pair in one out-of-line body (one call instead of three)
 struct QdPair {
@@ -852,15 +748,9 @@ TOR_HD_RNI QdPair qd_vec_ool(qd s0, qd s1, qd r1, qd u1, qd r2) {
     return QdPair{u, qd_mul_body<true>(qd_rank1_body<!kQdLazy>(s1, u1, u), r2)};
 }
 TOR_HD void Arith<qd>::vec(const qd& s0, const qd& s1, const qd& r1, const qd& u1, const qd& r2, qd& u, qd& w) {
-#if TOR_QD_PIVOT_OOL
     const QdPair p = qd_vec_ool(s0, s1, r1, u1, r2);
     u = p.u;
     w = p.w;
-#else
-    const qd uu = mul(s0, r1);
-    w = mul(rank1s(s1, u1, uu), r2);
-    u = uu;
-#endif
 }
 // Term factor of a one-mode (leaf) state: t / sqrt(det).
 template <class T>
@@ -871,7 +761,6 @@ TOR_HD T leaf_term(const T& s00, const T& s01, const T& s11, const T& t, bool& b
     bad = nonpositive(A::hi(det));
     return A::mul(t, A::rsqrt(det));
 }
-#if TOR_QD_PIVOT_OOL
 struct QdLeaf {
     qd v;
     bool bad;
@@ -880,19 +769,11 @@ TOR_HD_RNI QdLeaf qd_leaf_ool(qd s00, qd s01, qd s11, qd t) {
     const qd det = qd_rank2_body<true>(qd{{0.0, 0.0, 0.0, 0.0}}, qd_neg(s00), s11, s01, s01);
     return QdLeaf{qd_mul_body<true>(t, qd_rsqrt_body<true>(det)), nonpositive(det.x[0])};
 }
-#endif
 template <>
 TOR_HD qd leaf_term<qd>(const qd& s00, const qd& s01, const qd& s11, const qd& t, bool& bad) {
-#if TOR_QD_PIVOT_OOL
     const QdLeaf r = qd_leaf_ool(s00, s01, s11, t);
     bad = r.bad;
     return r.v;
-#else
-    using A = Arith<qd>;
-    const qd det = A::det2(s00, s01, s11);
-    bad = nonpositive(det.x[0]);
-    return A::mul(t, A::rsqrt(det));
-#endif
 }
 template <>
 TOR_HD dd leaf_term<dd>(const dd& s00, const dd& s01, const dd& s11, const dd& t, bool& bad) {
@@ -944,9 +825,6 @@ template <> struct Acc<double> {
     }
 };
 
-#ifndef TOR_ACC_NOBR
-#define TOR_ACC_NOBR 0
-#endif
 template <> struct Acc<dd> {
     // running sum s (accurate DD) + a lazily renormalised block (h, c): per term one
     // TwoSum on the leading words and one plain add for the low words; the block is
@@ -957,19 +835,11 @@ template <> struct Acc<dd> {
     double abs_sum = 0.0;
     int sc = 0;
     TOR_HD void add(dd t, bool negative, int z) {
-#if TOR_ACC_NOBR
-        {  // branch-free: pow2i(0) = 1 exactly
-            const double f = pow2i(-sc * z);
-            t.hi *= f;
-            t.lo *= f;
-        }
-#else
         if (sc) {
             const double f = pow2i(-sc * z);
             t.hi *= f;
             t.lo *= f;
         }
-#endif
         const double th = negative ? -t.hi : t.hi;
         const double tl = negative ? -t.lo : t.lo;
         double nh, e;

@@ -73,9 +73,6 @@ __host__ __device__ constexpr int ijtab_off(int a) { return 2 * (a - 1) * a * (2
 // TMEM: the lane states of the last fan-out level are handed to their lanes through
 // tensor memory (each lane's own TMEM row) instead of shared-memory buffers; needs
 // 4-warp CTAs (one warp per TMEM lane quadrant).
-#ifndef TOR_DD_TMEM
-#define TOR_DD_TMEM 1
-#endif
 template <class T> struct Cfg;
 template <> struct Cfg<double> {
 #ifndef TOR_F64_MINB
@@ -93,26 +90,16 @@ template <> struct Cfg<double> {
 };
 template <> struct Cfg<dd> {
     static constexpr int L = 4;
-#ifndef TOR_DD_WS
-#define TOR_DD_WS 2
-#endif
-    // Warp specialisation (TMEM only).  0: none, every warp runs whole leaves.
-    // 1: 4 producer warps (DFS + fan-out levels 1-4) + 4 consumer warps (level 5 +
-    //    lane subtrees), double-buffered fan areas per pair.
-    // 2: 4 producers (DFS + levels 1-3) + 8 consumers (levels 4, 5 + lane subtrees),
-    //    each producer alternating between two jobs / two consumers; 12 warps at 168
-    //    registers (3 per SM sub-partition).
-    static constexpr int WS_MODE = TOR_DD_TMEM ? TOR_DD_WS : 0;
-    static constexpr bool WS = WS_MODE >= 1;
-#ifdef TOR_DD_WPB
-    static constexpr int WPB = TOR_DD_WPB;
-#else
-    // one 8-warp CTA per SM (two warps per TMEM lane quadrant, 256 columns each):
-    // measured 123 ms vs 138 ms for two 4-warp CTAs at n=32
-    static constexpr int WPB = TOR_DD_TMEM ? (WS_MODE == 2 ? 12 : 8) : 2;
-#endif
-    static constexpr int MINB = (TOR_DD_TMEM && WPB == 4) ? 2 : 1;
-    static constexpr bool TMEM = TOR_DD_TMEM;
+    // Warp specialisation (WS_MODE 2; the other types run unspecialised, WS_MODE 0):
+    // 4 producers (DFS + fan-out levels 1-2) + 8 consumers (levels 3-5 + lane subtrees),
+    // each producer alternating between two jobs / two consumers; one 12-warp CTA per SM
+    // at 168 registers (3 warps per SM sub-partition), two consumers per TMEM lane quadrant
+    // (256 columns each)
+    static constexpr int WS_MODE = 2;
+    static constexpr bool WS = true;
+    static constexpr int WPB = 12;
+    static constexpr int MINB = 1;
+    static constexpr bool TMEM = true;
 };
 template <> struct Cfg<qd> {
 #ifndef TOR_QD_L
@@ -170,12 +157,6 @@ __device__ __forceinline__ void report_breakdown(unsigned long long* err, uint64
 // Per-thread breakdown sink of the lane-level code: the same min key kept in a register
 // and published once per warp lifetime (flush), so the pivot checks are selects instead
 // of branches around an atomic (no basic-block split between consecutive pivot chains).
-#ifndef TOR_BAD_DEFER
-#define TOR_BAD_DEFER 1
-#endif
-#ifndef TOR_BAD_DEFER_P
-#define TOR_BAD_DEFER_P 0
-#endif
 struct LocalErr {
     unsigned long long v = ~0ull;
     __device__ __forceinline__ void flush(unsigned long long* err) const {
@@ -299,19 +280,6 @@ __device__ void warp_elim(const T* S, int d, int sr, int q, T* dst, const T& t_i
     __syncwarp();
 }
 
-#ifdef TOR_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[32];
-#define PHASE_T0() long long _pt = clock64()
-#define PHASE_MARK(k)                                                                \
-    do {                                                                             \
-        const long long _pn = clock64();                                             \
-        if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[k], (unsigned long long)(_pn - _pt)); \
-        _pt = _pn;                                                                   \
-    } while (0)
-#else
-#define PHASE_T0()
-#define PHASE_MARK(k)
-#endif
 
 // DFS step of the subtree kernel: eliminates the first mode of the q-mode source
 // state P (contiguous packed 2q-row triangle, HBM/L2 resident) and writes (a) the new
@@ -333,7 +301,6 @@ __device__ void dfs_elim(const T* P, int q, T* slot, bool write_slot, T* root, c
     constexpr int NB = sizeof(T) == sizeof(qd) ? TOR_QD_NB : TOR_NB;  // entries per lane per batch
     constexpr int RT = tri_sz(2 * Q0);
     const int lane = threadIdx.x & 31;
-    PHASE_T0();
     const int m = 2 * q;
     const int total = tri_sz(m - 2);
     const T* Pt = P + 2 * m - 1;
@@ -361,7 +328,6 @@ __device__ void dfs_elim(const T* P, int q, T* slot, bool write_slot, T* root, c
     load_batch(0);
     // ---- pivots (all lanes, warp-uniform) and pivot-row vectors
     const Piv<T> pv = pivot2<T>(p00, p01, p11, t_in);
-    PHASE_MARK(20);
     if (lane == 0) {
         if (pv.bad0 || pv.bad1) report_breakdown(err, mask, 2 * nsel + (pv.bad0 ? 0 : 1));
         *t_out = pv.tn;
@@ -377,7 +343,6 @@ __device__ void dfs_elim(const T* P, int q, T* slot, bool write_slot, T* root, c
         }
     }
     __syncwarp();
-    PHASE_MARK(21);
     // ---- trailing update, batch by batch
     T* rootb = root - (total - RT);  // entry k >= total-RT is root entry k-(total-RT)
     for (int kb = 0;;) {
@@ -400,7 +365,6 @@ __device__ void dfs_elim(const T* P, int q, T* slot, bool write_slot, T* root, c
         load_batch(kb);
     }
     __syncwarp();
-    PHASE_MARK(22);
 }
 
 // ---------------------------------------------------------- prefix levels ----
@@ -535,17 +499,10 @@ __global__ void direct_prefix_kernel(int n, int k, const T* R, int ninst, size_t
 // State of Q modes in registers: packed upper triangle of 2Q rows.
 // Pivot chain inside the lane subtrees: optionally one out-of-line copy (instruction
 // footprint) instead of one per call site.
-#ifdef TOR_PIVOT_NOINLINE
-template <class T>
-__device__ __noinline__ Piv<T> piv_lt(T s00, T s01, T s11, T t) {
-    return pivot2<T>(s00, s01, s11, t);
-}
-#else
 template <class T>
 __device__ __forceinline__ Piv<T> piv_lt(const T& s00, const T& s01, const T& s11, const T& t) {
     return pivot2<T>(s00, s01, s11, t);
 }
-#endif
 
 template <class T, int Q> struct St {
     T e[tri_sz(2 * Q)];
@@ -744,11 +701,8 @@ constexpr int kMirD = 8;
 // phase decides the bank conflicts.  kL5VecMap: lane & 15 -> parent for the pivot / vector
 // phase (conflict-free); kL5PairMap: lane pair -> parent for the mirror-split update (272 vs
 // 459 wavefronts per leaf for the identity map, ideal 208).  Nibble i = map(i).
-#ifndef TOR_L5_MAPS
-#define TOR_L5_MAPS 1
-#endif
-constexpr uint64_t kL5PairMap = TOR_L5_MAPS ? 0x0e249f35d71bac68ull : 0xfedcba9876543210ull;
-constexpr uint64_t kL5VecMap = TOR_L5_MAPS ? 0x79b0ec2568adf134ull : 0xfedcba9876543210ull;
+constexpr uint64_t kL5PairMap = 0x0e249f35d71bac68ull;
+constexpr uint64_t kL5VecMap = 0x79b0ec2568adf134ull;
 __host__ __device__ __forceinline__ int l5_map(uint64_t map, int i) { return static_cast<int>((map >> (4 * i)) & 15); }
 // level-5 node held by a consumer lane (lane pair -> parent x: nodes 2x, 2x + 1)
 __host__ __device__ __forceinline__ int l5_lane_node(int lane) { return 2 * l5_map(kL5PairMap, lane >> 1) + (lane & 1); }
@@ -811,16 +765,13 @@ __device__ __forceinline__ void tm_ld16(uint32_t taddr, uint32_t* r) {
         : "r"(taddr)
         : "memory");
 }
-#ifndef TOR_TM_LD16
-#define TOR_TM_LD16 1
-#endif
 template <int D, int K, int N> struct TmLd {
     __device__ __forceinline__ static void run(uint32_t row, uint32_t* r) {
         if constexpr (N > 0) {
             constexpr int col = tm_col<D>(K);
             // natural column layout (the scratch states): four consecutive entries per
             // 16-column load
-            if constexpr (TOR_TM_LD16 && N >= 4 && D != kMirD) {
+            if constexpr (N >= 4 && D != kMirD) {
                 tm_ld16(row + col, r);
                 TmLd<D, K + 4, N - 4>::run(row, r + 16);
             } else {
@@ -840,58 +791,6 @@ __device__ __forceinline__ void lt_wave(uint32_t row, const T (&u)[M], const T (
     tm_ld_entries<M, 2 * M - 1 + KB, CNT>(row, rt);
     tm_wait_ld();
     LtUpd<T, M, KB, KB + CNT>::run(rt, u, w, Sn);
-}
-
-// Lane subtree whose L-mode root state sits in this lane's TMEM row (entry k of the
-// packed 2L-row triangle at columns tm_col(k)..+3, DD words).  Same arithmetic as
-// lane_tree; only the source of the root entries differs.
-template <class T, int L, class E>
-__device__ __forceinline__ void lane_tree_tmem(uint32_t row, const T& t, bool neg, uint64_t mask, int nsel,
-                                               Acc<T>& acc, E* err) {
-    using A = Arith<T>;
-    constexpr int M = 2 * L;
-    constexpr int K01 = 2 * M - 1;  // entries of rows 0 and 1
-    acc.add(t, neg, nsel);
-    const uint64_t bit = 1ull << (L - 1);
-#pragma unroll 1
-    for (int br = 0; br < 2; ++br) {
-        St<T, L - 1> Sn;
-        T tn;
-        if (br == 0) {
-            uint32_t r0[4 * K01];
-            tm_ld_entries<M, 0, K01>(row, r0);
-            tm_wait_ld();
-            T e0[K01];
-#pragma unroll
-            for (int k = 0; k < K01; ++k) e0[k] = u32_to_dd(r0[4 * k], r0[4 * k + 1], r0[4 * k + 2], r0[4 * k + 3]);
-            // row 0: k = j (j = 0..M-1); row 1: k = M + (j - 1) (j = 1..M-1)
-            const Piv<T> pv = pivot2<T>(e0[0], e0[1], e0[M], t);
-            if (pv.bad0 || pv.bad1) report_breakdown(err, mask | bit, 2 * nsel + (pv.bad0 ? 0 : 1));
-            tn = pv.tn;
-            T u[M], w[M];
-#pragma unroll
-            for (int j = 2; j < M; ++j) {
-                u[j] = A::mul(A::unb(e0[j]), pv.r1);
-                w[j] = A::mul(A::rank1s(e0[M + j - 1], pv.u1, u[j]), pv.r2);
-            }
-            // trailing block in two waves to bound live registers
-            constexpr int NT = tri_sz(M - 2);
-            constexpr int H = NT / 2;
-            lt_wave<T, M, 0, H>(row, u, w, Sn);
-            lt_wave<T, M, H, NT - H>(row, u, w, Sn);
-            acc.add(tn, !neg, nsel + 1);
-        } else {
-            constexpr int NT = tri_sz(M - 2);
-            uint32_t rt[4 * NT];
-            tm_ld_entries<M, K01, NT>(row, rt);
-            tm_wait_ld();
-#pragma unroll
-            for (int kk = 0; kk < NT; ++kk) Sn.e[kk] = u32_to_dd(rt[4 * kk], rt[4 * kk + 1], rt[4 * kk + 2], rt[4 * kk + 3]);
-            tn = t;
-        }
-        SubReg<T, L - 1>::run(Sn, tn, br == 0 ? !neg : neg, br == 0 ? (mask | bit) : mask, nsel + (br == 0), acc,
-                              err);
-    }
 }
 
 // TMEM-streamed lane subtree: emits the 2^L - 1 extension terms of the L-mode node in
@@ -925,7 +824,7 @@ template <class T, int M, int K, int END> struct LtUpdTm {
         if constexpr (K < END) {
             constexpr int D = M - 2;
             constexpr int i = tri_row(D, K), j = tri_col(D, K);
-            if constexpr (TOR_TM_LD16 && END - K >= 4) {
+            if constexpr (END - K >= 4) {
                 // four entries, one 16-column store (natural scratch layout)
                 uint32_t r[16];
                 LtQuad<T, M, K, 4>::run(rt, u, w, r);
@@ -945,7 +844,7 @@ template <class T, int M, int K, int END> struct LtUpdTm {
 template <int D, int K, int END> struct TmCopy {
     __device__ __forceinline__ static void run(const uint32_t* rt, uint32_t dst) {
         if constexpr (K < END) {
-            if constexpr (TOR_TM_LD16 && END - K >= 4) {
+            if constexpr (END - K >= 4) {
                 tm_st16p(dst + tm_col<D - 2>(K), rt);
                 TmCopy<D, K + 4, END>::run(rt + 16, dst);
             } else {
@@ -955,14 +854,9 @@ template <int D, int K, int END> struct TmCopy {
         }
     }
 };
-// kPre: the include branch's pivot was computed by the parent (pre), overlapping the
-// parent's trailing update instead of starting after it.
-#ifndef TOR_PIV_AHEAD
-#define TOR_PIV_AHEAD 0
-#endif
-template <class T, int L, class E, bool kPre = false>
+template <class T, int L, class E>
 __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t, bool neg, uint64_t mask, int nsel,
-                                         Acc<T>& acc, E* err, const Piv<T>* pre = nullptr) {
+                                         Acc<T>& acc, E* err) {
     using A = Arith<T>;
     constexpr int M = 2 * L;
     constexpr int K01 = 2 * M - 1;  // entries of rows 0 and 1
@@ -972,7 +866,6 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
     for (int br = 0; br < 2; ++br) {
         T tn;
         if constexpr (L >= 4) {
-            Piv<T> cpiv;
             if (br == 0) {
                 uint32_t r0[4 * K01];
                 tm_ld_entries<M, 0, K01>(row, r0);
@@ -995,18 +888,6 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
                     tm_ld_entries<M, K01, H>(row, rt);
                     tm_wait_ld();
                     LtUpdTm<T, M, 0, H>::run(rt, u, w, scr);
-#if TOR_PIV_AHEAD
-                    if constexpr (L == 4) {
-                        // the child's pivot entries (0,0), (0,1), (1,1) = trailing entries 0, 1, M-2
-                        static_assert(M - 2 < H, "child pivot entries in the first wave");
-                        const T c00 = A::rank2(u32_to_dd(rt[0], rt[1], rt[2], rt[3]), u[2], u[2], w[2], w[2]);
-                        const T c01 = A::rank2(u32_to_dd(rt[4], rt[5], rt[6], rt[7]), u[2], u[3], w[2], w[3]);
-                        const T c11 = A::rank2(u32_to_dd(rt[4 * (M - 2)], rt[4 * (M - 2) + 1], rt[4 * (M - 2) + 2],
-                                                         rt[4 * (M - 2) + 3]),
-                                               u[3], u[3], w[3], w[3]);
-                        cpiv = piv_lt<T>(c00, c01, c11, tn);
-                    }
-#endif
                 }
                 {
                     uint32_t rt[4 * H];
@@ -1028,14 +909,6 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
                     tm_ld_entries<M, K01, H>(row, rt);
                     tm_wait_ld();
                     TmCopy<M, 0, H>::run(rt, scr);
-#if TOR_PIV_AHEAD
-                    if constexpr (L == 4) {
-                        cpiv = piv_lt<T>(u32_to_dd(rt[0], rt[1], rt[2], rt[3]), u32_to_dd(rt[4], rt[5], rt[6], rt[7]),
-                                         u32_to_dd(rt[4 * (M - 2)], rt[4 * (M - 2) + 1], rt[4 * (M - 2) + 2],
-                                                   rt[4 * (M - 2) + 3]),
-                                         t);
-                    }
-#endif
                 }
                 {
                     uint32_t rt[4 * (NT - H)];
@@ -1046,9 +919,8 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
                 tn = t;
             }
             tm_wait_st();
-            tmem_ext<T, L - 1, E, TOR_PIV_AHEAD && L == 4>(scr, scr, tn, br == 0 ? !neg : neg,
-                                                             br == 0 ? (mask | bit) : mask, nsel + (br == 0), acc,
-                                                             err, &cpiv);
+            tmem_ext<T, L - 1, E>(scr, scr, tn, br == 0 ? !neg : neg, br == 0 ? (mask | bit) : mask, nsel + (br == 0),
+                                  acc, err);
         } else {
             St<T, L - 1> Sn;
             if (br == 0) {
@@ -1058,9 +930,7 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
                 T e0[K01];
 #pragma unroll
                 for (int k = 0; k < K01; ++k) e0[k] = u32_to_dd(r0[4 * k], r0[4 * k + 1], r0[4 * k + 2], r0[4 * k + 3]);
-                Piv<T> pv;
-                if constexpr (kPre) pv = *pre;
-                else pv = piv_lt<T>(e0[0], e0[1], e0[M], t);
+                const Piv<T> pv = piv_lt<T>(e0[0], e0[1], e0[M], t);
                 if (pv.bad0 || pv.bad1) report_breakdown(err, mask | bit, 2 * nsel + (pv.bad0 ? 0 : 1));
                 tn = pv.tn;
                 T u[M], w[M];
@@ -1234,17 +1104,12 @@ template <class T, int M, int C> struct MirChunk {
 #ifndef TOR_UB
 #define TOR_UB 5
 #endif
-#ifndef TOR_ITEM_UNROLL
-#define TOR_ITEM_UNROLL 1
-#endif
-constexpr int kItemUnroll = TOR_ITEM_UNROLL;  // fan-out item batches per loop trip
 #ifndef TOR_QD_UB
 #define TOR_QD_UB 1
 #endif
 #ifndef TOR_F64_UB
 #define TOR_F64_UB 5
 #endif
-#if TOR_QD_PIVOT_OOL
 // QD fan-out level trailing update: one out-of-line loop over this lane's items
 // it = lane + 32 s (s < nit, it < ne), each s - u_i u_j - w_i w_j with the operands loaded
 // from shared memory inside (one call per level instead of one per item)
@@ -1259,7 +1124,6 @@ __device__ __noinline__ void qd_items_ool(const qd* sm, const qd* uwv, const uin
         out[32 * s] = qd_rank2_body<!kQdLazy>(sm[src], uwv[a], uwv[b], uwv[a + m], uwv[b + m]);
     }
 }
-#endif
 template <class T, int E_LVL> struct FanLevel {
     static constexpr int Q0 = WarpSmem<T>::Q0;
     static constexpr int E = 1 << (E_LVL - 1);
@@ -1275,7 +1139,6 @@ template <class T, int E_LVL> struct FanLevel {
         const int lane = threadIdx.x & 31;
         const int x = (Cfg<T>::TMEM && E_LVL == FAN) ? l5_map(kL5VecMap, lane & (E - 1)) : lane & (E - 1);
         const int g = lane / E;
-        PHASE_T0();
         const NodeRef nr = node_ref<T>(tabs, E_LVL - 1, x);
         const T* P = sm + nr.off;
         const Piv<T> pv = pivot2<T>(P[0], P[1], P[m], tvals[nr.tix]);
@@ -1284,7 +1147,6 @@ template <class T, int E_LVL> struct FanLevel {
             if (pv.bad0 || pv.bad1) report_breakdown(err, nm, 2 * (leaf_sel + __popc(x)) + (pv.bad0 ? 0 : 1));
             tvals[E - 1 + x] = pv.tn;  // level e-1 t values live below index E-1: no hazard
         }
-        PHASE_MARK(5 + 3 * (E_LVL - 1));
         // pivot-row vectors u_j, w_j (j = 2..m-1) of parent x
         T* uwx = uwv + x * (2 * m + 1);  // odd stride: parents spread over the banks
         {
@@ -1308,7 +1170,6 @@ template <class T, int E_LVL> struct FanLevel {
                 }
         }
         __syncwarp();
-        PHASE_MARK(6 + 3 * (E_LVL - 1));
         if constexpr (Cfg<T>::TMEM && E_LVL == FAN) {
             // last level -> TMEM: lane 2x+1 owns include child x, lane 2x the exclude
             // child (= parent x's trailing block Pt).  The pair splits the include
@@ -1342,7 +1203,6 @@ template <class T, int E_LVL> struct FanLevel {
             }
             tm_wait_st();
             __syncwarp();
-            PHASE_MARK(7 + 3 * (E_LVL - 1));
             return;
         }
         // trailing updates into the level-e buffers: item it = lane + 32 s (x-major)
@@ -1352,7 +1212,6 @@ template <class T, int E_LVL> struct FanLevel {
                            : (sizeof(T) == sizeof(double) ? TOR_F64_UB : TOR_UB);  // items per batch
         const uint32_t* itb = tabs + WarpSmem<T>::item_off(E_LVL) + lane;
         T* out = sm + WarpSmem<T>::lvl_off(E_LVL) + lane;
-#if TOR_QD_PIVOT_OOL && !defined(TOR_QD_ITEM_INLINE)
         if constexpr (sizeof(T) == sizeof(qd)) {
             // QD: the item loop as one out-of-line call that loads its operands itself
             static_assert(WarpSmem<T>::buf_stride(E_LVL) == tn, "QD fan-out buffers are unpadded");
@@ -1361,8 +1220,7 @@ template <class T, int E_LVL> struct FanLevel {
             __syncwarp();
             return;
         }
-#endif
-#pragma unroll(kItemUnroll)
+#pragma unroll 1
         for (int s0 = 0; s0 < NIT; s0 += UB) {
             T sv[UB], ui[UB], uj[UB], wi[UB], wj[UB];
 #pragma unroll
@@ -1391,7 +1249,6 @@ template <class T, int E_LVL> struct FanLevel {
             }
         }
         __syncwarp();
-        PHASE_MARK(7 + 3 * (E_LVL - 1));
     }
 };
 
@@ -1480,15 +1337,9 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
     // DFS step + root + fan-out of one leaf of job J into the fan area fsm (buffers +
     // t values): all FAN levels, or (warp-specialised) levels 1..FAN-1 -- the level-FAN
     // states in shared memory, or in TMEM at tm_slot for the TMEM types
-#if TOR_BAD_DEFER_P
-    LocalErr perr_l;  // fan-out breakdown keys of this warp, published at kernel end
-    LocalErr* perr = &perr_l;
-#else
     unsigned long long* perr = err;
-#endif
     auto produce_leaf = [&](const Job<T>& J, uint64_t leaf, uint32_t tm_slot, T* fsm, T* dfs_t, T* slots) {
         T* ftv = fsm + SM::kTOff;
-        PHASE_T0();
         if (leaf > 0) {
             // flip exclude->include at depth kd (lowest set bit of leaf)
             const int b = __ffsll(static_cast<long long>(leaf)) - 1;
@@ -1516,7 +1367,6 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
             if (lane == 0) ftv[31] = dfs_t[kd + 1];
             __syncwarp();
         }
-        PHASE_MARK(0);
         if (leaf == 0) {
             // first leaf: the root is the job state's trailing Q0 modes (HBM), a
             // contiguous packed triangle
@@ -1538,7 +1388,6 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         __syncwarp();
         const uint64_t leaf_mask = J.mask | (leaf << Q0);
         const int leaf_sel = J.nsel + __popcll(leaf);
-        PHASE_MARK(1);
         FanLevel<T, 1>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
         FanLevel<T, 2>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
         if constexpr (Cfg<T>::WS_MODE != 2 || kConsFirst > 3)
@@ -1597,13 +1446,6 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                     : "r"(a), "r"(parity), "r"(static_cast<uint32_t>(TOR_MB_HINT))
                     : "memory");
         };
-#ifndef TOR_WS_REGS
-#define TOR_WS_REGS 0  // e.g. 120: producers give registers to the consumers (setmaxnreg)
-#endif
-        if constexpr (TOR_WS_REGS > 0) {
-            if (wib < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(TOR_WS_REGS));
-            else asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(168 + (168 - TOR_WS_REGS) / 2));
-        }
         if (wib < 4) {
             const int p = wib;
             Job<T> J[2];
@@ -1658,12 +1500,8 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
             T* cuw = csm + SM::kUwOff;
             Acc<T> acc;
             acc.sc = tsc;
-#if TOR_BAD_DEFER
             LocalErr lerr;
             LocalErr* cerr = &lerr;
-#else
-            unsigned long long* cerr = err;
-#endif
             for (uint32_t k = 0;; ++k) {
                 mb_wait(c, k & 1);
                 const unsigned long long leaf_mask = meta[c].mask;
@@ -1689,81 +1527,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                     acc.sc = tsc;
                 }
             }
-#if TOR_BAD_DEFER
             lerr.flush(err);
-#endif
-        }
-    } else if constexpr (Cfg<T>::WS) {
-        // ---- warp-specialised: producer warp p (0-3) runs the DFS and fan-out levels
-        // 1..FAN-1 of leaf i into fan area 2p + (i & 1); consumer warp p+4 runs level FAN
-        // (into its TMEM lane quadrant) and the lane subtrees from that area.  One named
-        // barrier per leaf hands area i to the consumer and area i-1 back to the producer.
-        struct WsMeta {
-            unsigned long long mask;
-            unsigned long long job;
-            int sel, flags;  // 1: last leaf of the job, 2: no more leaves
-        };
-        __shared__ WsMeta meta[4][2];
-        const int pair = wib & 3;
-        auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;\n" ::"r"(1 + pair) : "memory"); };
-        int slot = 0;
-        if (wib < 4) {
-            for (;;) {
-                unsigned long long job = 0;
-                if (lane == 0) job = atomicAdd(job_counter, 1ull);
-                job = __shfl_sync(0xffffffffu, job, 0);
-                if (job >= njobs) break;
-                const Job<T> J = jobs[job];
-                for (uint64_t leaf = 0; leaf < (1ull << D); ++leaf) {
-                    produce_leaf(J, leaf, 0u, area(2 * pair + slot), dfs_t, slots);
-                    if (lane == 0) {
-                        meta[pair][slot].mask = J.mask | (leaf << Q0);
-                        meta[pair][slot].job = job;
-                        meta[pair][slot].sel = J.nsel + __popcll(leaf);
-                        meta[pair][slot].flags = leaf + 1 == (1ull << D) ? 1 : 0;
-                    }
-                    __syncwarp();
-                    pair_sync();
-                    slot ^= 1;
-                }
-            }
-            if (lane == 0) meta[pair][slot].flags = 2;
-            __syncwarp();
-            pair_sync();
-        } else {
-            const uint32_t crow = tmem_base + ((32u * pair) << 16);
-            T* cuw = area(2 * pair + 1) + SM::kUwOff;  // the consumer's pivot-row vectors
-            Acc<T> acc;
-            acc.sc = tsc;
-            for (;;) {
-                pair_sync();
-                const unsigned long long leaf_mask = meta[pair][slot].mask;
-                const unsigned long long job = meta[pair][slot].job;
-                const int leaf_sel = meta[pair][slot].sel, flags = meta[pair][slot].flags;
-                if (flags & 2) break;
-                T* fsm = area(2 * pair + slot);
-                T* ftv = fsm + SM::kTOff;
-                FanLevel<T, FAN>::run(fsm, ftv, cuw, tabs, leaf_mask, leaf_sel, err, crow);
-                const int c = l5_lane_node(lane);
-                const T vt = ftv[node_ref<T>(tabs, FAN, c).tix];
-                const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(c) << L);
-                const int lsel = leaf_sel + __popc(c);
-                const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
-#ifdef TOR_LT_REGS
-                lane_tree_tmem<T, L>(crow, vt, nodeneg, lmask, lsel, acc, err);
-#else
-                acc.add(vt, nodeneg, lsel);
-                tmem_ext<T, L>(crow, crow + 4 * tri_sz(2 * L), vt, nodeneg, lmask, lsel, acc, err);
-#endif
-                acc.flush();
-                if (flags & 1) {
-                    write_partial(acc, job);
-                    acc = Acc<T>();
-                    acc.sc = tsc;
-                }
-                __syncwarp();
-                slot ^= 1;
-            }
         }
     } else {
         for (;;) {
@@ -1776,28 +1540,22 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
             acc.sc = tsc;
             for (uint64_t leaf = 0; leaf < (1ull << D); ++leaf) {
                 produce_leaf(J, leaf, tm_row, sm, dfs_t, slots);
-                PHASE_T0();
                 // lanes: node (FAN, c); TMEM rows hold the nodes of the level-5 lane map
                 const uint64_t leaf_mask = J.mask | (leaf << Q0);
                 const int leaf_sel = J.nsel + __popcll(leaf);
-                const int c = Cfg<T>::TMEM ? l5_lane_node(lane) : lane;
+                const int c = lane;
                 const NodeRef nr = node_ref<T>(tabs, FAN, c);
                 const T vt = tvals[nr.tix];
                 const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(c) << L);
                 const int lsel = leaf_sel + __popc(c);
                 const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
-                if constexpr (Cfg<T>::TMEM) lane_tree_tmem<T, L>(tm_row, vt, nodeneg, lmask, lsel, acc, err);
-                else lane_tree<T, L>(sm + nr.off, 2 * L, 0, vt, nodeneg, lmask, lsel, acc, err);
+                lane_tree<T, L>(sm + nr.off, 2 * L, 0, vt, nodeneg, lmask, lsel, acc, err);
                 acc.flush();
                 __syncwarp();
-                PHASE_MARK(4);
             }
             write_partial(acc, job);
         }
     }
-#if TOR_BAD_DEFER_P
-    perr_l.flush(err);
-#endif
     if constexpr (Cfg<T>::TMEM) {
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         __syncthreads();
@@ -2232,24 +1990,6 @@ class PlanImpl final : public Plan {
         unsigned long long herr = 0;
         CK(cudaMemcpyAsync(&herr, errw, sizeof(herr), cudaMemcpyDeviceToHost, st_));
         CK(cudaStreamSynchronize(st_));
-#ifdef TOR_PHASE_TIMING
-        {
-            unsigned long long pc[32];
-            cudaMemcpyFromSymbol(pc, g_phase_cycles, sizeof(pc));
-            const char* names[23] = {"dfs_elim", "root_copy", "-", "-", "lane_tree", "L1 piv", "L1 vec",
-                                     "L1 ent", "L2 piv", "L2 vec", "L2 ent", "L3 piv", "L3 vec", "L3 ent",
-                                     "L4 piv", "L4 vec", "L4 ent", "L5 piv", "L5 vec", "L5 ent",
-                                     "dfs ld+piv", "dfs vec", "dfs ent"};
-            double tot = 0;
-            for (int i = 0; i < 20; ++i) tot += pc[i];
-            for (int i = 0; i < 23; ++i)
-                if (pc[i])
-                    std::fprintf(stderr, "[phase] %-10s %6.2f%%  %.3e warp-cycles\n", names[i], 100.0 * pc[i] / tot,
-                                 (double)pc[i]);
-            unsigned long long z[32] = {0};
-            cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
-        }
-#endif
         out.assign(ninst_, EngineOut{});
         const uint64_t terms = (chi_ - clo_) << (n_ - kbits_);
         for (int i = 0; i < ninst_; ++i) {
