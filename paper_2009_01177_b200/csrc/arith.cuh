@@ -787,7 +787,19 @@ TOR_HD dd leaf_term<dd>(const dd& s00, const dd& s01, const dd& s11, const dd& t
 // ========================================================== accumulators ==
 // Signed term accumulation.  fp64 and DD terms accumulate in an accurate DD sum,
 // QD terms in QD.  Sum |t| is carried in fp64 for the posterior cancellation check.
-template <class T> struct Acc;
+// kScaled: the input was scaled by 2^-sc (DD grid states need max R_kk < 3.75; physical
+// states have R_kk <= 2 and never are), so each term is multiplied back by 2^(sc |Z|).  A
+// compile-time switch: a runtime `if (sc)` is if-converted and costs every term.
+template <class T, bool kScaled = false> struct Acc;
+
+// x or -x: one integer XOR of the sign bit (no select on both words)
+TOR_HD double flip_sign(double x, bool negative) {
+#if defined(__CUDA_ARCH__)
+    return __hiloint2double(__double2hiint(x) ^ (static_cast<int>(negative) << 31), __double2loint(x));
+#else
+    return negative ? -x : x;
+#endif
+}
 
 // term scaling for scaled inputs (R -> 2^-s R multiplies t(Z) by 2^(s|Z|)): exact
 TOR_HD double pow2i(int e) {
@@ -798,13 +810,13 @@ TOR_HD double pow2i(int e) {
 #endif
 }
 
-template <> struct Acc<double> {
+template <bool kScaled> struct Acc<double, kScaled> {
     dd s{0.0, 0.0};
     double abs_sum = 0.0;
     int sc = 0;
     TOR_HD void add(double t, bool negative, int z) {
-        if (sc) t *= pow2i(-sc * z);
-        const double v = negative ? -t : t;
+        if constexpr (kScaled) t *= pow2i(-sc * z);
+        const double v = flip_sign(t, negative);
         double h, e;
         two_sum(s.hi, v, h, e);
         s.hi = h;
@@ -825,7 +837,7 @@ template <> struct Acc<double> {
     }
 };
 
-template <> struct Acc<dd> {
+template <bool kScaled> struct Acc<dd, kScaled> {
     // running sum s (accurate DD) + a lazily renormalised block (h, c): per term one
     // TwoSum on the leading words and one plain add for the low words; the block is
     // folded into s by flush() every few terms (lane subtrees), keeping the lazy
@@ -835,13 +847,13 @@ template <> struct Acc<dd> {
     double abs_sum = 0.0;
     int sc = 0;
     TOR_HD void add(dd t, bool negative, int z) {
-        if (sc) {
+        if constexpr (kScaled) {
             const double f = pow2i(-sc * z);
             t.hi *= f;
             t.lo *= f;
         }
-        const double th = negative ? -t.hi : t.hi;
-        const double tl = negative ? -t.lo : t.lo;
+        const double th = flip_sign(t.hi, negative);  // 85.7 vs 86.2 ms with selects (n=32)
+        const double tl = flip_sign(t.lo, negative);
         double nh, e;
         two_sum(h, th, nh, e);
         h = nh;
@@ -865,7 +877,7 @@ template <> struct Acc<dd> {
     }
 };
 
-template <> struct Acc<qd> {
+template <bool kScaled> struct Acc<qd, kScaled> {
     // running sum s (renormalised QD) + a lazy block b: per term, exact TwoSums on the
     // words of orders 0..2 (each order's errors into the next order), order 3 plainly;
     // the block is renormalised and added to s by flush() (every lane subtree).
@@ -875,15 +887,14 @@ template <> struct Acc<qd> {
     int sc = 0;
     TOR_HD void add(const qd& t, bool negative, int z) {
         (void)z;  // QD words are never grid-scaled
-        const double g = negative ? -1.0 : 1.0;
         double e0, e1, e2, e3, e4, e5;
-        two_sum(b0, g * t.x[0], b0, e0);
-        two_sum(b1, g * t.x[1], b1, e1);
+        two_sum(b0, flip_sign(t.x[0], negative), b0, e0);
+        two_sum(b1, flip_sign(t.x[1], negative), b1, e1);
         two_sum(b1, e0, b1, e2);
-        two_sum(b2, g * t.x[2], b2, e3);
+        two_sum(b2, flip_sign(t.x[2], negative), b2, e3);
         two_sum(b2, e1, b2, e4);
         two_sum(b2, e2, b2, e5);
-        b3 += ((g * t.x[3] + e3) + e4) + e5;
+        b3 += ((flip_sign(t.x[3], negative) + e3) + e4) + e5;
         abs_sum += fabs(t.x[0]);
     }
     TOR_HD void flush() {

@@ -195,20 +195,11 @@ template <> __device__ __forceinline__ qd shfl_t<qd>(const qd& v, int s) {
     return r;
 }
 
-template <class T> __device__ __forceinline__ void warp_fold(Acc<T>& a) {
+// (fp64 mode accumulates in DD: a.s is a dd there)
+template <class AC> __device__ __forceinline__ void warp_fold(AC& a) {
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) {
-        Acc<T> o;
-        o.s = shfl_xor_t(a.s, m);
-        o.abs_sum = __shfl_xor_sync(0xffffffffu, a.abs_sum, m);
-        a.merge(o);
-    }
-}
-// fp64 mode accumulates in DD
-template <> __device__ __forceinline__ void warp_fold<double>(Acc<double>& a) {
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) {
-        Acc<double> o;
+        AC o;
         o.s = shfl_xor_t(a.s, m);
         o.abs_sum = __shfl_xor_sync(0xffffffffu, a.abs_sum, m);
         a.merge(o);
@@ -547,9 +538,9 @@ constexpr int kLoopQ = TOR_LOOPQ;
 constexpr int kLoopQQd = TOR_QD_LOOPQ;
 
 template <class T, int Q> struct SubReg {
-    template <class E>
+    template <class AC, class E>
     __device__ __forceinline__ static void branch(const St<T, Q>& S, int br, const T& t, bool neg, uint64_t mask,
-                                                  int nsel, Acc<T>& acc, E* err) {
+                                                  int nsel, AC& acc, E* err) {
         constexpr int M = 2 * Q;
         const uint64_t bit = 1ull << (Q - 1);
         St<T, Q - 1> Sn;
@@ -567,9 +558,9 @@ template <class T, int Q> struct SubReg {
         SubReg<T, Q - 1>::run(Sn, tn, br == 0 ? !neg : neg, br == 0 ? (mask | bit) : mask, nsel + (br == 0),
                               acc, err);
     }
-    template <class E>
+    template <class AC, class E>
     __device__ __forceinline__ static void run(const St<T, Q>& S, const T& t, bool neg, uint64_t mask, int nsel,
-                                               Acc<T>& acc, E* err) {
+                                               AC& acc, E* err) {
         if constexpr (Q >= (sizeof(T) == sizeof(qd) ? kLoopQQd : kLoopQ)) {
 #pragma unroll 1
             for (int br = 0; br < 2; ++br) branch(S, br, t, neg, mask, nsel, acc, err);
@@ -580,9 +571,9 @@ template <class T, int Q> struct SubReg {
     }
 };
 template <class T> struct SubReg<T, 1> {
-    template <class E>
+    template <class AC, class E>
     __device__ __forceinline__ static void run(const St<T, 1>& S, const T& t, bool neg, uint64_t mask, int nsel,
-                                               Acc<T>& acc, E* err) {
+                                               AC& acc, E* err) {
         bool bad;
         const T tn = leaf_term<T>(S.e[0], S.e[1], S.e[2], t, bad);
         // both pivots of the last mode: a negative-definite 2x2 block has det > 0.  The state
@@ -597,9 +588,9 @@ template <class T> struct SubReg<T, 1> {
 // Lane subtree rooted at an L-mode view in shared memory: emits the node's own
 // term and all 2^L - 1 extensions.  Branch 0 includes the first view mode (its
 // elimination reads shared memory), branch 1 excludes it (loads the trailing block).
-template <class T, int L, class E>
+template <class T, int L, class AC, class E>
 __device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t, bool neg, uint64_t mask, int nsel,
-                                          Acc<T>& acc, E* err) {
+                                          AC& acc, E* err) {
     using A = Arith<T>;
     constexpr int M = 2 * L;
     acc.add(t, neg, nsel);
@@ -854,9 +845,9 @@ template <int D, int K, int END> struct TmCopy {
         }
     }
 };
-template <class T, int L, class E>
+template <class T, int L, class AC, class E>
 __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t, bool neg, uint64_t mask, int nsel,
-                                         Acc<T>& acc, E* err) {
+                                         AC& acc, E* err) {
     using A = Arith<T>;
     constexpr int M = 2 * L;
     constexpr int K01 = 2 * M - 1;  // entries of rows 0 and 1
@@ -919,7 +910,7 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
                 tn = t;
             }
             tm_wait_st();
-            tmem_ext<T, L - 1, E>(scr, scr, tn, br == 0 ? !neg : neg, br == 0 ? (mask | bit) : mask, nsel + (br == 0),
+            tmem_ext<T, L - 1, AC, E>(scr, scr, tn, br == 0 ? !neg : neg, br == 0 ? (mask | bit) : mask, nsel + (br == 0),
                                   acc, err);
         } else {
             St<T, L - 1> Sn;
@@ -1253,7 +1244,8 @@ template <class T, int E_LVL> struct FanLevel {
 };
 
 
-template <class T>
+// kScaled: the input was scaled by 2^-tsc (Acc)
+template <class T, bool kScaled>
 __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
     subtree_kernel(const Job<T>* jobs, uint64_t njobs, int nmodes, int rjob, T* scratch, size_t scratch_stride,
                    double* partials, unsigned long long* err, unsigned long long* job_counter, int tsc) {
@@ -1395,8 +1387,9 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         if constexpr (Cfg<T>::WS_MODE != 2) FanLevel<T, 4>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
         if constexpr (!Cfg<T>::WS) FanLevel<T, 5>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
     };
-    auto write_partial = [&](Acc<T>& acc, unsigned long long job) {
-        warp_fold<T>(acc);
+    using AccT = Acc<T, kScaled>;
+    auto write_partial = [&](AccT& acc, unsigned long long job) {
+        warp_fold(acc);
         if (lane == 0) {
             double w[4];
             acc.words(w);
@@ -1498,7 +1491,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
             T* csm = area(c);
             T* ctv = csm + SM::kTOff;
             T* cuw = csm + SM::kUwOff;
-            Acc<T> acc;
+            AccT acc;
             acc.sc = tsc;
             LocalErr lerr;
             LocalErr* cerr = &lerr;
@@ -1519,11 +1512,11 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 const int lsel = leaf_sel + __popc(node);
                 const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
                 acc.add(vt, nodeneg, lsel);
-                tmem_ext<T, L>(crow, crow + 4 * tri_sz(2 * L), vt, nodeneg, lmask, lsel, acc, cerr);
+                tmem_ext<T, L, AccT>(crow, crow + 4 * tri_sz(2 * L), vt, nodeneg, lmask, lsel, acc, cerr);
                 acc.flush();
                 if (flags & 1) {
                     write_partial(acc, job);
-                    acc = Acc<T>();
+                    acc = AccT();
                     acc.sc = tsc;
                 }
             }
@@ -1536,7 +1529,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
             job = __shfl_sync(0xffffffffu, job, 0);
             if (job >= njobs) break;
             const Job<T> J = jobs[job];
-            Acc<T> acc;
+            AccT acc;
             acc.sc = tsc;
             for (uint64_t leaf = 0; leaf < (1ull << D); ++leaf) {
                 produce_leaf(J, leaf, tm_row, sm, dfs_t, slots);
@@ -1549,7 +1542,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(c) << L);
                 const int lsel = leaf_sel + __popc(c);
                 const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
-                lane_tree<T, L>(sm + nr.off, 2 * L, 0, vt, nodeneg, lmask, lsel, acc, err);
+                lane_tree<T, L, AccT>(sm + nr.off, 2 * L, 0, vt, nodeneg, lmask, lsel, acc, err);
                 acc.flush();
                 __syncwarp();
             }
@@ -1577,7 +1570,7 @@ __global__ void small_job_kernel(const Job<T>* jobs, uint64_t njobs, int nmodes,
     const uint64_t jid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (jid >= njobs) return;
     const Job<T> J = jobs[jid];
-    Acc<T> acc;
+    Acc<T, true> acc;  // runtime scale (small jobs are off the hot path)
     acc.sc = tsc;
     T M[tri_sz(2 * RMAX)];
     int sel[RMAX];
@@ -1839,11 +1832,12 @@ class PlanImpl final : public Plan {
             constexpr int WPB = Cfg<T>::WPB;
             smem_ = Cfg<T>::WS_MODE == 2 ? SM::kTabBytes + SM::kWarpBytes * 8 + sizeof(T) * SM::kProdEntries * 4
                                          : SM::kTabBytes + SM::kWarpBytes * WPB;
-            CK(cudaFuncSetAttribute(subtree_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem_)));
-            CK(cudaFuncSetAttribute(subtree_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            for (auto* kfn : {subtree_kernel<T, false>, subtree_kernel<T, true>}) {
+                CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
+                CK(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            }
             int bps = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, subtree_kernel<T>, 32 * WPB, smem_));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, subtree_kernel<T, false>, 32 * WPB, smem_));
             if (bps < 1) {
                 err = "subtree kernel does not fit on an SM";
                 return -1;
@@ -1855,15 +1849,15 @@ class PlanImpl final : public Plan {
             if (range.blocks_per_sm > 0) bps = range.blocks_per_sm;
             if (std::getenv("TOR_DEBUG_TIMING")) {
                 cudaFuncAttributes fa;
-                cudaFuncGetAttributes(&fa, subtree_kernel<T>);
+                cudaFuncGetAttributes(&fa, subtree_kernel<T, false>);
                 std::fprintf(stderr, "[tor] subtree_kernel: %d blocks/SM x %d warps, smem %zu B/block, %d regs, "
                                      "local %zu B, static smem %zu\n",
                              bps, WPB, smem_, fa.numRegs, fa.localSizeBytes, fa.sharedSizeBytes);
                 for (size_t s2 : {size_t(0), size_t(50000), size_t(100000), size_t(110000), smem_}) {
                     int b2 = 0;
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, subtree_kernel<T>, 32 * WPB, s2);
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, subtree_kernel<T, false>, 32 * WPB, s2);
                     size_t avail = 0;
-                    cudaOccupancyAvailableDynamicSMemPerBlock(&avail, subtree_kernel<T>, 2, 32 * WPB);
+                    cudaOccupancyAvailableDynamicSMemPerBlock(&avail, subtree_kernel<T, false>, 2, 32 * WPB);
                     std::fprintf(stderr, "[tor]   smem %zu -> %d blocks/SM (avail dyn smem @2 blocks: %zu)\n", s2, b2,
                                  avail);
                 }
@@ -1951,8 +1945,10 @@ class PlanImpl final : public Plan {
         CK(cudaEventRecord(ev_[1], st_));
         if (rjob_ >= Q0) {
             constexpr int WPB = Cfg<T>::WPB;
-            subtree_kernel<T><<<static_cast<unsigned>(blocks_), 32 * WPB, smem_, st_>>>(
-                jobs, njobs_, n_, rjob_, static_cast<T*>(scr_.p), scr_stride_, parts, errw, ctr, tsc_);
+            auto* kfn = tsc_ ? subtree_kernel<T, true> : subtree_kernel<T, false>;
+            kfn<<<static_cast<unsigned>(blocks_), 32 * WPB, smem_, st_>>>(jobs, njobs_, n_, rjob_,
+                                                                          static_cast<T*>(scr_.p), scr_stride_, parts,
+                                                                          errw, ctr, tsc_);
         } else {
             const uint64_t blocks = (njobs_ + 127) / 128;
             small_job_kernel<T, Q0 - 1><<<static_cast<unsigned>(blocks), 128, 0, st_>>>(jobs, njobs_, n_, rjob_,
