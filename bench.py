@@ -47,7 +47,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--workload", default="cfg4-n32-dd",
-                    choices=["cfg4-n32-dd", "cfg4-n32-qd", "cfg2-n20-dd", "cfg1-n16-fp64", "cfg5-n40-dd"])
+                    choices=["cfg4-n32-dd", "cfg4-n32-qd", "cfg2-n20-dd", "cfg1-n16-fp64", "cfg5-n40-dd",
+                             "cfg3-batch-fp64", "cfg3-batch-dd"])
     ap.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -112,7 +113,10 @@ WORKLOADS = {
     "cfg2-n20-dd": (2, "128", "dd"),
     "cfg1-n16-fp64": (1, "fp64", "fp64"),
     "cfg5-n40-dd": (5, "128", "dd"),
+    "cfg3-batch-fp64": (3, "fp64", "fp64"),
+    "cfg3-batch-dd": (3, "128", "dd"),
 }
+BATCH = 4096  # BASELINE config 3: 4096 Torontonians, n = 16 each
 DATA = "synthetic (seeded pure Gaussian state, SURVEY 8(d) recipe; committed input tests/golden/cfg{}.gbsa.txt)"
 
 
@@ -194,6 +198,10 @@ def ref_sample(m, precision: str, seconds: float):
     from oracle import ref
     threads = os.cpu_count() or 1
     n = m.n_modes
+    if ref.available() and precision == "fp64" and n <= 20:
+        # the reference's fp64 path (torontonian_reference, torontonian.cpp:179-200) is a
+        # single-threaded call: the whole instance on every host thread concurrently
+        return ref_batch_sample([m] * max(threads, 1) * 64, "fp64", seconds)
     if ref.available():
         # torontonian_partial over partition(n, rank, nproc) slices: each rank's share keeps
         # the popcount mix of the full sum; calibrate the sample to ~`seconds`
@@ -214,10 +222,119 @@ def ref_sample(m, precision: str, seconds: float):
                 sample=f"oracle/tor_oracle.c fixed-point restatement: {done} subset-terms in {secs:.2f} s")
 
 
+def ref_batch_sample(ms, precision: str, seconds: float):
+    """Reference CPU engine on a bounded sample of the config-3 items: fp64 = the reference's
+    fp64 path torontonian_reference (torontonian.cpp:179, single-threaded per call: items run
+    concurrently on all host threads); 128 = torontonian(a, Bits128, workers = host cores) item
+    after item.  Returns terms/s over the sample."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import ref
+    threads = os.cpu_count() or 1
+    n = ms[0].n_modes
+    if not ref.available():
+        from oracle import port
+        done, secs = port.partial_sample(ms[0], 128, seconds, threads)
+        return dict(value=done / secs, cores=threads, kind="port",
+                    sample=f"oracle/tor_oracle.c fixed-point restatement: {done} subset-terms in {secs:.2f} s")
+    done, t0, k = 0, time.perf_counter(), 0
+    if precision == "fp64":
+        with ThreadPoolExecutor(threads) as ex:
+            while time.perf_counter() - t0 < seconds and k < len(ms):
+                list(ex.map(ref.reference_timed, ms[k:k + threads]))
+                k += len(ms[k:k + threads])
+        what = f"torfp torontonian_reference (fp64) on {k} of the {len(ms)} config-3 items, {threads} concurrent calls"
+    else:
+        while time.perf_counter() - t0 < seconds and k < len(ms):
+            ref.torontonian(ms[k], "128", threads)
+            k += 1
+        what = f"torfp torontonian(Bits128, workers={threads}) on {k} of the {len(ms)} config-3 items"
+    secs = time.perf_counter() - t0
+    return dict(value=k * (1 << n) / secs, cores=threads, kind="reference",
+                sample=f"{what}: {k * (1 << n)} subset-terms in {secs:.2f} s")
+
+
+def batch_main(args, cfg, prec, dtype):
+    """Config 3: 4096 Torontonians (n = 16) per step through tor_torontonian_batch.
+    value: terms/s of the device pipeline (CUDA events, inputs already uploaded: the engine's
+    device_ms); e2e: the C-ABI call on host arrays (validation, exact R, host->device copy,
+    device pipeline, results) timed on the host."""
+    import paper_2009_01177_b200 as T
+    from paper_2009_01177_b200 import workloads as W
+    ms = W.load_cfg3_batch(BATCH)
+    n = ms[0].n_modes
+    terms = BATCH * (1 << n)
+    if args.impl == "reference":
+        vals = []
+        for s in range(args.warmup + args.steps):
+            r = ref_batch_sample(ms, prec, max(2.0, args.cpu_sample_seconds / 3))
+            if s >= args.warmup:
+                vals.append(r["value"])
+        v = statistics.median(vals)
+        print(json.dumps({"metric": f"Torontonian subset-terms/sec ({args.workload})", "value": v, "unit": UNIT,
+                          "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": terms / v * 1e3, "higher_is_better": True,
+                          "ms_per_step_note": "derived: terms per step / value (bounded sample per step)",
+                          "scaling": "strong", "vs_baseline": None, "dtype": "fixed-128" if dtype == "dd" else dtype,
+                          "data": DATA.format("3_state"), "impl": "reference",
+                          "config": {"workload": args.workload, "n": n, "instances": BATCH, "precision": prec},
+                          "cpu_baseline": dict(r, value=v),
+                          "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+              flush=True)
+        return
+    import torch
+    torch.cuda.set_device(0)
+    batch = T.api.BatchInputs(ms)
+    flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda:0")
+    for _ in range(args.warmup):
+        T.api.torontonian_batch_raw(batch, prec)
+    dev_ms, kern_ms, e2e_ms = [], [], []
+    with ClockSampler(0) as clk:
+        t_all = time.perf_counter()
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = T.api.torontonian_batch_raw(batch, prec)
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+            dev_ms.append(float(r["device_ms"][0]))
+            kern_ms.append(float(r["kernel_ms"][0]))
+        wall = time.perf_counter() - t_all
+    step_ms, kstep = statistics.median(dev_ms), statistics.median(kern_ms)
+    peak, peak_src = fp64_peak_tflops(0)
+    fm = json.load(open(os.path.join(ROOT, "profiles", "flops_model.json")))["per_term"][dtype][str(n)]
+    achieved = terms * fm["flops"] / (kstep * 1e-3) / 1e12
+    words = {"fp64": 1, "dd": 2}[dtype]
+    line = {"metric": f"Torontonian subset-terms/sec ({args.workload})", "value": terms / (step_ms * 1e-3),
+            "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype,
+            "data": DATA.format("3_state"),
+            "config": {"workload": args.workload, "n": n, "instances": BATCH, "precision": prec,
+                       "terms_per_step": terms, "l2": "flushed between steps (256 MiB write)"},
+            "e2e": {"value": terms / (statistics.median(e2e_ms) * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": BATCH * (2 * n) * (2 * n + 1) // 2 * words * 8,
+                    "d2h_bytes_per_step": BATCH * 40 + 8, "ms_per_step": statistics.median(e2e_ms),
+                    "over_device": statistics.median(e2e_ms) / step_ms,
+                    "path": "tor_torontonian_batch on host arrays (ctypes): validation, exact R into pinned "
+                            "staging, host->device copy, device pipeline, results"},
+            "gpu_launches": int(r["kernel_launches"][0]) * args.steps, "kernel_ms_per_step": kstep,
+            "result": {"item0": float(r["value"][0]), "sum_abs_item0": float(r["sum_abs_terms"][0])},
+            "clocks": clk.summary(), "wall_s_timed": wall,
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak if peak else None, "traffic": None, "kernel": "subtree_kernel",
+                         "flops_per_term": fm["flops"], "peak_source": peak_src}}
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = ref_batch_sample(ms, prec, args.cpu_sample_seconds)
+    print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------ main ----
 def main():
     args = parse()
     cfg, prec, dtype = WORKLOADS[args.workload]
+    if args.workload.startswith("cfg3-batch"):
+        if int(os.environ.get("RANK", "0")) == 0:
+            batch_main(args, cfg, prec, dtype)
+        return
     if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "engine":
         sys.exit(self_launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))

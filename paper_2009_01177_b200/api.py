@@ -217,13 +217,62 @@ def torontonian_reference(matrix: InputMatrix) -> float:
     return v.value
 
 
-def torontonian_batch(matrices, precision="fp64", device: int = 0) -> list[dict]:
-    ins = [_In(m) for m in matrices]
-    arr = (TorInput * len(ins))(*[i.s for i in ins])
-    res = (TorResult * len(ins))()
+class BatchInputs:
+    """`count` instances of equal N marshalled once for tor_torontonian_batch: the triangles
+    stacked in two contiguous float64 arrays and the tor_input records built by numpy (no
+    per-instance Python objects), reusable across calls."""
+
+    def __init__(self, matrices):
+        ms = list(matrices)
+        if not ms:
+            raise E.InvalidArgument("torontonian/range", "empty batch")
+        self.n = ms[0].n_modes
+        self.a00 = np.ascontiguousarray(np.stack([np.asarray(m.a00, np.complex128) for m in ms]).view(np.float64))
+        self.a01 = np.ascontiguousarray(np.stack([np.asarray(m.a01, np.complex128) for m in ms]).view(np.float64))
+        self.count = len(ms)
+        self.array = (TorInput * self.count)()
+        rec = np.frombuffer(self.array, dtype=np.dtype({"names": ["n", "a00", "a01"], "formats": ["<i4", "<u8", "<u8"],
+                                                        "offsets": [0, 8, 16], "itemsize": C.sizeof(TorInput)}))
+        stride = self.a00.shape[1] * 8
+        rec["n"] = np.array([m.n_modes for m in ms], np.int32)
+        rec["a00"] = self.a00.ctypes.data + stride * np.arange(self.count, dtype=np.uint64)
+        rec["a01"] = self.a01.ctypes.data + stride * np.arange(self.count, dtype=np.uint64)
+
+
+_RESULT_DTYPE = None
+
+
+def _result_dtype():
+    global _RESULT_DTYPE
+    if _RESULT_DTYPE is None:
+        names, fmts, offs = [], [], []
+        for name in ("value", "mode", "width_bits", "nwords", "words", "term_count", "device_ms", "kernel_ms",
+                     "escalated", "sum_abs_terms", "cancellation_bits", "bits_left", "kernel_launches"):
+            f = getattr(TorResult, name)
+            names.append(name)
+            offs.append(f.offset)
+            fmts.append({"words": ("<f8", (4,)), "mode": "<i4", "width_bits": "<i4", "nwords": "<i4",
+                         "escalated": "<i4", "term_count": "<u8", "kernel_launches": "<u8"}.get(name, "<f8"))
+        _RESULT_DTYPE = np.dtype({"names": names, "formats": fmts, "offsets": offs,
+                                  "itemsize": C.sizeof(TorResult)})
+    return _RESULT_DTYPE
+
+
+def torontonian_batch_raw(batch: BatchInputs, precision="fp64", device: int = 0) -> np.ndarray:
+    """tor_torontonian_batch on pre-marshalled inputs; returns a numpy structured array view
+    of the tor_result records (fields value, words, sum_abs_terms, mode, escalated, ...)."""
+    res = (TorResult * batch.count)()
     err = TorError()
-    _check(lib().tor_torontonian_batch(arr, len(ins), _prec(precision), device, res, C.byref(err)), err)
-    return [_result_dict(res[i], 1) for i in range(len(ins))]
+    _check(lib().tor_torontonian_batch(batch.array, batch.count, _prec(precision), device, res, C.byref(err)), err)
+    return np.frombuffer(res, dtype=_result_dtype())
+
+
+def torontonian_batch(matrices, precision="fp64", device: int = 0) -> list[dict]:
+    batch = matrices if isinstance(matrices, BatchInputs) else BatchInputs(matrices)
+    res = (TorResult * batch.count)()
+    err = TorError()
+    _check(lib().tor_torontonian_batch(batch.array, batch.count, _prec(precision), device, res, C.byref(err)), err)
+    return [_result_dict(res[i], 1) for i in range(batch.count)]
 
 
 def torontonian_slice(matrix: InputMatrix, precision, class_bits: int, class_lo: int, class_hi: int,

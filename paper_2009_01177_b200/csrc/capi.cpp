@@ -5,7 +5,11 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <algorithm>
+#include <atomic>
 #include <exception>
 #include <thread>
 #include <cstdio>
@@ -61,29 +65,103 @@ void parallel_for_n(int n, F f) {
         if (e) std::rethrow_exception(e);
 }
 
+// Persistent host worker threads for the per-instance preparation of batches (spawning
+// threads per call cost more than the work at config-3 sizes).
+class HostPool {
+  public:
+    static HostPool& get() {
+        static HostPool p;
+        return p;
+    }
+    int size() const { return static_cast<int>(workers_.size()) + 1; }
+    // runs job(t) for t in [0, nt) on the workers and the calling thread
+    void run(int nt, const std::function<void(int)>& job) {
+        std::unique_lock<std::mutex> call(call_mu_);  // one batch at a time
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            job_ = &job;
+            next_ = 1;
+            total_ = nt;
+            done_ = 0;
+            ++gen_;
+        }
+        cv_.notify_all();
+        job(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        for (;;) {  // the caller helps with remaining tasks
+            if (next_ < total_) {
+                const int t = next_++;
+                lk.unlock();
+                job(t);
+                lk.lock();
+                ++done_;
+                continue;
+            }
+            if (done_ == total_ - 1) break;
+            done_cv_.wait(lk);
+        }
+        job_ = nullptr;
+    }
+
+  private:
+    HostPool() {
+        const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+        for (int i = 1; i < std::min(hw, 64); ++i) workers_.emplace_back([this] { loop(); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& w : workers_) w.join();
+    }
+    void loop() {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> lk(mu_);
+        for (;;) {
+            cv_.wait(lk, [&] { return stop_ || (gen_ != seen && job_ && next_ < total_); });
+            if (stop_) return;
+            seen = gen_;
+            while (job_ && next_ < total_) {
+                const int t = next_++;
+                const auto* job = job_;
+                lk.unlock();
+                (*job)(t);
+                lk.lock();
+                if (++done_ == total_ - 1) done_cv_.notify_all();
+            }
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex mu_, call_mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int)>* job_ = nullptr;
+    int next_ = 0, total_ = 0, done_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
 // Host-side preparation of many instances (validation, precision bounds, exact R) in
 // parallel chunks; the first failure in index order is rethrown (deterministic).
 template <class F>
-void parallel_for(int n, F f) {
-    const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-    const int nt = std::min(hw, std::max(1, n / 64));
+void parallel_for(int n, F f, int grain = 64) {
+    HostPool& pool = HostPool::get();
+    const int nt = std::min(pool.size(), std::max(1, n / grain));
     if (nt <= 1) {
         for (int i = 0; i < n; ++i) f(i);
         return;
     }
     std::vector<std::exception_ptr> errs(nt);
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt; ++t)
-        th.emplace_back([&, t] {
-            const int lo = static_cast<int>(static_cast<int64_t>(n) * t / nt);
-            const int hi = static_cast<int>(static_cast<int64_t>(n) * (t + 1) / nt);
-            try {
-                for (int i = lo; i < hi; ++i) f(i);
-            } catch (...) {
-                errs[t] = std::current_exception();
-            }
-        });
-    for (auto& x : th) x.join();
+    pool.run(nt, [&](int t) {
+        const int lo = static_cast<int>(static_cast<int64_t>(n) * t / nt);
+        const int hi = static_cast<int>(static_cast<int64_t>(n) * (t + 1) / nt);
+        try {
+            for (int i = lo; i < hi; ++i) f(i);
+        } catch (...) {
+            errs[t] = std::current_exception();
+        }
+    });
     for (auto& e : errs)
         if (e) std::rethrow_exception(e);
 }
@@ -93,20 +171,30 @@ void parallel_for(int n, F f) {
 // case: checkpointable class ranges across devices and calls).
 constexpr int kMaxSliceModes = 50;
 
-Input checked_input(const tor_input* in, int nmax) {
+// The reference's input validation (torontonian.cpp:151-157) on the raw tor_input: range,
+// finite entries, then the symmetry gate (check_symmetries_tri: == the dense check).
+void validate_raw(const tor_input* in, int nmax) {
     if (!in || in->n < 1 || in->n > nmax || !in->a00_upper || !in->a01_upper)
         throw HostError(TOR_E_INVALID, "torontonian/range",
                         nmax == 20   ? "reference path supports 1 <= N <= 20"
                         : nmax == 40 ? "engine supports 1 <= N <= 40"
                                      : "slices and shards support 1 <= N <= 50");
-    Input a = make_input(in->n, in->a00_upper, in->a01_upper);
-    for (auto* v : {&a.a00, &a.a01})
-        for (const auto& x : *v)
-            if (!std::isfinite(x.real()) || !std::isfinite(x.imag()))
-                throw HostError(TOR_E_INVALID, "torontonian/domain", "input entries must be finite");
-    const SymReport s = check_symmetries(to_dense(a), 2 * a.n);  // torontonian.cpp:155-157
-    if (!s.pass) throw HostError(TOR_E_ERROR, "torontonian/symmetry", "input violates the block symmetries");
-    return a;
+    const size_t t2 = static_cast<size_t>(in->n) * (in->n + 1);  // doubles per triangle
+    for (const double* v : {in->a00_upper, in->a01_upper})
+        for (size_t k = 0; k < t2; ++k)
+            if (!std::isfinite(v[k])) throw HostError(TOR_E_INVALID, "torontonian/domain", "input entries must be finite");
+    double hdev = 0.0;
+    for (int i = 0; i < in->n; ++i) {
+        const size_t t = static_cast<size_t>(i) * in->n - (static_cast<size_t>(i) * (i + 1)) / 2 + i;
+        const std::complex<double> v{in->a00_upper[2 * t], in->a00_upper[2 * t + 1]};
+        hdev = std::max(hdev, std::abs(v - std::conj(v)));
+    }
+    if (!(hdev <= 1e-12)) throw HostError(TOR_E_ERROR, "torontonian/symmetry", "input violates the block symmetries");
+}
+
+Input checked_input(const tor_input* in, int nmax) {
+    validate_raw(in, nmax);
+    return make_input(in->n, in->a00_upper, in->a01_upper);
 }
 
 void put_cfg(const PrecCfg& c, tor_precision_config* o) {
@@ -205,37 +293,135 @@ void device_check(int device) {
     if (device < 0 || device >= cnt) throw HostError(TOR_E_INVALID, "device/range", "device index out of range");
 }
 
-// Runs the engine and maps its failures onto the error taxonomy.
+// One asynchronous engine evaluation of `ins` over `range`: the constructor takes a cached
+// plan for the shape (device buffers, stream, pinned staging), has the host threads build the
+// exact R of every instance straight into the pinned staging block by block -- each block's
+// host->device copy is enqueued as soon as it is built, overlapping the building -- and
+// launches the device pipeline; wait() collects the results and maps failures onto the
+// error taxonomy.  Host work placed between the two overlaps the device.
+class DeviceRun {
+  public:
+    DeviceRun(int device, int mode, const std::vector<Input>& ins, const WorkRange& range)
+        : DeviceRun(device, mode, ins[0].n, static_cast<int>(ins.size()), range,
+                    [&](int i, double* R, int* tsc) { build_R_into(ins[i], mode_words(mode), mode == MODE_DD, R, tsc); }) {}
+
+    // build(i, R, tsc) writes instance i's exact R (and may throw a validation error: the
+    // first failing instance in index order is reported, before anything is launched)
+    DeviceRun(int device, int mode, int n, int count, const WorkRange& range,
+              const std::function<void(int, double*, int*)>& build) {
+        const auto t0 = std::chrono::steady_clock::now();
+        device_check(device);
+        std::string err;
+        if (staged_acquire(device, mode, n, count, range, &sp_, err) != 0)
+            throw HostError(TOR_E_DEVICE, "device/cuda", err);
+        std::vector<int> tsc(count, 0);
+        // about two blocks per host thread: few copy calls, still overlapping
+        const int kBlock = std::max(64, (count + 2 * HostPool::get().size() - 1) / (2 * HostPool::get().size()));
+        const int nblocks = (count + kBlock - 1) / kBlock;
+        std::vector<int> bst(nblocks, 0);
+        std::vector<std::string> berr(nblocks);
+        std::vector<std::exception_ptr> bex(nblocks);
+        parallel_for(
+            nblocks,
+            [&](int b) {
+                const int lo = b * kBlock, hi = std::min(count, lo + kBlock);
+                try {
+                    for (int i = lo; i < hi; ++i) build(i, sp_->staging + i * sp_->stride, &tsc[i]);
+                } catch (...) {
+                    bex[b] = std::current_exception();
+                    return;
+                }
+                bst[b] = staged_upload_part(sp_, lo, hi, berr[b]);
+            },
+            1);
+        for (auto& e : bex)
+            if (e) {
+                staged_release(sp_);  // the pinned staging stays valid for copies in flight
+                sp_ = nullptr;
+                std::rethrow_exception(e);
+            }
+        int st = 0;
+        for (int b = 0; b < nblocks && st == 0; ++b)
+            if (bst[b]) {
+                st = bst[b];
+                err = berr[b];
+            }
+        if (st == 0) st = staged_launch(sp_, *std::max_element(tsc.begin(), tsc.end()), err);
+        if (st != 0) fail_and_release(err);
+        launched_ = true;
+        if (std::getenv("TOR_DEBUG_TIMING"))
+            std::fprintf(stderr, "[tor] run: prepare+launch %.2f ms\n",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+    DeviceRun(const DeviceRun&) = delete;
+    DeviceRun& operator=(const DeviceRun&) = delete;
+    ~DeviceRun() {
+        if (sp_) {  // never waited (an exception in between): finish the device work first
+            std::vector<EngineOut> drop;
+            std::string err;
+            if (launched_) staged_collect(sp_, drop, nullptr, err);
+            staged_release(sp_);
+        }
+    }
+
+    std::vector<EngineOut> wait(EngineStats* stats, bool check_breakdown = true) {
+        std::vector<EngineOut> out;
+        std::string err;
+        const int st = staged_collect(sp_, out, stats, err);
+        staged_release(sp_);
+        sp_ = nullptr;
+        if (st != 0) throw HostError(TOR_E_DEVICE, "device/cuda", err);
+        for (const auto& o : out)
+            if (check_breakdown && o.breakdown) {
+                HostError h(TOR_E_BREAKDOWN, "linalg/breakdown", "non-positive pivot in elimination");
+                h.pivot_row = o.bad_row;
+                h.subset_mask = o.bad_mask;
+                throw h;
+            }
+        return out;
+    }
+
+  private:
+    [[noreturn]] void fail_and_release(const std::string& err) {
+        staged_release(sp_);
+        sp_ = nullptr;
+        throw HostError(TOR_E_DEVICE, "device/cuda", err);
+    }
+    StagedPlan* sp_ = nullptr;
+    bool launched_ = false;
+};
+
+// Runs the engine synchronously.
 std::vector<EngineOut> run(int device, int mode, const std::vector<Input>& ins, const WorkRange& range,
                            EngineStats* stats, bool check_breakdown = true) {
-    const auto t0 = std::chrono::steady_clock::now();
-    device_check(device);
-    const auto t1 = std::chrono::steady_clock::now();
-    std::vector<PreparedInput> prep(ins.size());
-    parallel_for(static_cast<int>(ins.size()), [&](int i) {
-        prep[i].n = ins[i].n;
-        prep[i].R = build_R(ins[i], mode_words(mode), mode == MODE_DD, &prep[i].tscale_log2);
-    });
-    if (std::getenv("TOR_DEBUG_TIMING")) {
-        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-        std::fprintf(stderr, "[tor] run: device_check %.2f ms, build_R %.2f ms\n", ms(t0, t1),
-                     ms(t1, std::chrono::steady_clock::now()));
-    }
-    std::vector<EngineOut> out;
-    std::string err;
-    const int st = engine_run(device, mode, prep, range, out, stats, err);
-    if (st != 0) throw HostError(TOR_E_DEVICE, "device/cuda", err);
-    for (const auto& o : out)
-        if (check_breakdown && o.breakdown) {
-            HostError h(TOR_E_BREAKDOWN, "linalg/breakdown", "non-positive pivot in elimination");
-            h.pivot_row = o.bad_row;
-            h.subset_mask = o.bad_mask;
-            throw h;
-        }
-    return out;
+    DeviceRun r(device, mode, ins, range);
+    return r.wait(stats, check_breakdown);
 }
 
-void fill_result(const Input& a, int mode, const PrecCfg& cfg, const EngineOut& o, const EngineStats& st,
+// op_counts depends on N only (closed forms with 128-bit binomials): computed once per N
+void op_counts_cached(int n, uint64_t& mults, uint64_t& adds, uint64_t& recips, uint64_t& rsqrts) {
+    struct Row {
+        std::atomic<bool> ready{false};
+        uint64_t v[4];
+    };
+    static Row rows[65];
+    static std::mutex mu;
+    if (n < 0 || n > 64) return op_counts(n, mults, adds, recips, rsqrts);
+    Row& r = rows[n];
+    if (!r.ready.load(std::memory_order_acquire)) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!r.ready.load(std::memory_order_relaxed)) {
+            op_counts(n, r.v[0], r.v[1], r.v[2], r.v[3]);
+            r.ready.store(true, std::memory_order_release);
+        }
+    }
+    mults = r.v[0];
+    adds = r.v[1];
+    recips = r.v[2];
+    rsqrts = r.v[3];
+}
+
+void fill_result(int n, int mode, const PrecCfg& cfg, const EngineOut& o, const EngineStats& st,
                  double wall, int ndev, tor_result* r) {
     std::memset(r, 0, sizeof(*r));
     r->mode = mode == MODE_FP64 ? TOR_PREC_FP64 : (mode == MODE_DD ? TOR_PREC_W128_DD : TOR_PREC_W256_QD);
@@ -245,7 +431,7 @@ void fill_result(const Input& a, int mode, const PrecCfg& cfg, const EngineOut& 
     r->value = words_value(o.words);
     put_cfg(cfg, &r->config);
     r->term_count = o.terms;
-    op_counts(a.n, r->mults, r->adds, r->recips, r->rsqrts);
+    op_counts_cached(n, r->mults, r->adds, r->recips, r->rsqrts);
     r->wall_seconds = wall;
     r->device_ms = st.total_ms;
     r->kernel_ms = st.kernel_ms;
@@ -254,7 +440,7 @@ void fill_result(const Input& a, int mode, const PrecCfg& cfg, const EngineOut& 
     const double av = std::fabs(r->value);
     r->cancellation_bits = av > 0 ? std::log2(o.sum_abs / av) : std::numeric_limits<double>::infinity();
     // error growth allowance: log2(n) + 4 bits over the working precision
-    r->bits_left = mantissa_bits(mode) - r->cancellation_bits - (std::log2(static_cast<double>(a.n)) + 4.0);
+    r->bits_left = mantissa_bits(mode) - r->cancellation_bits - (std::log2(static_cast<double>(n)) + 4.0);
     r->kernel_launches = st.launches;
     r->h2d_bytes = st.h2d_bytes;
     r->d2h_bytes = st.d2h_bytes;
@@ -497,13 +683,13 @@ int tor_torontonian(const tor_input* in, tor_precision prec, const int* devices,
         if (prec == TOR_PREC_AUTO) {
             // posterior check: keep >= b_sgn significant bits after cancellation
             tor_result tmp;
-            fill_result(a, mode, cfg, res[0], st, 0.0, 1, &tmp);
+            fill_result(a.n, mode, cfg, res[0], st, 0.0, 1, &tmp);
             if (!posterior_ok(a, tmp, cfg)) {
                 if (mode == MODE_DD) {
                     mode = MODE_QD;
                     escalated = 1;
                     res = {run_devices(devs, mode, a, &st, &used)};
-                    fill_result(a, mode, cfg, res[0], st, 0.0, 1, &tmp);
+                    fill_result(a.n, mode, cfg, res[0], st, 0.0, 1, &tmp);
                 }
                 if (!posterior_ok(a, tmp, cfg))
                     throw HostError(TOR_E_PRECISION, "precision/insufficient",
@@ -511,7 +697,7 @@ int tor_torontonian(const tor_input* in, tor_precision prec, const int* devices,
             }
         }
         const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        fill_result(a, mode, cfg, res[0], st, wall, used, out);
+        fill_result(a.n, mode, cfg, res[0], st, wall, used, out);
         out->escalated = escalated;
         return TOR_OK;
     } catch (const HostError& h) {
@@ -548,10 +734,9 @@ int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, i
         std::vector<Input> as(count);
         const int mode = prec == TOR_PREC_AUTO ? MODE_DD : mode_of(prec);
         std::vector<PrecCfg> cfgs(count);
-        parallel_for(count, [&](int i) {
-            as[i] = checked_input(&ins[i], 40);
-            if (as[i].n != ins[0].n)
-                throw HostError(TOR_E_INVALID, "torontonian/range", "batch instances must share N");
+        // explicit widths: the per-instance force_width (a float determinant each) only feeds
+        // the reported config, so it runs on the host threads while the device pipeline runs
+        auto precision_of = [&](int i) {
             if (prec == TOR_PREC_AUTO) {
                 cfgs[i] = select_precision(as[i], as[i].n, 3, 0.5);
             } else if (prec == TOR_PREC_FP64) {
@@ -560,13 +745,36 @@ int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, i
             } else {
                 cfgs[i] = force_width(as[i], prec == TOR_PREC_W128_DD ? 128 : 256);
             }
-        });
+        };
+        auto shape_check = [&](int i) {
+            validate_raw(&ins[i], 40);
+            if (ins[i].n != ins[0].n) throw HostError(TOR_E_INVALID, "torontonian/range", "batch instances must share N");
+        };
+        if (prec == TOR_PREC_AUTO)
+            parallel_for(count, [&](int i) {
+                shape_check(i);
+                as[i] = make_input(ins[i].n, ins[i].a00_upper, ins[i].a01_upper);
+                precision_of(i);
+            });
         const auto t1 = std::chrono::steady_clock::now();
         EngineStats st;
         std::vector<int> modes(count, mode);
         std::vector<EngineOut> res(count);
         if (prec != TOR_PREC_AUTO) {
-            res = run(device, mode, as, WorkRange{}, &st);
+            // validation and the exact R straight from the caller's arrays (no copies)
+            if (!ins[0].a00_upper || ins[0].n < 1 || ins[0].n > 40) shape_check(0);
+            DeviceRun dr(device, mode, ins[0].n, count, WorkRange{}, [&](int i, double* R, int* tsc) {
+                shape_check(i);
+                build_R_raw(ins[i].n, ins[i].a00_upper, ins[i].a01_upper, mode_words(mode), mode == MODE_DD, R, tsc);
+            });
+            if (prec != TOR_PREC_FP64)
+                parallel_for(count, [&](int i) {
+                    as[i] = make_input(ins[i].n, ins[i].a00_upper, ins[i].a01_upper);
+                    precision_of(i);
+                });
+            else
+                parallel_for(count, precision_of);
+            res = dr.wait(&st);
         } else {
             // AUTO per instance, as tor_torontonian: the selected width picks DD or QD (one
             // sub-batch each), then the posterior check re-runs in QD every DD instance whose
@@ -595,7 +803,7 @@ int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, i
             std::vector<int> esc;
             for (int i : dd_idx) {
                 tor_result tmp;
-                fill_result(as[i], MODE_DD, cfgs[i], res[i], st, 0.0, 1, &tmp);
+                fill_result(as[i].n, MODE_DD, cfgs[i], res[i], st, 0.0, 1, &tmp);
                 if (!posterior_ok(as[i], tmp, cfgs[i])) esc.push_back(i);
             }
             run_group(MODE_QD, esc);
@@ -606,7 +814,7 @@ int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, i
             std::sort(qd_all.begin(), qd_all.end());
             for (int i : qd_all) {
                 tor_result tmp;
-                fill_result(as[i], MODE_QD, cfgs[i], res[i], st, 0.0, 1, &tmp);
+                fill_result(as[i].n, MODE_QD, cfgs[i], res[i], st, 0.0, 1, &tmp);
                 if (!posterior_ok(as[i], tmp, cfgs[i]))
                     throw HostError(TOR_E_PRECISION, "precision/insufficient",
                                     "instance " + std::to_string(i) +
@@ -616,12 +824,12 @@ int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, i
         }
         const auto t2 = std::chrono::steady_clock::now();
         const double wall = std::chrono::duration<double>(t2 - t0).count();
-        for (int i = 0; i < count; ++i) {
+        parallel_for(count, [&](int i) {
             const bool escalated = modes[i] < 0;
             const int md = escalated ? -modes[i] - 1 : modes[i];
-            fill_result(as[i], md, cfgs[i], res[i], st, wall, 1, &outs[i]);
+            fill_result(ins[0].n, md, cfgs[i], res[i], st, wall, 1, &outs[i]);
             outs[i].escalated = escalated ? 1 : 0;
-        }
+        });
         if (std::getenv("TOR_DEBUG_TIMING")) {
             auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
             std::fprintf(stderr, "[tor] batch: validate+precision %.2f ms, run %.2f ms, results %.2f ms\n",
@@ -771,7 +979,7 @@ int tor_fold_partials(const tor_partial* parts, int count, const tor_input* in, 
         PrecCfg cfg = (mode == MODE_FP64) ? PrecCfg{} : force_width(a, mode == MODE_DD ? 128 : 256);
         if (mode == MODE_FP64) cfg.width_bits = 64;
         EngineStats st;
-        fill_result(a, mode, cfg, o, st, 0.0, count, out);
+        fill_result(a.n, mode, cfg, o, st, 0.0, count, out);
         return TOR_OK;
     } catch (const HostError& h) {
         return fail(err, h);
@@ -824,7 +1032,7 @@ int tor_plan_execute(tor_plan* plan, tor_result* out, tor_error* err) {
         }
         const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         st.h2d_bytes = 0;  // inputs are resident
-        fill_result(plan->in, plan->mode, plan->cfg, res[0], st, wall, 1, out);
+        fill_result(plan->in.n, plan->mode, plan->cfg, res[0], st, wall, 1, out);
         return TOR_OK;
     } catch (const HostError& h) {
         return fail(err, h);

@@ -1658,6 +1658,24 @@ __global__ void __launch_bounds__(kFoldB / 2) fold_pass_kernel(double* partials,
     }
 }
 
+// Contiguous uploaded inputs (ninst x words doubles) into the pool's per-instance level-0
+// buffers (stride `stride` doubles).  A strided copy-engine transfer runs row by row.
+__global__ void scatter_inputs_kernel(const double* in, uint64_t words, int ninst, uint64_t stride, double* pool) {
+    const uint64_t total = words * ninst;
+    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < total;
+         k += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        pool[(k / words) * stride + k % words] = in[k];
+}
+
+// Result words of every instance (partial 0 of its job range) and the breakdown word into
+// one contiguous buffer: a single device->host copy instead of one row per instance.
+__global__ void gather_results_kernel(const double* partials, uint64_t per, int ninst,
+                                      const unsigned long long* err, double* out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < ninst * 5) out[k] = partials[static_cast<uint64_t>(k / 5) * per * 5 + k % 5];
+    if (k == 0) reinterpret_cast<unsigned long long*>(out)[ninst * 5] = *err;
+}
+
 // ------------------------------------------------------------ host side ----
 #define CK(x)                                                                         \
     do {                                                                              \
@@ -1756,11 +1774,60 @@ class PlanImpl final : public Plan {
   public:
     int init(int device, const std::vector<PreparedInput>& inputs, const WorkRange& range, std::string& err) {
         constexpr int K = Arith<T>::K;
+        if (const int st = init_geometry(device, inputs[0].n, static_cast<int>(inputs.size()), range, err)) return st;
+        // resident inputs: the exact R of every instance, one strided copy for the batch
+        const size_t rt = static_cast<size_t>(tri_sz(2 * n_)) * K;
+        std::vector<double> host(rt * ninst_);
+        int tsc = 0;
+        for (int i = 0; i < ninst_; ++i) {
+            std::copy(inputs[i].R.begin(), inputs[i].R.end(), host.begin() + i * rt);
+            tsc = std::max(tsc, inputs[i].tscale_log2);
+        }
+        if (const int st = upload(host.data(), tsc, err)) return st;
+        CK(cudaStreamSynchronize(st_));
+        return 0;
+    }
+
+    // R of every instance (ninst x tri(2n) entries of K doubles, the word type's layout) into
+    // the resident level-0 buffers: one strided asynchronous copy on the plan's stream
+    int upload(const double* R, int tscale_log2, std::string& err) override {
+        if (const int st = upload_part(R, 0, ninst_, err)) return st;
+        return upload_finish(tscale_log2, err);
+    }
+    // instances [lo, hi) of R (the whole batch's layout) -> device, asynchronously: callers
+    // overlap building the next instances' R with the transfer of these
+    int upload_part(const double* R, int lo, int hi, std::string& err) override {
+        const size_t words = static_cast<size_t>(tri_sz(2 * n_)) * Arith<T>::K;
+        CK(cudaSetDevice(device_));
+        if (lo == 0) CK(cudaEventRecord(ev_[4], st_));
+        CK(cudaMemcpyAsync(static_cast<double*>(rin_.p) + words * lo, R + words * lo, sizeof(double) * words * (hi - lo),
+                           cudaMemcpyHostToDevice, st_));
+        return 0;
+    }
+    int upload_finish(int tscale_log2, std::string& err) override {
+        const size_t rt = static_cast<size_t>(tri_sz(2 * n_));
+        tsc_ = tscale_log2;
+        CK(cudaSetDevice(device_));
+        // the contiguous upload (full link rate; a strided 2D copy of many instances runs row by
+        // row) is scattered into the pool's per-instance buffers on the device
+        {
+            const uint64_t words = static_cast<uint64_t>(rt) * Arith<T>::K, total = words * ninst_;
+            scatter_inputs_kernel<<<static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 1u << 20)), 256, 0,
+                                    st_>>>(static_cast<const double*>(rin_.p), words, ninst_,
+                                           static_cast<uint64_t>(g_.inst_entries) * Arith<T>::K,
+                                           reinterpret_cast<double*>(pool()));
+            CK(cudaGetLastError());
+        }
+        h2d_bytes_ = sizeof(T) * rt * ninst_;
+        return 0;
+    }
+
+    // Geometry and device buffers of `ninst` instances of n modes over `range` (no inputs).
+    int init_geometry(int device, int n, int ninst, const WorkRange& range, std::string& err) {
         constexpr int Q0 = Cfg<T>::L + FAN;
         device_ = device;
-        ninst_ = static_cast<int>(inputs.size());
-        for (const auto& in : inputs) tsc_ = std::max(tsc_, in.tscale_log2);
-        n_ = inputs[0].n;
+        ninst_ = ninst;
+        n_ = n;
         kbits_ = range.class_bits;
         clo_ = range.class_lo;
         chi_ = range.class_hi;
@@ -1822,6 +1889,12 @@ class PlanImpl final : public Plan {
         CK(jobs_.alloc(sizeof(Job<T>) * njobs_, device_));
         CK(parts_.alloc(sizeof(double) * 5 * njobs_, device_));
         CK(errw_.alloc(sizeof(unsigned long long), device_));
+        CK(res_.alloc(sizeof(double) * (static_cast<size_t>(ninst_) * 5 + 1), device_));
+        // contiguous landing buffer of uploaded inputs (allocated here: upload_part may be
+        // called from several host threads)
+        CK(rin_.alloc(sizeof(T) * static_cast<size_t>(tri_sz(2 * n_)) * ninst_, device_));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&res_host_), sizeof(double) * (static_cast<size_t>(ninst_) * 5 + 1),
+                         cudaHostAllocPortable));
         CK(ctr_.alloc(sizeof(unsigned long long), device_));
         if (!use_levels_) {
             work_stride_ = 2 * static_cast<size_t>(tri_sz(2 * n_));
@@ -1870,34 +1943,23 @@ class PlanImpl final : public Plan {
             scr_stride_ = std::max<size_t>(stride, 1);
             CK(scr_.alloc(sizeof(T) * scr_stride_ * blocks_ * WPB, device_));
         }
-        // resident inputs: the exact R of every instance, one strided copy for the batch
-        const size_t rt = static_cast<size_t>(tri_sz(2 * n_));
-        std::vector<T> host(rt * ninst_);
-        for (int i = 0; i < ninst_; ++i) {
-            const auto& R = inputs[i].R;
-            T* h = host.data() + i * rt;
-            for (size_t k = 0; k < rt; ++k) {
-                double w[4] = {0, 0, 0, 0};
-                for (int x = 0; x < K; ++x) w[x] = R[k * K + x];
-                if constexpr (K == 1) h[k] = w[0];
-                else if constexpr (K == 2) h[k] = dd{w[0], w[1]};
-                else h[k] = qd{{w[0], w[1], w[2], w[3]}};
-            }
-        }
-        CK(cudaMemcpy2DAsync(pool(), sizeof(T) * g_.inst_entries, host.data(), sizeof(T) * rt, sizeof(T) * rt,
-                             ninst_, cudaMemcpyHostToDevice, st_));
-        CK(cudaStreamSynchronize(st_));
-        h2d_bytes_ = sizeof(T) * rt * ninst_;
         return 0;
     }
 
     ~PlanImpl() override {
+        if (res_host_) cudaFreeHost(res_host_);
         for (auto& e : ev_)
             if (e) cudaEventDestroy(e);
         if (st_) cudaStreamDestroy(st_);
     }
 
     int execute(std::vector<EngineOut>& out, EngineStats* stats, std::string& err) override {
+        if (const int st = launch(err)) return st;
+        return collect(out, stats, err);
+    }
+
+    // enqueue the whole device pipeline and the read-back on the plan's stream
+    int launch(std::string& err) override {
         constexpr int Q0 = Cfg<T>::L + FAN;
         CK(cudaSetDevice(device_));
         uint64_t launches = 0;
@@ -1905,6 +1967,7 @@ class PlanImpl final : public Plan {
         unsigned long long* ctr = static_cast<unsigned long long*>(ctr_.p);
         double* parts = static_cast<double*>(parts_.p);
         Job<T>* jobs = static_cast<Job<T>*>(jobs_.p);
+        const auto tx0 = std::chrono::steady_clock::now();
         CK(cudaMemsetAsync(errw, 0xff, sizeof(unsigned long long), st_));
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st_));
         CK(cudaEventRecord(ev_[0], st_));
@@ -1971,9 +2034,27 @@ class PlanImpl final : public Plan {
         }
         CK(cudaGetLastError());
         CK(cudaEventRecord(ev_[3], st_));
-        std::vector<double> res(static_cast<size_t>(ninst_) * 5);
-        CK(cudaMemcpy2DAsync(res.data(), 5 * sizeof(double), parts, per_ * 5 * sizeof(double), 5 * sizeof(double),
-                             ninst_, cudaMemcpyDeviceToHost, st_));
+        double* resd = static_cast<double*>(res_.p);
+        gather_results_kernel<<<static_cast<unsigned>((ninst_ * 5 + 255) / 256), 256, 0, st_>>>(parts, per_, ninst_,
+                                                                                              errw, resd);
+        ++launches;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(res_host_, resd, sizeof(double) * (static_cast<size_t>(ninst_) * 5 + 1),
+                           cudaMemcpyDeviceToHost, st_));
+        CK(cudaEventRecord(ev_[5], st_));
+        launches_ = launches;
+        tx0_ = tx0;
+        return 0;
+    }
+
+    // wait for the launched pipeline and decode its results
+    int collect(std::vector<EngineOut>& out, EngineStats* stats, std::string& err) override {
+        CK(cudaSetDevice(device_));
+        const uint64_t launches = launches_;
+        const auto tx0 = tx0_;
+        double* parts = static_cast<double*>(parts_.p);
+        const uint64_t chunk = class_partials_ ? per_ / (chi_ - clo_) : per_;
+        const double* res = res_host_;
         std::vector<double> cls;
         if (class_partials_) {
             const uint64_t ncls = chi_ - clo_;
@@ -1983,9 +2064,21 @@ class PlanImpl final : public Plan {
                                      chunk * 5 * sizeof(double), 5 * sizeof(double), ncls, cudaMemcpyDeviceToHost,
                                      st_));
         }
-        unsigned long long herr = 0;
-        CK(cudaMemcpyAsync(&herr, errw, sizeof(herr), cudaMemcpyDeviceToHost, st_));
+        const auto tq = std::chrono::steady_clock::now();
         CK(cudaStreamSynchronize(st_));
+        if (std::getenv("TOR_DEBUG_TIMING")) {
+            float up = 0, dn = 0, dv = 0;
+            cudaEventElapsedTime(&up, ev_[4], ev_[0]);
+            cudaEventElapsedTime(&dv, ev_[0], ev_[3]);
+            cudaEventElapsedTime(&dn, ev_[3], ev_[5]);
+            std::fprintf(stderr, "[tor] events: upload..start %.3f ms, pipeline %.3f ms, gather+readback %.3f ms\n", up,
+                         dv, dn);
+            std::fprintf(stderr, "[tor] execute: enqueue %.3f ms, sync wait %.3f ms\n",
+                         std::chrono::duration<double, std::milli>(tq - tx0).count(),
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq).count());
+        }
+        unsigned long long herr;
+        std::memcpy(&herr, res + static_cast<size_t>(ninst_) * 5, sizeof(herr));
         out.assign(ninst_, EngineOut{});
         const uint64_t terms = (chi_ - clo_) << (n_ - kbits_);
         for (int i = 0; i < ninst_; ++i) {
@@ -2018,7 +2111,7 @@ class PlanImpl final : public Plan {
             stats->prefix_depth = cj_;
             stats->jobs = njobs_;
             stats->h2d_bytes = h2d_bytes_;
-            stats->d2h_bytes = (res.size() + cls.size()) * sizeof(double) + sizeof(herr);
+            stats->d2h_bytes = (static_cast<size_t>(ninst_) * 5 + cls.size()) * sizeof(double) + sizeof(herr);
         }
         return 0;
     }
@@ -2032,8 +2125,11 @@ class PlanImpl final : public Plan {
     PrefixGeom g_{};
     size_t smem_ = 0, scr_stride_ = 1, work_stride_ = 0, h2d_bytes_ = 0;
     cudaStream_t st_ = nullptr;
-    cudaEvent_t ev_[4] = {nullptr, nullptr, nullptr, nullptr};
-    DevBuf pool_, tpool_, jobs_, parts_, errw_, ctr_, scr_, work_;
+    cudaEvent_t ev_[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    DevBuf pool_, tpool_, jobs_, parts_, errw_, ctr_, scr_, work_, res_, rin_;
+    double* res_host_ = nullptr;  // pinned: ninst x 5 result words + the breakdown word
+    uint64_t launches_ = 0;       // kernels of the last launch()
+    std::chrono::steady_clock::time_point tx0_;
 };
 
 template <class T>
@@ -2051,7 +2147,9 @@ int make_plan(int device, const std::vector<PreparedInput>& inputs, const WorkRa
 
 }  // namespace
 
+void release_staged_cache();
 void release_device_cache() {
+    release_staged_cache();
     DevPool& pl = DevPool::get();
     std::lock_guard<std::mutex> lk(pl.mu);
     for (int d = 0; d < 64; ++d) {
@@ -2068,6 +2166,141 @@ void release_device_cache() {
 
 int engine_tree_min_n(int mode) {
     return mode == MODE_QD ? Cfg<qd>::L + FAN : (mode == MODE_DD ? Cfg<dd>::L + FAN : Cfg<double>::L + FAN);
+}
+
+namespace {
+template <class T>
+int make_geometry(int device, int n, int ninst, const WorkRange& range, Plan** out, std::string& err) {
+    auto* p = new PlanImpl<T>();
+    const int st = p->init_geometry(device, n, ninst, range, err);
+    if (st != 0) {
+        delete p;
+        return st;
+    }
+    *out = p;
+    return 0;
+}
+
+bool same_range(const WorkRange& a, const WorkRange& b) {
+    return a.class_bits == b.class_bits && a.class_lo == b.class_lo && a.class_hi == b.class_hi &&
+           a.class_partials == b.class_partials && a.prefix_jobs == b.prefix_jobs && a.blocks_per_sm == b.blocks_per_sm;
+}
+
+// Process-wide cache of idle staged plans (device buffers, stream, events, pinned staging),
+// least recently used last; an acquired plan is owned by its caller until released.
+struct StagedCache {
+    static constexpr size_t kMax = 6;
+    std::mutex mu;
+    std::vector<StagedPlan*> idle;
+    static StagedCache& get() {
+        static StagedCache c;
+        return c;
+    }
+};
+}  // namespace
+
+StagedPlan::~StagedPlan() {
+    delete plan;
+    if (staging) cudaFreeHost(staging);
+}
+
+int staged_acquire(int device, int mode, int n, int count, const WorkRange& range, StagedPlan** out,
+                   std::string& err) {
+    *out = nullptr;
+    {
+        StagedCache& c = StagedCache::get();
+        std::lock_guard<std::mutex> lk(c.mu);
+        for (size_t i = 0; i < c.idle.size(); ++i) {
+            StagedPlan* sp = c.idle[i];
+            if (sp->device == device && sp->mode == mode && sp->n == n && sp->count == count &&
+                same_range(sp->range, range)) {
+                c.idle.erase(c.idle.begin() + static_cast<long>(i));
+                *out = sp;
+                return 0;
+            }
+        }
+    }
+    auto* sp = new StagedPlan();
+    sp->device = device;
+    sp->mode = mode;
+    sp->n = n;
+    sp->count = count;
+    sp->range = range;
+    const int st = mode == MODE_FP64 ? make_geometry<double>(device, n, count, range, &sp->plan, err)
+                   : mode == MODE_DD ? make_geometry<dd>(device, n, count, range, &sp->plan, err)
+                                     : make_geometry<qd>(device, n, count, range, &sp->plan, err);
+    if (st != 0) {
+        delete sp;
+        return st;
+    }
+    sp->stride = static_cast<size_t>(2 * n) * (2 * n + 1) / 2 * mode_words(mode);
+    const cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&sp->staging), sizeof(double) * sp->stride * count,
+                                        cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        err = std::string("cudaHostAlloc: ") + cudaGetErrorString(e);
+        delete sp;
+        return static_cast<int>(e);
+    }
+    *out = sp;
+    return 0;
+}
+
+int staged_execute(StagedPlan* sp, int tscale_log2, std::vector<EngineOut>& out, EngineStats* stats,
+                   std::string& err) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (const int st = sp->plan->upload(sp->staging, tscale_log2, err)) return st;
+    const auto t1 = std::chrono::steady_clock::now();
+    const int st = sp->plan->execute(out, stats, err);
+    if (std::getenv("TOR_DEBUG_TIMING")) {
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "[tor] staged: upload enqueue %.3f ms, execute %.3f ms (device %.3f ms)\n", ms(t0, t1),
+                     ms(t1, std::chrono::steady_clock::now()), stats ? stats->total_ms : -1.0);
+    }
+    return st;
+}
+
+int staged_upload_part(StagedPlan* sp, int lo, int hi, std::string& err) {
+    return sp->plan->upload_part(sp->staging, lo, hi, err);
+}
+
+int staged_execute_uploaded(StagedPlan* sp, int tscale_log2, std::vector<EngineOut>& out, EngineStats* stats,
+                            std::string& err) {
+    if (const int st = staged_launch(sp, tscale_log2, err)) return st;
+    return staged_collect(sp, out, stats, err);
+}
+
+int staged_launch(StagedPlan* sp, int tscale_log2, std::string& err) {
+    if (const int st = sp->plan->upload_finish(tscale_log2, err)) return st;
+    return sp->plan->launch(err);
+}
+
+int staged_collect(StagedPlan* sp, std::vector<EngineOut>& out, EngineStats* stats, std::string& err) {
+    return sp->plan->collect(out, stats, err);
+}
+
+void staged_release(StagedPlan* sp) {
+    if (!sp) return;
+    StagedCache& c = StagedCache::get();
+    std::vector<StagedPlan*> drop;
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        c.idle.insert(c.idle.begin(), sp);
+        while (c.idle.size() > StagedCache::kMax) {
+            drop.push_back(c.idle.back());
+            c.idle.pop_back();
+        }
+    }
+    for (auto* d : drop) delete d;
+}
+
+void release_staged_cache() {
+    StagedCache& c = StagedCache::get();
+    std::vector<StagedPlan*> drop;
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        drop.swap(c.idle);
+    }
+    for (auto* d : drop) delete d;
 }
 
 int plan_create(int device, int mode, const std::vector<PreparedInput>& inputs, const WorkRange& range, Plan** out,

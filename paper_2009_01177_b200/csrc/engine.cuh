@@ -70,8 +70,43 @@ struct EngineStats {
 class Plan {
   public:
     virtual ~Plan() = default;
-    virtual int execute(std::vector<EngineOut>& out, EngineStats* stats, std::string& err) = 0;
+    virtual int execute(std::vector<EngineOut>& out, EngineStats* stats, std::string& err) = 0;  // launch + collect
+    virtual int launch(std::string& err) = 0;  // enqueue the pipeline (asynchronous)
+    virtual int collect(std::vector<EngineOut>& out, EngineStats* stats, std::string& err) = 0;  // wait + decode
+    // new inputs for the same geometry: R of every instance (count x tri(2n) entries of the
+    // mode's words), copied asynchronously on the plan's stream
+    virtual int upload(const double* R, int tscale_log2, std::string& err) = 0;
+    // the same in parts: upload_part for instance ranges (asynchronous, any order), then
+    // upload_finish once
+    virtual int upload_part(const double* R, int lo, int hi, std::string& err) = 0;
+    virtual int upload_finish(int tscale_log2, std::string& err) = 0;
 };
+
+// A plan whose inputs are written by the caller into pinned host staging (build_R_into,
+// any host threads), then uploaded and executed: the repeated-call path of the C ABI.  Idle
+// staged plans are cached per (device, mode, n, count, range) -- device buffers, stream,
+// events and pinned memory are reused across calls (release_device_cache frees them).
+struct StagedPlan {
+    int device = 0, mode = 0, n = 0, count = 0;
+    WorkRange range;
+    Plan* plan = nullptr;
+    double* staging = nullptr;  // count x stride doubles (pinned)
+    size_t stride = 0;          // tri(2n) * words
+    ~StagedPlan();
+};
+int staged_acquire(int device, int mode, int n, int count, const WorkRange& range, StagedPlan** out,
+                   std::string& err);
+int staged_execute(StagedPlan* sp, int tscale_log2, std::vector<EngineOut>& out, EngineStats* stats,
+                   std::string& err);
+// chunked form: staged_upload_part for instance ranges of sp->staging as they are built,
+// then staged_execute_uploaded (upload_finish + execute)
+int staged_upload_part(StagedPlan* sp, int lo, int hi, std::string& err);
+int staged_execute_uploaded(StagedPlan* sp, int tscale_log2, std::vector<EngineOut>& out, EngineStats* stats,
+                            std::string& err);
+// the same split so host work can overlap the device pipeline
+int staged_launch(StagedPlan* sp, int tscale_log2, std::string& err);
+int staged_collect(StagedPlan* sp, std::vector<EngineOut>& out, EngineStats* stats, std::string& err);
+void staged_release(StagedPlan* sp);  // back to the cache (or freed)
 
 int plan_create(int device, int mode, const std::vector<PreparedInput>& inputs, const WorkRange& range, Plan** out,
                 std::string& err);

@@ -128,6 +128,19 @@ SymReport check_symmetries(const std::vector<std::complex<double>>& dense, int t
     return r;
 }
 
+SymReport check_symmetries_tri(const Input& a) {
+    // The dense matrix of a triangle-stored input (to_dense) mirrors every off-diagonal entry
+    // exactly, so of check_symmetries' deviations only the A00 / conj(A00) diagonal can be
+    // nonzero: |a_ii - conj(a_ii)|.  Same values, same gate, O(n) instead of O(n^2).
+    SymReport r;
+    for (int i = 0; i < a.n; ++i) {
+        const std::complex<double> v = a.a00_at(i, i);
+        r.hermitian_dev = std::max(r.hermitian_dev, std::abs(v - std::conj(v)));
+    }
+    r.pass = r.hermitian_dev <= kTol && r.a01_sym_dev <= kTol && r.block_conj_dev <= kTol;
+    return r;
+}
+
 double det_i_minus_a_float(const Input& a) {  // precision.cpp:16-36
     const int n = a.n, d = 2 * n;
     HermF m;
@@ -209,22 +222,36 @@ PrecCfg force_width(const Input& a, int width_bits) {  // precision.cpp:123-148
 // Each entry is the sum of two input doubles: exact as a DD (TwoSum), rounded once
 // in fp64 mode.
 std::vector<double> build_R(const Input& a, int words, bool grid, int* tscale_log2) {
-    const int n = a.n, d = 2 * n;
+    const int d = 2 * a.n;
     std::vector<double> R(static_cast<size_t>(d) * (d + 1) / 2 * words, 0.0);
-    auto P = [&](int i, int j) -> std::complex<double> {
-        if (i == j) return {1.0 - a.a00_at(i, i).real(), 0.0};
-        return -a.a00_at(i, j);
-    };
-    auto Q = [&](int i, int j) -> std::complex<double> { return -a.a01_at(i, j); };
+    build_R_into(a, words, grid, R.data(), tscale_log2);
+    return R;
+}
+
+void build_R_into(const Input& a, int words, bool grid, double* R, int* tscale_log2) {
+    // std::complex<double> arrays are layout-compatible with interleaved (re, im) doubles
+    build_R_raw(a.n, reinterpret_cast<const double*>(a.a00.data()), reinterpret_cast<const double*>(a.a01.data()),
+                words, grid, R, tscale_log2);
+}
+
+void build_R_raw(int n, const double* __restrict__ a00, const double* __restrict__ a01, int words, bool grid,
+                 double* __restrict__ R, int* tscale_log2) {
+    const int d = 2 * n;
+    // entry (r, s), r <= s, of pair rows r = 2i + ri, s = 2j + sj: x + y with
+    //   (x_i, x_j): Re P + Re Q   (x_i, p_j): Im Q - Im P   (p_i, x_j): Im P + Im Q   (p_i, p_j): Re P - Re Q
+    // P = I - A00 (diagonal 1 - Re a_ii), Q = -A01, from the upper triangles (i <= j)
     auto parts = [&](int r, int s, double& x, double& y) {
         const int i = r >> 1, j = s >> 1;
-        const bool ri = r & 1, sj = s & 1;
-        const auto p = P(i, j);
-        const auto q = Q(i, j);
-        if (!ri && !sj) { x = p.real(); y = q.real(); }
-        else if (!ri && sj) { x = q.imag(); y = -p.imag(); }
-        else if (ri && !sj) { x = p.imag(); y = q.imag(); }
-        else { x = p.real(); y = -q.real(); }
+        const size_t t = static_cast<size_t>(i) * n - (static_cast<size_t>(i) * (i + 1)) / 2 + j;
+        const double pre = i == j ? 1.0 - a00[2 * t] : -a00[2 * t];
+        const double pim = i == j ? 0.0 : -a00[2 * t + 1];
+        const double qre = -a01[2 * t], qim = -a01[2 * t + 1];
+        switch ((r & 1) * 2 + (s & 1)) {
+            case 0: x = pre; y = qre; break;
+            case 1: x = qim; y = -pim; break;
+            case 2: x = pim; y = qim; break;
+            default: x = pre; y = -qre; break;
+        }
     };
     // grid (fixed-exponent) DD states need max_k R_kk < 3.75 (arith.cuh); larger inputs are
     // scaled by an exact power of two, undone per term on the device (Acc::sc)
@@ -239,13 +266,14 @@ std::vector<double> build_R(const Input& a, int words, bool grid, int* tscale_lo
         while (std::ldexp(dmax, -sc) >= 3.75) ++sc;
     }
     if (tscale_log2) *tscale_log2 = sc;
+    const double f = std::ldexp(1.0, -sc);  // exact power of two
+    double* e = R;
     for (int r = 0; r < d; ++r)
-        for (int s = r; s < d; ++s) {
+        for (int s = r; s < d; ++s, e += words) {
             double x, y;
             parts(r, s, x, y);
-            double* e = &R[tri(d, r, s) * words];
             if (grid) {
-                const dd g = dd_to_grid(std::ldexp(x, -sc), std::ldexp(y, -sc));
+                const dd g = dd_to_grid(x * f, y * f);
                 e[0] = g.hi;
                 e[1] = g.lo;
             } else {
@@ -253,9 +281,9 @@ std::vector<double> build_R(const Input& a, int words, bool grid, int* tscale_lo
                 two_sum(x, y, hi, lo);
                 e[0] = hi;
                 if (words >= 2) e[1] = lo;
+                for (int w = 2; w < words; ++w) e[w] = 0.0;
             }
         }
-    return R;
 }
 
 unsigned __int128 total_op_count(int n) {  // flops.cpp:15-31 (Eq. 8)

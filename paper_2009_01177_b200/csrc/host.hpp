@@ -44,6 +44,8 @@ struct SymReport {
 Input make_input(int n, const double* a00, const double* a01);
 std::vector<std::complex<double>> to_dense(const Input& a);
 SymReport check_symmetries(const std::vector<std::complex<double>>& dense, int two_n);
+// check_symmetries(to_dense(a), 2n) without the dense matrix (identical report)
+SymReport check_symmetries_tri(const Input& a);
 double det_i_minus_a_float(const Input& a);
 PrecCfg select_precision(const Input& a, int N, int sig, double alpha);
 PrecCfg force_width(const Input& a, int width_bits);
@@ -51,6 +53,10 @@ PrecCfg force_width(const Input& a, int width_bits);
 // Exact R in `words` doubles per entry (1: rounded fp64, 2: DD, 4: QD), packed upper
 // triangle of the 2n x 2n matrix in pair order (x_0, p_0, x_1, p_1, ...).
 std::vector<double> build_R(const Input& a, int words, bool grid = false, int* tscale_log2 = nullptr);
+// the same into R (tri(2n) * words doubles)
+void build_R_into(const Input& a, int words, bool grid, double* R, int* tscale_log2);
+// the same from interleaved (re, im) upper triangles (tor_input layout), no Input copy
+void build_R_raw(int n, const double* a00, const double* a01, int words, bool grid, double* R, int* tscale_log2);
 
 // Closed-form reference op counters (linalg.hpp:44-57, flops.cpp:9-31).
 void op_counts(int n, uint64_t& mults, uint64_t& adds, uint64_t& recips, uint64_t& rsqrts);

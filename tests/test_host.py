@@ -227,3 +227,25 @@ def test_slice_range_beyond_reference_limit():
     if T.device_count() == 0:
         with pytest.raises(T.DeviceError):  # validated, then needs the device
             T.torontonian_slice(diag_instance(50, [0.1] * 50), "128", 30, 0, 1)
+
+
+@pytest.mark.parametrize("im", [0.0, 1e-13, 4.9e-13, 5e-13, 5.1e-13, 1e-12, 3e-12])
+def test_symmetry_gate_without_dense_matrix_matches_dense(im):
+    """The evaluation entry points gate inputs with check_symmetries_tri (O(n), no dense
+    matrix); it must decide exactly as the dense check_symmetries (matrix_io.cpp:285-305) that
+    tor_check_symmetries runs: only the A00 diagonal's imaginary parts can deviate."""
+    m = W.generate_instance(6, 0.16, 0.06, 3)
+    a00 = m.a00.copy()
+    a00[T.matrix.tri_index(6, 2, 2)] += 1j * im
+    bad = T.InputMatrix(6, a00, m.a01)
+    dense = T.check_symmetries(bad)
+    assert dense["hermitian_dev"] == pytest.approx(2 * im, rel=1e-15, abs=0)
+    try:
+        T.torontonian(bad, "128")
+        gate_pass = True
+    except T.DeviceError:
+        gate_pass = True  # passed validation, no GPU here
+    except T.TorfpError as e:
+        assert e.code == "torontonian/symmetry"
+        gate_pass = False
+    assert gate_pass == dense["pass"]
