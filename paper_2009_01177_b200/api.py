@@ -227,14 +227,19 @@ class BatchInputs:
         if not ms:
             raise E.InvalidArgument("torontonian/range", "empty batch")
         self.n = ms[0].n_modes
-        self.a00 = np.ascontiguousarray(np.stack([np.asarray(m.a00, np.complex128) for m in ms]).view(np.float64))
-        self.a01 = np.ascontiguousarray(np.stack([np.asarray(m.a01, np.complex128) for m in ms]).view(np.float64))
         self.count = len(ms)
         self.array = (TorInput * self.count)()
+        if any(m.n_modes != self.n for m in ms):  # mixed N: the C side reports it
+            self._keep = [_In(m) for m in ms]
+            for i, k in enumerate(self._keep):
+                self.array[i] = k.s
+            return
+        self.a00 = np.ascontiguousarray(np.stack([np.asarray(m.a00, np.complex128) for m in ms]).view(np.float64))
+        self.a01 = np.ascontiguousarray(np.stack([np.asarray(m.a01, np.complex128) for m in ms]).view(np.float64))
         rec = np.frombuffer(self.array, dtype=np.dtype({"names": ["n", "a00", "a01"], "formats": ["<i4", "<u8", "<u8"],
                                                         "offsets": [0, 8, 16], "itemsize": C.sizeof(TorInput)}))
         stride = self.a00.shape[1] * 8
-        rec["n"] = np.array([m.n_modes for m in ms], np.int32)
+        rec["n"] = self.n
         rec["a00"] = self.a00.ctypes.data + stride * np.arange(self.count, dtype=np.uint64)
         rec["a01"] = self.a01.ctypes.data + stride * np.arange(self.count, dtype=np.uint64)
 

@@ -750,21 +750,21 @@ int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, i
             validate_raw(&ins[i], 40);
             if (ins[i].n != ins[0].n) throw HostError(TOR_E_INVALID, "torontonian/range", "batch instances must share N");
         };
-        if (prec == TOR_PREC_AUTO)
-            parallel_for(count, [&](int i) {
-                shape_check(i);
+        // validation first (the first bad instance in index order, before any device work)
+        parallel_for(count, [&](int i) {
+            shape_check(i);
+            if (prec == TOR_PREC_AUTO) {
                 as[i] = make_input(ins[i].n, ins[i].a00_upper, ins[i].a01_upper);
                 precision_of(i);
-            });
+            }
+        });
         const auto t1 = std::chrono::steady_clock::now();
         EngineStats st;
         std::vector<int> modes(count, mode);
         std::vector<EngineOut> res(count);
         if (prec != TOR_PREC_AUTO) {
-            // validation and the exact R straight from the caller's arrays (no copies)
-            if (!ins[0].a00_upper || ins[0].n < 1 || ins[0].n > 40) shape_check(0);
+            // the exact R straight from the caller's arrays (no copies)
             DeviceRun dr(device, mode, ins[0].n, count, WorkRange{}, [&](int i, double* R, int* tsc) {
-                shape_check(i);
                 build_R_raw(ins[i].n, ins[i].a00_upper, ins[i].a01_upper, mode_words(mode), mode == MODE_DD, R, tsc);
             });
             if (prec != TOR_PREC_FP64)
