@@ -680,23 +680,18 @@ __host__ __device__ constexpr int tri_col(int D, int k) {
     }
     return i + k;
 }
-// TMEM column layout of a lane's level-FAN state (packed D = 2L row triangle, D = 8).
-// The level-FAN include child is formed by a lane pair (see FanLevel): entries with
-// i + j < D-1 ("A" set, 16 entries, row-major order A[0..15]) by the even lane,
-// their mirrors (D-1-j, D-1-i) by the odd lane, the 4 anti-diagonal entries
-// (n, D-1-n) by both.  TMEM slot 4c+p holds A[2c+p], slot 4c+2+p its mirror
-// (c < 8), slot 32+n anti-diagonal entry n.  Column of entry k = 4 * slot(k).
+// TMEM layout of a lane's level-FAN state (packed D = 2L row triangle, D = 8).  The
+// level-FAN include child is formed by a thread pair (see FanLevel): entries with i + j < D-1
+// ("A" set, 16 entries, row-major order A[0..15]) by one thread, their mirrors
+// (D-1-j, D-1-i) by the other, the 4 anti-diagonal entries (n, D-1-n) by both (split_col).
 constexpr int kMirD = 8;
-// Level-5 (TMEM) lane maps, found by tools/l5_layout_search.py for the padded fan-out
-// layout: 128-bit shared-memory loads are served per 8-lane phase, so which parents share a
-// phase decides the bank conflicts.  kL5VecMap: lane & 15 -> parent for the pivot / vector
-// phase (conflict-free); kL5PairMap: lane pair -> parent for the mirror-split update (272 vs
-// 459 wavefronts per leaf for the identity map, ideal 208).  Nibble i = map(i).
-constexpr uint64_t kL5PairMap = 0x0e249f35d71bac68ull;
+// Level-5 (TMEM) lane maps, found by bank-conflict searches for the padded fan-out layout
+// (tools/l5_layout_search.py): 128-bit shared-memory loads are served per 8-lane phase, so
+// which parents share a phase decides the bank conflicts.  kL5VecMap: lane & 15 -> parent for
+// the pivot / vector phase (conflict-free).  Nibble i = map(i).
 constexpr uint64_t kL5VecMap = 0x79b0ec2568adf134ull;
 __host__ __device__ __forceinline__ int l5_map(uint64_t map, int i) { return static_cast<int>((map >> (4 * i)) & 15); }
-// level-5 node held by a consumer lane (lane pair -> parent x: nodes 2x, 2x + 1)
-__host__ __device__ __forceinline__ int l5_lane_node(int lane) { return 2 * l5_map(kL5PairMap, lane >> 1) + (lane & 1); }
+
 __host__ __device__ constexpr int mir_a_index(int i, int j) {  // index of (i,j) in A
     int n = 0;
     for (int a = 0; a < kMirD; ++a)
@@ -719,16 +714,18 @@ __host__ __device__ constexpr int mir_a_col(int n) {
             if (a + b < kMirD - 1 && n-- == 0) return b;
     return -1;
 }
-__host__ __device__ constexpr int mir_slot(int k) {
+// Split level-5 layout: a level-5 state row holds the 16 "A" entries (i + j < 7) in A order
+// at columns 4a, their 16 mirrors at 64 + 4a and the 4 anti-diagonal entries at 128 + 4n
+// (the row-0/1 entries the lane subtree loads first are then mostly consecutive A entries)
+__host__ __device__ constexpr int split_col(int k) {
     const int i = tri_row(kMirD, k), j = tri_col(kMirD, k);
-    if (i + j == kMirD - 1) return 32 + i;
-    const int n = i + j < kMirD - 1 ? mir_a_index(i, j) : mir_a_index(kMirD - 1 - j, kMirD - 1 - i);
-    return 4 * (n >> 1) + (i + j < kMirD - 1 ? 0 : 2) + (n & 1);
+    if (i + j == kMirD - 1) return 128 + 4 * i;
+    return i + j < kMirD - 1 ? 4 * mir_a_index(i, j) : 64 + 4 * mir_a_index(kMirD - 1 - j, kMirD - 1 - i);
 }
 // TMEM column of entry k of a D-row lane state
 template <int D>
 __host__ __device__ constexpr int tm_col(int k) {
-    if constexpr (D == kMirD) return 4 * mir_slot(k);
+    if constexpr (D == kMirD) return split_col(k);
     else return 4 * k;
 }
 
@@ -762,7 +759,8 @@ template <int D, int K, int N> struct TmLd {
             constexpr int col = tm_col<D>(K);
             // natural column layout (the scratch states): four consecutive entries per
             // 16-column load
-            if constexpr (N >= 4 && D != kMirD) {
+            if constexpr (N >= 4 && tm_col<D>(K + 1) == col + 4 && tm_col<D>(K + 2) == col + 8 &&
+                          tm_col<D>(K + 3) == col + 12) {
                 tm_ld16(row + col, r);
                 TmLd<D, K + 4, N - 4>::run(row, r + 16);
             } else {
@@ -1062,9 +1060,34 @@ __device__ __forceinline__ NodeRef node_ref(const uint32_t* tabs, int e, int c) 
 // (x, g) = (lane % E, lane / E) works on parent x throughout (pivots redundantly in
 // registers, pivot-row vectors j = 2+g+sG, trailing entries k = g+sG, G = 32/E), so
 // every source, table and destination address is a per-lane base plus a constant.
-// Chunk C (< 8) of the mirror-split level-FAN update (see FanLevel): A entries
-// 2C, 2C+1 and their mirrors, all indices compile-time.
-template <class T, int M, int C> struct MirChunk {
+// Split level 5: threads x and x + 16 (x < 16) share parent kL5Split(x); their 128-bit
+// loads of the parent's trailing block are served per 8-thread phase {0-7, 8-15, 16-23,
+// 24-31}, so the parents of threads 0-7 (and of 8-15) must start on distinct 16-byte bank
+// slots: the padded layout puts the 16 level-4 nodes on every slot exactly twice, and the map
+// takes one of each slot for each half.
+// conflict-free for the parent, anti-diagonal and pivot-row vector loads of the split
+// chunks (144 wavefronts per leaf, the ideal; identity 224): tools/l5_split_search.py
+constexpr uint64_t kL5Split = 0x3fc9a650e821b7d4ull;
+// level-5 node in a consumer lane's TMEM row: lanes 0-15 the include children, 16-31 the
+// exclude children of parents kL5Split(lane & 15)
+__host__ __device__ __forceinline__ int l5_lane_node(int lane) {
+    return 2 * l5_map(kL5Split, lane & 15) + (lane < 16 ? 1 : 0);
+}
+__device__ __forceinline__ void tm_st_x2_8(uint32_t taddr, const uint32_t (&r)[8]) {  // 16x32bx2, split 64
+    asm volatile("tcgen05.st.sync.aligned.16x32bx2.x8.b32 [%0], 64, {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
+}
+__device__ __forceinline__ void tm_st_x2_16(uint32_t taddr, const uint32_t (&r)[16]) {  // 16x32bx2, split 16
+    asm volatile(
+        "tcgen05.st.sync.aligned.16x32bx2.x16.b32 [%0], 16, {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16};\n" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
+// Chunk C (< 8): A entries 2C, 2C+1 (thread x) or their mirrors (thread x + 16) of the
+// include child (computed) and of the exclude child (the parent's trailing block, raw):
+// include rows at lanes 0-15, exclude rows at lanes 16-31, A at column 8C, mirrors at +64.
+template <class T, int C> struct SplitChunk {
     __device__ __forceinline__ static void run(const T* Pt, const T (&u)[kMirD], const T (&w)[kMirD], int h,
                                                uint32_t tm_row) {
         if constexpr (C < 8) {
@@ -1075,19 +1098,16 @@ template <class T, int M, int C> struct MirChunk {
             constexpr int kA0 = cix<D>(i0, j0), kB0 = cix<D>(D - 1 - j0, D - 1 - i0);
             constexpr int kA1 = cix<D>(i1, j1), kB1 = cix<D>(D - 1 - j1, D - 1 - i1);
             const T in0 = Pt[h ? kB0 : kA0], in1 = Pt[h ? kB1 : kA1];
-            const T sb0 = Pt[kB0], sb1 = Pt[kB1];
             const T v0 = A::rank2(in0, u[i0], u[j0], w[i0], w[j0]);
             const T v1 = A::rank2(in1, u[i1], u[j1], w[i1], w[j1]);
-            const T y0 = shfl_xor_t(v0, 1), y1 = shfl_xor_t(v1, 1);
-            uint32_t r[16];
-            if constexpr (sizeof(T) == sizeof(dd)) {
-                dd_to_u32(h ? y0 : in0, r + 0);
-                dd_to_u32(h ? y1 : in1, r + 4);
-                dd_to_u32(h ? v0 : sb0, r + 8);
-                dd_to_u32(h ? v1 : sb1, r + 12);
-            }
-            tm_st16(tm_row + 16 * C, r);
-            MirChunk<T, M, C + 1>::run(Pt, u, w, h, tm_row);
+            uint32_t ri[8], re[8];
+            dd_to_u32(v0, ri);
+            dd_to_u32(v1, ri + 4);
+            dd_to_u32(in0, re);
+            dd_to_u32(in1, re + 4);
+            tm_st_x2_8(tm_row + 8 * C, ri);
+            tm_st_x2_8(tm_row + (16u << 16) + 8 * C, re);
+            SplitChunk<T, C + 1>::run(Pt, u, w, h, tm_row);
         }
     }
 };
@@ -1162,39 +1182,43 @@ template <class T, int E_LVL> struct FanLevel {
         }
         __syncwarp();
         if constexpr (Cfg<T>::TMEM && E_LVL == FAN) {
-            // last level -> TMEM: lane 2x+1 owns include child x, lane 2x the exclude
-            // child (= parent x's trailing block Pt).  The pair splits the include
-            // child's entries by the mirror (i,j) -> (7-j,7-i): the even lane forms the
-            // "A" entries (i+j < 7) with u, w in registers, the odd lane the mirrors
+            // last level -> TMEM: threads x and x + 16 share parent kL5Split(x) and split
+            // its include child's entries by the mirror (i,j) -> (7-j,7-i): thread x forms
+            // the "A" entries (i+j < 7) with u, w in registers, thread x + 16 the mirrors
             // with the vectors held reversed -- the same register indices, so (i,j) are
-            // compile-time for both.  The 4 self-mirror entries are formed by both (the
-            // odd lane keeps them).  Even-lane results cross over by shuffle; each lane
-            // stores its node's state to its TMEM row in mir_slot order.
+            // compile-time for both.  16x32bx2 stores write both halves into ONE TMEM lane
+            // (A at column 8C, mirrors at +64): lanes 0-15 receive the include children,
+            // lanes 16-31 the exclude children (the parents' trailing blocks, loaded by the
+            // same threads) -- no shuffles, no selects.  (Round 1's lane-pair mirror split
+            // crossed results by shuffle + select: 84.1 vs 83.8 ms at n = 32.)
             static_assert(dn == kMirD && tn == 36 && E == 16, "mirror split layout");
-            const int xe = l5_map(kL5PairMap, lane >> 1), h = lane & 1;
-            const T* Pt = sm + node_ref<T>(tabs, E_LVL - 1, xe).off + 2 * m - 1;
-            const T* uwe = uwv + xe * (2 * m + 1);
-            T u[dn], w[dn];
-#pragma unroll
-            for (int k = 0; k < dn; ++k) {
-                const int kk = 2 + (h ? dn - 1 - k : k);
-                u[k] = uwe[kk];
-                w[k] = uwe[m + kk];
-            }
-            MirChunk<T, m, 0>::run(Pt, u, w, h, tm_row);
             {
-                uint32_t r[16];
+                const int xe = l5_map(kL5Split, lane & 15), h = lane >> 4;
+                const T* Pt = sm + node_ref<T>(tabs, E_LVL - 1, xe).off + 2 * m - 1;
+                const T* uwe = uwv + xe * (2 * m + 1);
+                T u[dn], w[dn];
+#pragma unroll
+                for (int k = 0; k < dn; ++k) {
+                    const int kk = 2 + (h ? dn - 1 - k : k);
+                    u[k] = uwe[kk];
+                    w[k] = uwe[m + kk];
+                }
+                SplitChunk<T, 0>::run(Pt, u, w, h, tm_row);
+                uint32_t ri[16], re[16];
 #pragma unroll
                 for (int a = 0; a < 4; ++a) {
                     const T sv = Pt[cix<dn>(a, dn - 1 - a)];
-                    const T v = A::rank2(sv, u[dn - 1 - a], u[a], w[dn - 1 - a], w[a]);
-                    if constexpr (sizeof(T) == sizeof(dd)) dd_to_u32(h ? v : sv, r + 4 * a);
+                    dd_to_u32(A::rank2(sv, u[dn - 1 - a], u[a], w[dn - 1 - a], w[a]), ri + 4 * a);
+                    dd_to_u32(sv, re + 4 * a);
                 }
-                tm_st16(tm_row + 16 * 8, r);
+                // the anti-diagonal entries at column 128 (the upper half's duplicate at 144 lands
+                // in the lane subtree's scratch columns, written only later)
+                tm_st_x2_16(tm_row + 128, ri);
+                tm_st_x2_16(tm_row + (16u << 16) + 128, re);
+                tm_wait_st();
+                __syncwarp();
+                return;
             }
-            tm_wait_st();
-            __syncwarp();
-            return;
         }
         // trailing updates into the level-e buffers: item it = lane + 32 s (x-major)
         constexpr int NE = E * tn;
