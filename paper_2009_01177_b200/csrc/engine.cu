@@ -75,6 +75,11 @@ __host__ __device__ constexpr int ijtab_off(int a) { return 2 * (a - 1) * a * (2
 // 4-warp CTAs (one warp per TMEM lane quadrant).
 template <class T> struct Cfg;
 template <> struct Cfg<double> {
+    // unspecialised: every warp runs whole leaves, lane subtrees of 5 modes from shared memory.
+    // (The DD kernel's structure with 8-byte words -- 4 producers + 8 consumers, level 5 and
+    // L = 4 lane subtrees in TMEM -- measured slower on config 3: 2.96 ms with the producers
+    // running level 1 only, 3.25 with levels 1-2, vs 2.51: the producers' job-state loads
+    // bound it and the consumers' fp64 lane subtrees are too short to hide them.)
 #ifndef TOR_F64_MINB
 #define TOR_F64_MINB 1
 #endif
@@ -119,11 +124,11 @@ template <> struct Cfg<qd> {
 template <class T> constexpr int root_modes() { return Cfg<T>::L + FAN; }
 
 // WS mode 2: first fan-out level run by the consumer warps (the producers run the DFS
-// and levels 1 .. kConsFirst-1)
+// and levels 1 .. cons_first - 1)
 #ifndef TOR_CONS_FIRST
 #define TOR_CONS_FIRST 3
 #endif
-constexpr int kConsFirst = TOR_CONS_FIRST;
+template <class T> __host__ __device__ constexpr int cons_first() { return TOR_CONS_FIRST; }
 
 constexpr int kIjTabEntries = ijtab_off(kMaxJobModes);
 __device__ uint32_t g_ijtab[kIjTabEntries];
@@ -662,6 +667,36 @@ __device__ __forceinline__ dd u32_to_dd(uint32_t a, uint32_t b, uint32_t c, uint
     return dd{__hiloint2double(static_cast<int>(b), static_cast<int>(a)),
               __hiloint2double(static_cast<int>(d), static_cast<int>(c))};
 }
+// TMEM words of one state entry: U 32-bit columns (2 for fp64, 4 for DD)
+template <class T> struct TmU {
+    static constexpr int U = 2 * Arith<T>::K;
+    static constexpr int EPL = 16 / U;  // entries per 16-column load / store
+};
+__device__ __forceinline__ void to_u32(const dd& v, uint32_t* r) { dd_to_u32(v, r); }
+__device__ __forceinline__ void to_u32(const double& v, uint32_t* r) {
+    r[0] = static_cast<uint32_t>(__double2loint(v));
+    r[1] = static_cast<uint32_t>(__double2hiint(v));
+}
+template <class T> __device__ __forceinline__ T from_u32(const uint32_t* r);
+template <> __device__ __forceinline__ dd from_u32<dd>(const uint32_t* r) { return u32_to_dd(r[0], r[1], r[2], r[3]); }
+template <> __device__ __forceinline__ double from_u32<double>(const uint32_t* r) {
+    return __hiloint2double(static_cast<int>(r[1]), static_cast<int>(r[0]));
+}
+__device__ __forceinline__ void tm_ld2(uint32_t taddr, uint32_t& a, uint32_t& b) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n" : "=r"(a), "=r"(b) : "r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tm_st2(uint32_t taddr, uint32_t a, uint32_t b) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(taddr), "r"(a), "r"(b) : "memory");
+}
+// one state entry (U words)
+template <int U> __device__ __forceinline__ void tm_ld_e(uint32_t taddr, uint32_t* r) {
+    if constexpr (U == 4) tm_ld4(taddr, r[0], r[1], r[2], r[3]);
+    else tm_ld2(taddr, r[0], r[1]);
+}
+template <int U> __device__ __forceinline__ void tm_st_e(uint32_t taddr, const uint32_t* r) {
+    if constexpr (U == 4) tm_st4(taddr, r[0], r[1], r[2], r[3]);
+    else tm_st2(taddr, r[0], r[1]);
+}
 
 // (row, col) of flat index k in a packed D-row upper triangle (compile-time)
 __host__ __device__ constexpr int tri_row(int D, int k) {
@@ -715,18 +750,19 @@ __host__ __device__ constexpr int mir_a_col(int n) {
     return -1;
 }
 // Split level-5 layout: a level-5 state row holds the 16 "A" entries (i + j < 7) in A order
-// at columns 4a, their 16 mirrors at 64 + 4a and the 4 anti-diagonal entries at 128 + 4n
-// (the row-0/1 entries the lane subtree loads first are then mostly consecutive A entries)
-__host__ __device__ constexpr int split_col(int k) {
+// at columns U a, their 16 mirrors at 16 U + U a and the 4 anti-diagonal entries at 32 U + U n
+// (U = words per entry; the row-0/1 entries the lane subtree loads first are then mostly
+// consecutive A entries)
+__host__ __device__ constexpr int split_col(int k, int U) {
     const int i = tri_row(kMirD, k), j = tri_col(kMirD, k);
-    if (i + j == kMirD - 1) return 128 + 4 * i;
-    return i + j < kMirD - 1 ? 4 * mir_a_index(i, j) : 64 + 4 * mir_a_index(kMirD - 1 - j, kMirD - 1 - i);
+    if (i + j == kMirD - 1) return 32 * U + U * i;
+    return i + j < kMirD - 1 ? U * mir_a_index(i, j) : 16 * U + U * mir_a_index(kMirD - 1 - j, kMirD - 1 - i);
 }
-// TMEM column of entry k of a D-row lane state
-template <int D>
+// TMEM column of entry k of a D-row lane state of word type T
+template <class T, int D>
 __host__ __device__ constexpr int tm_col(int k) {
-    if constexpr (D == kMirD) return split_col(k);
-    else return 4 * k;
+    if constexpr (D == kMirD) return split_col(k, TmU<T>::U);
+    else return TmU<T>::U * k;
 }
 
 // Rank-2 update of trailing entries [KB, KB+CNT) whose sources are in TMEM; the (i,j)
@@ -737,8 +773,8 @@ template <class T, int M, int K, int END> struct LtUpd {
         if constexpr (K < END) {
             constexpr int D = M - 2;
             constexpr int i = tri_row(D, K), j = tri_col(D, K);
-            Sn.e[K] = Arith<T>::rank2(u32_to_dd(rt[0], rt[1], rt[2], rt[3]), u[2 + i], u[2 + j], w[2 + i], w[2 + j]);
-            LtUpd<T, M, K + 1, END>::run(rt + 4, u, w, Sn);
+            Sn.e[K] = Arith<T>::rank2(from_u32<T>(rt), u[2 + i], u[2 + j], w[2 + i], w[2 + j]);
+            LtUpd<T, M, K + 1, END>::run(rt + TmU<T>::U, u, w, Sn);
         }
     }
 };
@@ -753,31 +789,36 @@ __device__ __forceinline__ void tm_ld16(uint32_t taddr, uint32_t* r) {
         : "r"(taddr)
         : "memory");
 }
-template <int D, int K, int N> struct TmLd {
+// EPL entries in consecutive columns from entry K (one 16-column load / store)?
+template <class T, int D, int K> __host__ __device__ constexpr bool tm_run16() {
+    for (int q = 1; q < TmU<T>::EPL; ++q)
+        if (tm_col<T, D>(K + q) != tm_col<T, D>(K) + TmU<T>::U * q) return false;
+    return true;
+}
+template <class T, int D, int K, int N> struct TmLd {
     __device__ __forceinline__ static void run(uint32_t row, uint32_t* r) {
         if constexpr (N > 0) {
-            constexpr int col = tm_col<D>(K);
-            // natural column layout (the scratch states): four consecutive entries per
-            // 16-column load
-            if constexpr (N >= 4 && tm_col<D>(K + 1) == col + 4 && tm_col<D>(K + 2) == col + 8 &&
-                          tm_col<D>(K + 3) == col + 12) {
+            constexpr int col = tm_col<T, D>(K), EPL = TmU<T>::EPL;
+            // runs of EPL entries in consecutive columns (the natural scratch layout, the split
+            // layout's A entries): one 16-column load
+            if constexpr (N >= EPL && tm_run16<T, D, K>()) {
                 tm_ld16(row + col, r);
-                TmLd<D, K + 4, N - 4>::run(row, r + 16);
+                TmLd<T, D, K + EPL, N - EPL>::run(row, r + 16);
             } else {
-                tm_ld4(row + col, r[0], r[1], r[2], r[3]);
-                TmLd<D, K + 1, N - 1>::run(row, r + 4);
+                tm_ld_e<TmU<T>::U>(row + col, r);
+                TmLd<T, D, K + 1, N - 1>::run(row, r + TmU<T>::U);
             }
         }
     }
 };
-template <int D, int K0, int N>
-__device__ __forceinline__ void tm_ld_entries(uint32_t row, uint32_t (&r)[4 * N]) {
-    TmLd<D, K0, N>::run(row, r);
+template <class T, int D, int K0, int N>
+__device__ __forceinline__ void tm_ld_entries(uint32_t row, uint32_t (&r)[TmU<T>::U * N]) {
+    TmLd<T, D, K0, N>::run(row, r);
 }
 template <class T, int M, int KB, int CNT>
 __device__ __forceinline__ void lt_wave(uint32_t row, const T (&u)[M], const T (&w)[M], St<T, M / 2 - 1>& Sn) {
-    uint32_t rt[4 * CNT];
-    tm_ld_entries<M, 2 * M - 1 + KB, CNT>(row, rt);
+    uint32_t rt[TmU<T>::U * CNT];
+    tm_ld_entries<T, M, 2 * M - 1 + KB, CNT>(row, rt);
     tm_wait_ld();
     LtUpd<T, M, KB, KB + CNT>::run(rt, u, w, Sn);
 }
@@ -794,10 +835,9 @@ template <class T, int M, int K, int Q> struct LtQuad {
         if constexpr (Q > 0) {
             constexpr int D = M - 2;
             constexpr int i = tri_row(D, K), j = tri_col(D, K);
-            const T v =
-                Arith<T>::rank2(u32_to_dd(rt[0], rt[1], rt[2], rt[3]), u[2 + i], u[2 + j], w[2 + i], w[2 + j]);
-            dd_to_u32(v, r);
-            LtQuad<T, M, K + 1, Q - 1>::run(rt + 4, u, w, r + 4);
+            const T v = Arith<T>::rank2(from_u32<T>(rt), u[2 + i], u[2 + j], w[2 + i], w[2 + j]);
+            to_u32(v, r);
+            LtQuad<T, M, K + 1, Q - 1>::run(rt + TmU<T>::U, u, w, r + TmU<T>::U);
         }
     }
 };
@@ -813,32 +853,33 @@ template <class T, int M, int K, int END> struct LtUpdTm {
         if constexpr (K < END) {
             constexpr int D = M - 2;
             constexpr int i = tri_row(D, K), j = tri_col(D, K);
-            if constexpr (END - K >= 4) {
-                // four entries, one 16-column store (natural scratch layout)
+            constexpr int EPL = TmU<T>::EPL, U = TmU<T>::U;
+            if constexpr (END - K >= EPL) {
+                // EPL entries, one 16-column store (natural scratch layout)
                 uint32_t r[16];
-                LtQuad<T, M, K, 4>::run(rt, u, w, r);
-                tm_st16p(dst + tm_col<D>(K), r);
-                LtUpdTm<T, M, K + 4, END>::run(rt + 16, u, w, dst);
+                LtQuad<T, M, K, EPL>::run(rt, u, w, r);
+                tm_st16p(dst + tm_col<T, D>(K), r);
+                LtUpdTm<T, M, K + EPL, END>::run(rt + 16, u, w, dst);
             } else {
-                const T v = Arith<T>::rank2(u32_to_dd(rt[0], rt[1], rt[2], rt[3]), u[2 + i], u[2 + j], w[2 + i],
-                                            w[2 + j]);
-                uint32_t r[4];
-                dd_to_u32(v, r);
-                tm_st4(dst + tm_col<D>(K), r[0], r[1], r[2], r[3]);
-                LtUpdTm<T, M, K + 1, END>::run(rt + 4, u, w, dst);
+                const T v = Arith<T>::rank2(from_u32<T>(rt), u[2 + i], u[2 + j], w[2 + i], w[2 + j]);
+                uint32_t r[U];
+                to_u32(v, r);
+                tm_st_e<U>(dst + tm_col<T, D>(K), r);
+                LtUpdTm<T, M, K + 1, END>::run(rt + U, u, w, dst);
             }
         }
     }
 };
-template <int D, int K, int END> struct TmCopy {
+template <class T, int D, int K, int END> struct TmCopy {
     __device__ __forceinline__ static void run(const uint32_t* rt, uint32_t dst) {
         if constexpr (K < END) {
-            if constexpr (END - K >= 4) {
-                tm_st16p(dst + tm_col<D - 2>(K), rt);
-                TmCopy<D, K + 4, END>::run(rt + 16, dst);
+            constexpr int EPL = TmU<T>::EPL, U = TmU<T>::U;
+            if constexpr (END - K >= EPL) {
+                tm_st16p(dst + tm_col<T, D - 2>(K), rt);
+                TmCopy<T, D, K + EPL, END>::run(rt + 16, dst);
             } else {
-                tm_st4(dst + tm_col<D - 2>(K), rt[0], rt[1], rt[2], rt[3]);
-                TmCopy<D, K + 1, END>::run(rt + 4, dst);
+                tm_st_e<U>(dst + tm_col<T, D - 2>(K), rt);
+                TmCopy<T, D, K + 1, END>::run(rt + U, dst);
             }
         }
     }
@@ -850,18 +891,19 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
     constexpr int M = 2 * L;
     constexpr int K01 = 2 * M - 1;  // entries of rows 0 and 1
     constexpr int NT = tri_sz(M - 2);
+    constexpr int U = TmU<T>::U;
     const uint64_t bit = 1ull << (L - 1);
 #pragma unroll 1
     for (int br = 0; br < 2; ++br) {
         T tn;
         if constexpr (L >= 4) {
             if (br == 0) {
-                uint32_t r0[4 * K01];
-                tm_ld_entries<M, 0, K01>(row, r0);
+                uint32_t r0[U * K01];
+                tm_ld_entries<T, M, 0, K01>(row, r0);
                 tm_wait_ld();
                 T e0[K01];
 #pragma unroll
-                for (int k = 0; k < K01; ++k) e0[k] = u32_to_dd(r0[4 * k], r0[4 * k + 1], r0[4 * k + 2], r0[4 * k + 3]);
+                for (int k = 0; k < K01; ++k) e0[k] = from_u32<T>(r0 + U * k);
                 const Piv<T> pv = piv_lt<T>(e0[0], e0[1], e0[M], t);
                 if (pv.bad0 || pv.bad1) report_breakdown(err, mask | bit, 2 * nsel + (pv.bad0 ? 0 : 1));
                 tn = pv.tn;
@@ -873,20 +915,20 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
                 }
                 constexpr int H = (NT + 2) / 3;
                 {
-                    uint32_t rt[4 * H];
-                    tm_ld_entries<M, K01, H>(row, rt);
+                    uint32_t rt[U * H];
+                    tm_ld_entries<T, M, K01, H>(row, rt);
                     tm_wait_ld();
                     LtUpdTm<T, M, 0, H>::run(rt, u, w, scr);
                 }
                 {
-                    uint32_t rt[4 * H];
-                    tm_ld_entries<M, K01 + H, H>(row, rt);
+                    uint32_t rt[U * H];
+                    tm_ld_entries<T, M, K01 + H, H>(row, rt);
                     tm_wait_ld();
                     LtUpdTm<T, M, H, 2 * H>::run(rt, u, w, scr);
                 }
                 {
-                    uint32_t rt[4 * (NT - 2 * H)];
-                    tm_ld_entries<M, K01 + 2 * H, NT - 2 * H>(row, rt);
+                    uint32_t rt[U * (NT - 2 * H)];
+                    tm_ld_entries<T, M, K01 + 2 * H, NT - 2 * H>(row, rt);
                     tm_wait_ld();
                     LtUpdTm<T, M, 2 * H, NT>::run(rt, u, w, scr);
                 }
@@ -894,16 +936,16 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
             } else {
                 constexpr int H = (NT + 1) / 2;
                 {
-                    uint32_t rt[4 * H];
-                    tm_ld_entries<M, K01, H>(row, rt);
+                    uint32_t rt[U * H];
+                    tm_ld_entries<T, M, K01, H>(row, rt);
                     tm_wait_ld();
-                    TmCopy<M, 0, H>::run(rt, scr);
+                    TmCopy<T, M, 0, H>::run(rt, scr);
                 }
                 {
-                    uint32_t rt[4 * (NT - H)];
-                    tm_ld_entries<M, K01 + H, NT - H>(row, rt);
+                    uint32_t rt[U * (NT - H)];
+                    tm_ld_entries<T, M, K01 + H, NT - H>(row, rt);
                     tm_wait_ld();
-                    TmCopy<M, H, NT>::run(rt, scr);
+                    TmCopy<T, M, H, NT>::run(rt, scr);
                 }
                 tn = t;
             }
@@ -913,12 +955,12 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
         } else {
             St<T, L - 1> Sn;
             if (br == 0) {
-                uint32_t r0[4 * K01];
-                tm_ld_entries<M, 0, K01>(row, r0);
+                uint32_t r0[U * K01];
+                tm_ld_entries<T, M, 0, K01>(row, r0);
                 tm_wait_ld();
                 T e0[K01];
 #pragma unroll
-                for (int k = 0; k < K01; ++k) e0[k] = u32_to_dd(r0[4 * k], r0[4 * k + 1], r0[4 * k + 2], r0[4 * k + 3]);
+                for (int k = 0; k < K01; ++k) e0[k] = from_u32<T>(r0 + U * k);
                 const Piv<T> pv = piv_lt<T>(e0[0], e0[1], e0[M], t);
                 if (pv.bad0 || pv.bad1) report_breakdown(err, mask | bit, 2 * nsel + (pv.bad0 ? 0 : 1));
                 tn = pv.tn;
@@ -931,12 +973,11 @@ __device__ __forceinline__ void tmem_ext(uint32_t row, uint32_t scr, const T& t,
                 lt_wave<T, M, 0, NT>(row, u, w, Sn);
                 acc.add(tn, !neg, nsel + 1);
             } else {
-                uint32_t rt[4 * NT];
-                tm_ld_entries<M, K01, NT>(row, rt);
+                uint32_t rt[U * NT];
+                tm_ld_entries<T, M, K01, NT>(row, rt);
                 tm_wait_ld();
 #pragma unroll
-                for (int kk = 0; kk < NT; ++kk)
-                    Sn.e[kk] = u32_to_dd(rt[4 * kk], rt[4 * kk + 1], rt[4 * kk + 2], rt[4 * kk + 3]);
+                for (int kk = 0; kk < NT; ++kk) Sn.e[kk] = from_u32<T>(rt + U * kk);
                 tn = t;
             }
             SubReg<T, L - 1>::run(Sn, tn, br == 0 ? !neg : neg, br == 0 ? (mask | bit) : mask, nsel + (br == 0), acc,
@@ -1073,20 +1114,28 @@ constexpr uint64_t kL5Split = 0x3fc9a650e821b7d4ull;
 __host__ __device__ __forceinline__ int l5_lane_node(int lane) {
     return 2 * l5_map(kL5Split, lane & 15) + (lane < 16 ? 1 : 0);
 }
-__device__ __forceinline__ void tm_st_x2_8(uint32_t taddr, const uint32_t (&r)[8]) {  // 16x32bx2, split 64
-    asm volatile("tcgen05.st.sync.aligned.16x32bx2.x8.b32 [%0], 64, {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
-                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
-}
-__device__ __forceinline__ void tm_st_x2_16(uint32_t taddr, const uint32_t (&r)[16]) {  // 16x32bx2, split 16
-    asm volatile(
-        "tcgen05.st.sync.aligned.16x32bx2.x16.b32 [%0], 16, {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-        "%14, %15, %16};\n" ::"r"(taddr),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+// 16x32bx2 stores: threads t and t + 16 write W columns each into TMEM lane t, the upper half
+// SPLIT columns further (W = 4, 8 or 16 words)
+template <int W, int SPLIT> __device__ __forceinline__ void tm_st_x2(uint32_t taddr, const uint32_t (&r)[W]) {
+    if constexpr (W == 4) {
+        asm volatile("tcgen05.st.sync.aligned.16x32bx2.x4.b32 [%0], %1, {%2, %3, %4, %5};\n" ::"r"(taddr), "n"(SPLIT),
+                     "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]));
+    } else if constexpr (W == 8) {
+        asm volatile("tcgen05.st.sync.aligned.16x32bx2.x8.b32 [%0], %1, {%2, %3, %4, %5, %6, %7, %8, %9};\n" ::"r"(
+                         taddr),
+                     "n"(SPLIT), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
+    } else {
+        static_assert(W == 16, "16x32bx2 store width");
+        asm volatile(
+            "tcgen05.st.sync.aligned.16x32bx2.x16.b32 [%0], %1, {%2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15, %16, %17};\n" ::"r"(taddr),
+            "n"(SPLIT), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+            "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+    }
 }
 // Chunk C (< 8): A entries 2C, 2C+1 (thread x) or their mirrors (thread x + 16) of the
 // include child (computed) and of the exclude child (the parent's trailing block, raw):
-// include rows at lanes 0-15, exclude rows at lanes 16-31, A at column 8C, mirrors at +64.
+// include rows at lanes 0-15, exclude rows at lanes 16-31, A at column 2UC, mirrors at +16U.
 template <class T, int C> struct SplitChunk {
     __device__ __forceinline__ static void run(const T* Pt, const T (&u)[kMirD], const T (&w)[kMirD], int h,
                                                uint32_t tm_row) {
@@ -1100,13 +1149,14 @@ template <class T, int C> struct SplitChunk {
             const T in0 = Pt[h ? kB0 : kA0], in1 = Pt[h ? kB1 : kA1];
             const T v0 = A::rank2(in0, u[i0], u[j0], w[i0], w[j0]);
             const T v1 = A::rank2(in1, u[i1], u[j1], w[i1], w[j1]);
-            uint32_t ri[8], re[8];
-            dd_to_u32(v0, ri);
-            dd_to_u32(v1, ri + 4);
-            dd_to_u32(in0, re);
-            dd_to_u32(in1, re + 4);
-            tm_st_x2_8(tm_row + 8 * C, ri);
-            tm_st_x2_8(tm_row + (16u << 16) + 8 * C, re);
+            constexpr int U = TmU<T>::U;
+            uint32_t ri[2 * U], re[2 * U];
+            to_u32(v0, ri);
+            to_u32(v1, ri + U);
+            to_u32(in0, re);
+            to_u32(in1, re + U);
+            tm_st_x2<2 * U, 16 * U>(tm_row + 2 * U * C, ri);
+            tm_st_x2<2 * U, 16 * U>(tm_row + (16u << 16) + 2 * U * C, re);
             SplitChunk<T, C + 1>::run(Pt, u, w, h, tm_row);
         }
     }
@@ -1204,17 +1254,18 @@ template <class T, int E_LVL> struct FanLevel {
                     w[k] = uwe[m + kk];
                 }
                 SplitChunk<T, 0>::run(Pt, u, w, h, tm_row);
-                uint32_t ri[16], re[16];
+                constexpr int U = TmU<T>::U;
+                uint32_t ri[4 * U], re[4 * U];
 #pragma unroll
                 for (int a = 0; a < 4; ++a) {
                     const T sv = Pt[cix<dn>(a, dn - 1 - a)];
-                    dd_to_u32(A::rank2(sv, u[dn - 1 - a], u[a], w[dn - 1 - a], w[a]), ri + 4 * a);
-                    dd_to_u32(sv, re + 4 * a);
+                    to_u32(A::rank2(sv, u[dn - 1 - a], u[a], w[dn - 1 - a], w[a]), ri + U * a);
+                    to_u32(sv, re + U * a);
                 }
-                // the anti-diagonal entries at column 128 (the upper half's duplicate at 144 lands
+                // the anti-diagonal entries at column 32U (the upper half's duplicate at 36U lands
                 // in the lane subtree's scratch columns, written only later)
-                tm_st_x2_16(tm_row + 128, ri);
-                tm_st_x2_16(tm_row + (16u << 16) + 128, re);
+                tm_st_x2<4 * U, 4 * U>(tm_row + 32 * U, ri);
+                tm_st_x2<4 * U, 4 * U>(tm_row + (16u << 16) + 32 * U, re);
                 tm_wait_st();
                 __syncwarp();
                 return;
@@ -1227,8 +1278,7 @@ template <class T, int E_LVL> struct FanLevel {
 #define TOR_UB_P 3  // producer fan-out levels (3 84.0, 4 84.2, 5 85.0, 6 84.3)
 #endif
         constexpr int UB = sizeof(T) == sizeof(qd) ? TOR_QD_UB
-                           : (sizeof(T) == sizeof(double) ? TOR_F64_UB
-                                                          : (E_LVL < kConsFirst ? TOR_UB_P : TOR_UB));  // items per batch
+                           : (!Cfg<T>::WS ? TOR_F64_UB : (E_LVL < cons_first<T>() ? TOR_UB_P : TOR_UB));  // items per batch
         const uint32_t* itb = tabs + WarpSmem<T>::item_off(E_LVL) + lane;
         T* out = sm + WarpSmem<T>::lvl_off(E_LVL) + lane;
         if constexpr (sizeof(T) == sizeof(qd)) {
@@ -1416,12 +1466,13 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         __syncwarp();
         const uint64_t leaf_mask = J.mask | (leaf << Q0);
         const int leaf_sel = J.nsel + __popcll(leaf);
-        FanLevel<T, 1>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
-        FanLevel<T, 2>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
-        if constexpr (Cfg<T>::WS_MODE != 2 || kConsFirst > 3)
-            FanLevel<T, 3>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
-        if constexpr (Cfg<T>::WS_MODE != 2) FanLevel<T, 4>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
-        if constexpr (!Cfg<T>::WS) FanLevel<T, 5>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
+        // fan-out levels 1 .. cons_first - 1 (all of them when unspecialised)
+        constexpr int CF = Cfg<T>::WS ? cons_first<T>() : FAN + 1;
+        if constexpr (CF > 1) FanLevel<T, 1>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
+        if constexpr (CF > 2) FanLevel<T, 2>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
+        if constexpr (CF > 3) FanLevel<T, 3>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
+        if constexpr (CF > 4) FanLevel<T, 4>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
+        if constexpr (CF > 5) FanLevel<T, 5>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
     };
     using AccT = Acc<T, kScaled>;
     auto write_partial = [&](AccT& acc, unsigned long long job) {
@@ -1537,8 +1588,9 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 const unsigned long long job = meta[c].job;
                 const int leaf_sel = meta[c].sel, flags = meta[c].flags;
                 if (flags & 2) break;
-                if constexpr (kConsFirst <= 3) FanLevel<T, 3>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, cerr, crow);
-                FanLevel<T, 4>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, cerr, crow);
+                if constexpr (cons_first<T>() <= 2) FanLevel<T, 2>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, cerr, crow);
+                if constexpr (cons_first<T>() <= 3) FanLevel<T, 3>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, cerr, crow);
+                if constexpr (cons_first<T>() <= 4) FanLevel<T, 4>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, cerr, crow);
                 FanLevel<T, FAN>::run(csm, ctv, cuw, tabs, leaf_mask, leaf_sel, cerr, crow);
                 const int node = l5_lane_node(lane);  // the level-5 node in this lane's TMEM row
                 const T vt = ctv[node_ref<T>(tabs, FAN, node).tix];
@@ -1548,7 +1600,7 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 const int lsel = leaf_sel + __popc(node);
                 const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
                 acc.add(vt, nodeneg, lsel);
-                tmem_ext<T, L, AccT>(crow, crow + 4 * tri_sz(2 * L), vt, nodeneg, lmask, lsel, acc, cerr);
+                tmem_ext<T, L, AccT>(crow, crow + TmU<T>::U * tri_sz(2 * L), vt, nodeneg, lmask, lsel, acc, cerr);
                 acc.flush();
                 if (flags & 1) {
                     write_partial(acc, job);
@@ -1878,7 +1930,7 @@ class PlanImpl final : public Plan {
         // gives bit-identical results.  kWantJobs whole-problem jobs keep the dynamic
         // schedule's tail short even for the 1/8 shard of an 8-GPU run; job states are
         // <= kMaxJobModes modes.
-        const uint64_t want_jobs = range.prefix_jobs ? range.prefix_jobs : kWantJobs;
+                const uint64_t want_jobs = range.prefix_jobs ? range.prefix_jobs : kWantJobs;
         class_partials_ = range.class_partials;
         c_ = 0;
         if (n_ >= Q0) {
