@@ -2035,6 +2035,7 @@ class PlanImpl final : public Plan {
     }
 
     ~PlanImpl() override {
+        if (graph_) cudaGraphExecDestroy(graph_);
         if (res_host_) cudaFreeHost(res_host_);
         for (auto& e : ev_)
             if (e) cudaEventDestroy(e);
@@ -2046,19 +2047,48 @@ class PlanImpl final : public Plan {
         return collect(out, stats, err);
     }
 
-    // enqueue the whole device pipeline and the read-back on the plan's stream
+    // Launch the whole device pipeline and the read-back on the plan's stream: the ~10-40
+    // launches (memsets, prefix levels, jobs, subtree kernel, fold passes, gather, copy) are
+    // captured once into a CUDA graph and replayed, so a repeated small evaluation pays one
+    // launch (the graph is re-captured when the input scaling selects the other kernel).
     int launch(std::string& err) override {
-        constexpr int Q0 = Cfg<T>::L + FAN;
         CK(cudaSetDevice(device_));
+        const auto tx0 = std::chrono::steady_clock::now();
+        if (!graph_ || graph_tsc_ != tsc_) {
+            if (graph_) {
+                cudaGraphExecDestroy(graph_);
+                graph_ = nullptr;
+            }
+            cudaGraph_t g = nullptr;
+            CK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+            const int st = enqueue(err);
+            const cudaError_t ce = cudaStreamEndCapture(st_, &g);
+            if (st != 0) {
+                if (g) cudaGraphDestroy(g);
+                return st;
+            }
+            CK(ce);
+            const cudaError_t ie = cudaGraphInstantiate(&graph_, g, 0);
+            cudaGraphDestroy(g);
+            CK(ie);
+            graph_tsc_ = tsc_;
+        }
+        CK(cudaGraphLaunch(graph_, st_));
+        tx0_ = tx0;
+        return 0;
+    }
+
+    // the pipeline's work on st_ (captured by launch)
+    int enqueue(std::string& err) {
+        constexpr int Q0 = Cfg<T>::L + FAN;
         uint64_t launches = 0;
         unsigned long long* errw = static_cast<unsigned long long*>(errw_.p);
         unsigned long long* ctr = static_cast<unsigned long long*>(ctr_.p);
         double* parts = static_cast<double*>(parts_.p);
         Job<T>* jobs = static_cast<Job<T>*>(jobs_.p);
-        const auto tx0 = std::chrono::steady_clock::now();
         CK(cudaMemsetAsync(errw, 0xff, sizeof(unsigned long long), st_));
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st_));
-        CK(cudaEventRecord(ev_[0], st_));
+        CK(cudaEventRecordWithFlags(ev_[0], st_, cudaEventRecordExternal));
         if (use_levels_) {
             const int wpb = 4;
             const size_t sm = sizeof(T) * 4 * n_ * wpb;
@@ -2093,7 +2123,7 @@ class PlanImpl final : public Plan {
             ++launches;
         }
         CK(cudaGetLastError());
-        CK(cudaEventRecord(ev_[1], st_));
+        CK(cudaEventRecordWithFlags(ev_[1], st_, cudaEventRecordExternal));
         if (rjob_ >= Q0) {
             constexpr int WPB = Cfg<T>::WPB;
             auto* kfn = tsc_ ? subtree_kernel<T, true> : subtree_kernel<T, false>;
@@ -2107,7 +2137,7 @@ class PlanImpl final : public Plan {
         }
         ++launches;
         CK(cudaGetLastError());
-        CK(cudaEventRecord(ev_[2], st_));
+        CK(cudaEventRecordWithFlags(ev_[2], st_, cudaEventRecordExternal));
         // jobs per output partial: the whole range, or one class (a power of two)
         const uint64_t chunk = class_partials_ ? per_ / (chi_ - clo_) : per_;
         for (uint64_t S = 1; S < chunk; S *= kFoldB) {
@@ -2121,7 +2151,7 @@ class PlanImpl final : public Plan {
             }
         }
         CK(cudaGetLastError());
-        CK(cudaEventRecord(ev_[3], st_));
+        CK(cudaEventRecordWithFlags(ev_[3], st_, cudaEventRecordExternal));
         double* resd = static_cast<double*>(res_.p);
         gather_results_kernel<<<static_cast<unsigned>((ninst_ * 5 + 255) / 256), 256, 0, st_>>>(parts, per_, ninst_,
                                                                                               errw, resd);
@@ -2129,9 +2159,8 @@ class PlanImpl final : public Plan {
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(res_host_, resd, sizeof(double) * (static_cast<size_t>(ninst_) * 5 + 1),
                            cudaMemcpyDeviceToHost, st_));
-        CK(cudaEventRecord(ev_[5], st_));
+        CK(cudaEventRecordWithFlags(ev_[5], st_, cudaEventRecordExternal));
         launches_ = launches;
-        tx0_ = tx0;
         return 0;
     }
 
@@ -2216,7 +2245,9 @@ class PlanImpl final : public Plan {
     cudaEvent_t ev_[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     DevBuf pool_, tpool_, jobs_, parts_, errw_, ctr_, scr_, work_, res_, rin_;
     double* res_host_ = nullptr;  // pinned: ninst x 5 result words + the breakdown word
-    uint64_t launches_ = 0;       // kernels of the last launch()
+    uint64_t launches_ = 0;       // kernels in the launched graph
+    cudaGraphExec_t graph_ = nullptr;
+    int graph_tsc_ = -1;
     std::chrono::steady_clock::time_point tx0_;
 };
 
