@@ -44,6 +44,10 @@ constexpr int MAX_LEVELS = 48;
 // keeps the prefix levels of an n = 50 shard (the paper's case) within a few GB
 constexpr int kMaxJobModes = 32;
 constexpr uint64_t kWantJobs = 262144;
+#ifndef TOR_WANT_JOBS_BATCH
+#define TOR_WANT_JOBS_BATCH 32768  // cfg3 4096 x n=16: fp64 2.19 -> 1.95 ms, DD 5.59 -> 5.47 (262144 / 65536 / 32768 / 8192 measured)
+#endif
+constexpr uint64_t kWantJobsBatch = TOR_WANT_JOBS_BATCH;  // batches of several instances
 constexpr int kShardBits = 6;
 #ifndef TOR_MB_HINT
 #define TOR_MB_HINT 100  // mbarrier try_wait suspend-time hint (ns): 1e6 measured 0.3% slower
@@ -541,6 +545,10 @@ constexpr int kLoopQ = TOR_LOOPQ;
 #define TOR_QD_LOOPQ 3
 #endif
 constexpr int kLoopQQd = TOR_QD_LOOPQ;
+#ifndef TOR_F64_LOOPQ
+#define TOR_F64_LOOPQ 4  // fp64: levels of >= 4 modes as loops (cfg3 fp64 2.50 -> 2.36 ms vs 3; 5: 2.36)
+#endif
+constexpr int kLoopQF64 = TOR_F64_LOOPQ;
 
 template <class T, int Q> struct SubReg {
     template <class AC, class E>
@@ -566,7 +574,7 @@ template <class T, int Q> struct SubReg {
     template <class AC, class E>
     __device__ __forceinline__ static void run(const St<T, Q>& S, const T& t, bool neg, uint64_t mask, int nsel,
                                                AC& acc, E* err) {
-        if constexpr (Q >= (sizeof(T) == sizeof(qd) ? kLoopQQd : kLoopQ)) {
+        if constexpr (Q >= (sizeof(T) == sizeof(qd) ? kLoopQQd : (sizeof(T) == sizeof(double) ? kLoopQF64 : kLoopQ))) {
 #pragma unroll 1
             for (int br = 0; br < 2; ++br) branch(S, br, t, neg, mask, nsel, acc, err);
         } else {
@@ -600,8 +608,7 @@ __device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t,
     constexpr int M = 2 * L;
     acc.add(t, neg, nsel);
     const uint64_t bit = 1ull << (L - 1);
-#pragma unroll 1
-    for (int br = 0; br < 2; ++br) {
+    auto branch = [&](int br) {
         St<T, L - 1> Sn;
         T tn;
         if (br == 0) {
@@ -630,7 +637,9 @@ __device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t,
         }
         SubReg<T, L - 1>::run(Sn, tn, br == 0 ? !neg : neg, br == 0 ? (mask | bit) : mask, nsel + (br == 0), acc,
                               err);
-    }
+    };
+#pragma unroll 1
+    for (int br = 0; br < 2; ++br) branch(br);
 }
 
 // ------------------------------------------------------------------ TMEM ----
@@ -999,18 +1008,24 @@ template <class T> struct WarpSmem {
     // parents, read lane-pair-wise by FanLevel<5>) then start on every 16-byte bank slot
     // mod 8 exactly twice and the 8 level-3 nodes on distinct slots, so those reads are
     // free of bank conflicts (found by exhaustive search over small paddings).
-    // fp64 (8-byte words, level-5 states in shared memory, read lane-wise by the lane
-    // subtrees in two 16-lane phases of 8-byte banks): base pads (0,0,1,2,8) and stride
-    // adds (1,0,3,0,0) for levels 1..5 (24 entries per area) cut the worst per-phase
-    // multiplicity of the 32 level-5 node bases mod 16 from 3+3 to 2+1
-    // (tools/f64_layout_search.py).
+    // fp64 (8-byte words, level-5 states in shared memory): base pads, child stride adds, pair
+    // strides and the fan-out lane maps of levels 1..5 from tools/f64_pairs_search.py, a bank
+    // model of every fan-out access (pivot / vector loads, pair stores, item table / source /
+    // pair loads and stores) and of the lane subtrees' level-5 reads (8-byte accesses served
+    // per 16-lane phase, 16-byte per 8-lane phase): 1229 wavefronts per leaf against an ideal
+    // of 1204 (the previous layout, tuned for the lane subtrees alone: 1681)
     static constexpr bool kF64Pad = sizeof(T) == sizeof(double) && !Cfg<T>::TMEM;
+    // per level e = 1..5, 4 bits each from bit 4(e-1): base pads (13, 6, 1, 15, 0), stride adds
+    // (6, 0, 3, 4, 3), pair strides m + (2, 2, 2, 1, 2) (16-byte units)
+    static constexpr uint32_t kF64LvlPad = 0x0f16du, kF64StrideAdd = 0x34306u, kF64PairAdd = 0x21222u;
+    static constexpr unsigned kF64Interleave = 0xeu;  // bit e-1: parent x = lane % E, else lane / G
+    __host__ __device__ static constexpr int nib(uint32_t pack, int e) { return static_cast<int>((pack >> (4 * (e - 1))) & 15u); }
     __host__ __device__ static constexpr int lvl_pad(int e) {
-        if constexpr (kF64Pad) return e == 3 ? 1 : (e == 4 ? 2 : (e == 5 ? 8 : 0));
+        if constexpr (kF64Pad) return e >= 1 && e <= 5 ? nib(kF64LvlPad, e) : 0;
         return Cfg<T>::TMEM ? (e == 1 ? 2 : (e == 2 ? 1 : 0)) : 0;
     }
     __host__ __device__ static constexpr int buf_stride(int e) {
-        if constexpr (kF64Pad) return tri_sz(2 * (Q0 - e)) + (e == 1 ? 1 : (e == 3 ? 3 : 0));
+        if constexpr (kF64Pad) return tri_sz(2 * (Q0 - e)) + nib(kF64StrideAdd, e);
         return tri_sz(2 * (Q0 - e)) + (Cfg<T>::TMEM && e == 2 ? 1 : 0);
     }
     __host__ __device__ static constexpr int lvl_off(int e) {
@@ -1021,15 +1036,22 @@ template <class T> struct WarpSmem {
     // with TMEM the last level's include states never touch shared memory
     static constexpr int kBufEntries = Cfg<T>::TMEM ? lvl_off(FAN) : lvl_off(FAN + 1);
     static constexpr int kTOff = kBufEntries;  // t of level buffers at 2^(e-1)-1+p, root t at 31
+    // fp64 (unspecialised): the fan-out levels' pivot-row vectors are stored as (u_j, w_j)
+    // pairs (one 16-byte load per index) and each parent's trailing items are run by its own
+    // lane group with item tables indexed by the child entry alone (FanLevel)
+    static constexpr bool kPairUw = sizeof(T) == sizeof(double) && !Cfg<T>::TMEM;
+    // pair stride of a level-e parent (16-byte units, >= m = 2(Q0-e+1) pairs)
+    __host__ __device__ static constexpr int uw_pair_stride(int e) { return 2 * (Q0 - e + 1) + nib(kF64PairAdd, e); }
     __host__ __device__ static constexpr int uw_need() {
         int mx = 4 * kMaxJobModes;  // DFS eliminations: 4q entries
         for (int e = 1; e <= FAN; ++e) {
-            const int need = (1 << (e - 1)) * (4 * (Q0 - e + 1) + 1);  // stride 2m+1 per parent
+            const int need = kPairUw ? (1 << (e - 1)) * 2 * uw_pair_stride(e)
+                                     : (1 << (e - 1)) * (4 * (Q0 - e + 1) + 1);  // stride 2m+1 per parent
             if (need > mx) mx = need;
         }
         return mx;
     }
-    static constexpr int kUwOff = kTOff + 32;
+    static constexpr int kUwOff = kPairUw ? ((kTOff + 33) / 2) * 2 : kTOff + 32;  // pairs: 16-byte aligned
     static constexpr int kUwEntries = uw_need();
     static constexpr int kDfsT = kUwOff + kUwEntries;  // DFS slot t values (<= 32)
     // (warp-specialised: the DFS t values are producer-private, see kProdEntries)
@@ -1056,7 +1078,7 @@ template <class T> struct WarpSmem {
     static constexpr int kItemLevels = Cfg<T>::TMEM ? FAN - 1 : FAN;
     __host__ __device__ static constexpr int item_off(int e) {
         int o = 0;
-        for (int x = 1; x < e; ++x) o += (1 << (x - 1)) * tri_sz(2 * (Q0 - x));
+        for (int x = 1; x < e; ++x) o += (kPairUw ? 1 : (1 << (x - 1))) * tri_sz(2 * (Q0 - x));
         return o;
     }
     static constexpr int kLastTabOff = item_off(kItemLevels + 1);
@@ -1193,9 +1215,86 @@ template <class T, int E_LVL> struct FanLevel {
     static constexpr int m = 2 * q;
     static constexpr int dn = m - 2;
     static constexpr int tn = tri_sz(dn);
+    // fp64: lane (x, g) = (lane / G, lane % G) (the G lanes of parent x consecutive) or
+    // (lane % E, lane / E) per level, whichever the bank search picked (WarpSmem).
+    // Item k = g + sG of parent x: source Pt[k], destination out_x[k] (per-lane base + a
+    // constant), (u, w) pairs of rows 2+i, 2+j at the byte offsets of table word k.
+    // 10 instructions per item (4 loads, 3 integer, 2 DFMA, 1 store) instead of 17 for the
+    // flat x-major item list with one decoded (src, ui, uj) word per item.
+    template <class ErrSink>
+    __device__ __forceinline__ static void run_pairs(double* sm, double* tvals, double* uwv, const uint32_t* tabs,
+                                                     uint64_t leaf_mask, int leaf_sel, ErrSink* err) {
+        using A = Arith<double>;
+        using SM = WarpSmem<double>;
+        const int lane = threadIdx.x & 31;
+        constexpr bool kIl = (SM::kF64Interleave >> (E_LVL - 1)) & 1u;
+        const int x = kIl ? lane % E : lane / G, g = kIl ? lane / E : lane % G;
+        const double* P = sm + node_ref<double>(tabs, E_LVL - 1, x).off;
+        const Piv<double> pv = pivot2<double>(P[0], P[1], P[m], tvals[node_ref<double>(tabs, E_LVL - 1, x).tix]);
+        if (g == 0) {
+            const uint64_t nm = leaf_mask | (static_cast<uint64_t>((x << 1) | 1) << (Q0 - E_LVL));
+            if (pv.bad0 || pv.bad1) report_breakdown(err, nm, 2 * (leaf_sel + __popc(x)) + (pv.bad0 ? 0 : 1));
+            tvals[E - 1 + x] = pv.tn;  // level e-1 t values live below index E-1: no hazard
+        }
+        constexpr int S2 = SM::uw_pair_stride(E_LVL);
+        double2* uw2 = reinterpret_cast<double2*>(uwv) + x * S2;
+        {
+            constexpr int NVS = (m - 2 + G - 1) / G;
+            double a[NVS], b[NVS];
+#pragma unroll
+            for (int s = 0; s < NVS; ++s) {
+                const int j = 2 + g + s * G;  // reads past row end stay inside the warp area
+                a[s] = P[j];
+                b[s] = P[m - 1 + j];
+            }
+#pragma unroll
+            for (int s = 0; s < NVS; ++s) A::vec(a[s], b[s], pv.r1, pv.u1, pv.r2, a[s], b[s]);
+#pragma unroll
+            for (int s = 0; s < NVS; ++s)
+                if (g + s * G < m - 2) uw2[2 + g + s * G] = make_double2(a[s], b[s]);
+        }
+        __syncwarp();
+        constexpr int NS = (tn + G - 1) / G;  // items per lane (the last one partial if tn % G)
+        constexpr bool kPart = (tn % G) != 0;
+        const char* uwb = reinterpret_cast<const char*>(uw2);
+        const double* Pt = P + 2 * m - 1 + g;
+        double* out = sm + SM::lvl_off(E_LVL) + x * SM::buf_stride(E_LVL) + g;
+        const uint32_t* kt = tabs + SM::item_off(E_LVL) + g;
+        const bool tail_ok = g < tn - (NS - 1) * G;
+        auto batch = [&](int s0, auto cnt, auto last_partial) {
+            constexpr int C = decltype(cnt)::value;
+            constexpr bool LP = decltype(last_partial)::value;
+            double sv[C];
+            double2 pi[C], pj[C];
+#pragma unroll
+            for (int u = 0; u < C; ++u) {
+                const uint32_t w = (!LP || u < C - 1 || tail_ok) ? kt[G * (s0 + u)] : 0u;
+                sv[u] = Pt[G * (s0 + u)];
+                pi[u] = *reinterpret_cast<const double2*>(uwb + (w & 0xffffu));
+                pj[u] = *reinterpret_cast<const double2*>(uwb + (w >> 16));
+            }
+#pragma unroll
+            for (int u = 0; u < C; ++u) sv[u] = A::rank2_item(sv[u], pi[u].x, pj[u].x, pi[u].y, pj[u].y);
+#pragma unroll
+            for (int u = 0; u < C; ++u)
+                if (!LP || u < C - 1 || tail_ok) out[G * (s0 + u)] = sv[u];
+        };
+        constexpr int NFULL = NS - (kPart ? 1 : 0);
+        constexpr int UB = TOR_F64_UB;
+        constexpr int SMAIN = (NFULL / UB) * UB;
+#pragma unroll 1
+        for (int s0 = 0; s0 < SMAIN; s0 += UB) batch(s0, std::integral_constant<int, UB>{}, std::false_type{});
+        constexpr int CT = NS - SMAIN;
+        if constexpr (CT > 0) batch(SMAIN, std::integral_constant<int, CT>{}, std::integral_constant<bool, kPart>{});
+        __syncwarp();
+    }
     template <class ErrSink>
     __device__ __forceinline__ static void run(T* sm, T* tvals, T* uwv, const uint32_t* tabs, uint64_t leaf_mask,
                                                int leaf_sel, ErrSink* err, uint32_t tm_row) {
+        if constexpr (WarpSmem<T>::kPairUw) {
+            run_pairs(sm, tvals, uwv, tabs, leaf_mask, leaf_sel, err);
+            return;
+        }
         using A = Arith<T>;
         const int lane = threadIdx.x & 31;
         const int x = (Cfg<T>::TMEM && E_LVL == FAN) ? l5_map(kL5VecMap, lane & (E - 1)) : lane & (E - 1);
@@ -1344,6 +1443,19 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
     // block-wide item tables of the fan-out levels (see WarpSmem)
     for (int e = 1; e <= SM::kItemLevels; ++e) {
         const int m = 2 * (Q0 - e + 1), D = m - 2, tn = tri_sz(D);
+        if constexpr (SM::kPairUw) {
+            // child entry k = (i, j): byte offsets of the pairs 2+i, 2+j in the parent's pair array
+            for (int k = threadIdx.x; k < tn; k += blockDim.x) {
+                int i = 0, r = k;
+                while (r >= D - i) {
+                    r -= D - i;
+                    ++i;
+                }
+                tabs[SM::item_off(e) + k] = static_cast<uint32_t>(16 * (2 + i)) |
+                                            (static_cast<uint32_t>(16 * (2 + i + r)) << 16);
+            }
+            continue;
+        }
         for (int it = threadIdx.x; it < (tn << (e - 1)); it += blockDim.x) {
             const int x = it / tn;
             int i = 0, r = it - x * tn;
@@ -1930,7 +2042,7 @@ class PlanImpl final : public Plan {
         // gives bit-identical results.  kWantJobs whole-problem jobs keep the dynamic
         // schedule's tail short even for the 1/8 shard of an 8-GPU run; job states are
         // <= kMaxJobModes modes.
-                const uint64_t want_jobs = range.prefix_jobs ? range.prefix_jobs : kWantJobs;
+        const uint64_t want_jobs = range.prefix_jobs ? range.prefix_jobs : (ninst_ > 1 ? kWantJobsBatch : kWantJobs);
         class_partials_ = range.class_partials;
         c_ = 0;
         if (n_ >= Q0) {
