@@ -295,6 +295,7 @@ __device__ void dfs_elim(const T* P, int q, T* slot, bool write_slot, T* root, c
 #ifndef TOR_NB
 #define TOR_NB 6
 #endif
+
 #ifndef TOR_QD_NB
 #define TOR_QD_NB 2
 #endif
@@ -345,6 +346,8 @@ __device__ void dfs_elim(const T* P, int q, T* slot, bool write_slot, T* root, c
     __syncwarp();
     // ---- trailing update, batch by batch
     T* rootb = root - (total - RT);  // entry k >= total-RT is root entry k-(total-RT)
+    // (a second register set holding the next batch's L2 loads in flight measured slower:
+    // n = 32 DD 84.5 vs 82.5 ms, 168 registers)
     for (int kb = 0;;) {
         T out[NB];
 #pragma unroll
@@ -1184,6 +1187,9 @@ template <class T, int C> struct SplitChunk {
     }
 };
 
+#ifndef TOR_UB_P
+#define TOR_UB_P 3  // producer fan-out levels (3 84.0, 4 84.2, 5 85.0, 6 84.3)
+#endif
 #ifndef TOR_UB
 #define TOR_UB 4  // items per batch, consumer fan-out levels (n=32 DD: 4 84.1 ms, 5 85.0, 3 84.1)
 #endif
@@ -1301,6 +1307,15 @@ template <class T, int E_LVL> struct FanLevel {
         const int g = lane / E;
         const NodeRef nr = node_ref<T>(tabs, E_LVL - 1, x);
         const T* P = sm + nr.off;
+        // item-table words one batch ahead (the first batch's before the pivot chain): the
+        // table read leaves each batch's load -> decode -> load -> update chain
+        constexpr bool kItems = !(Cfg<T>::TMEM && E_LVL == FAN) && sizeof(T) != sizeof(qd);
+        constexpr int UBQ = !Cfg<T>::WS ? TOR_F64_UB : (E_LVL < cons_first<T>() ? TOR_UB_P : TOR_UB);
+        uint32_t wq[UBQ];
+        if constexpr (kItems) {
+#pragma unroll
+            for (int u = 0; u < UBQ; ++u) wq[u] = tabs[WarpSmem<T>::item_off(E_LVL) + lane + 32 * u];
+        }
         const Piv<T> pv = pivot2<T>(P[0], P[1], P[m], tvals[nr.tix]);
         if (g == 0) {
             const uint64_t nm = leaf_mask | (static_cast<uint64_t>((x << 1) | 1) << (Q0 - E_LVL));
@@ -1373,9 +1388,6 @@ template <class T, int E_LVL> struct FanLevel {
         // trailing updates into the level-e buffers: item it = lane + 32 s (x-major)
         constexpr int NE = E * tn;
         constexpr int NIT = (NE + 31) / 32;
-#ifndef TOR_UB_P
-#define TOR_UB_P 3  // producer fan-out levels (3 84.0, 4 84.2, 5 85.0, 6 84.3)
-#endif
         constexpr int UB = sizeof(T) == sizeof(qd) ? TOR_QD_UB
                            : (!Cfg<T>::WS ? TOR_F64_UB : (E_LVL < cons_first<T>() ? TOR_UB_P : TOR_UB));  // items per batch
         const uint32_t* itb = tabs + WarpSmem<T>::item_off(E_LVL) + lane;
@@ -1399,7 +1411,7 @@ template <class T, int E_LVL> struct FanLevel {
 #pragma unroll
             for (int u = 0; u < C; ++u) {
                 const bool ok = !LP || u < C - 1 || lane < NREM;
-                const uint32_t w = ok ? itb[32 * (s0 + u)] : 0u;
+                const uint32_t w = ok ? wq[u] : 0u;
                 const int src = static_cast<int>(w & 0xfffu);
                 const int a = static_cast<int>((w >> 12) & 0x3ffu), b = static_cast<int>(w >> 22);
                 sv[u] = sm[src];
@@ -1407,6 +1419,11 @@ template <class T, int E_LVL> struct FanLevel {
                 uj[u] = uwv[b];
                 wi[u] = uwv[a + m];
                 wj[u] = uwv[b + m];
+            }
+            if constexpr (C == UB && !LP) {  // a main batch: the next batch's words (reads past the
+                                             // level's table stay inside shared memory, unused)
+#pragma unroll
+                for (int u = 0; u < UB; ++u) wq[u] = itb[32 * (s0 + UB + u)];
             }
 #pragma unroll
             for (int u = 0; u < C; ++u) sv[u] = A::rank2_item(sv[u], ui[u], uj[u], wi[u], wj[u]);
