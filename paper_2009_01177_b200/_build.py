@@ -67,7 +67,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
          os.path.join(BUILD, "fixed.log")),
         (["g++"] + CXX_FLAGS + inc + ["-c", os.path.join(CSRC, "host.cpp"), "-o", os.path.join(BUILD, "host.o")],
          os.path.join(BUILD, "host.log")),
-        (["g++"] + CXX_FLAGS + inc + ["-c", os.path.join(CSRC, "capi.cpp"), "-o", os.path.join(BUILD, "capi.o")],
+        (["g++"] + CXX_FLAGS + [f"-D{d}" for d in defines] + inc + ["-c", os.path.join(CSRC, "capi.cpp"), "-o", os.path.join(BUILD, "capi.o")],
          os.path.join(BUILD, "capi.log")),
         (["g++"] + CXX_FLAGS + inc + ["-c", os.path.join(CSRC, "gbsa.cpp"), "-o", os.path.join(BUILD, "gbsa.o")],
          os.path.join(BUILD, "gbsa.log")),

@@ -7,6 +7,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <algorithm>
 #include <atomic>
@@ -303,7 +304,7 @@ class DeviceRun {
   public:
     DeviceRun(int device, int mode, const std::vector<Input>& ins, const WorkRange& range)
         : DeviceRun(device, mode, ins[0].n, static_cast<int>(ins.size()), range,
-                    [&](int i, double* R, int* tsc) { build_R_into(ins[i], mode_words(mode), mode == MODE_DD, R, tsc); }) {}
+                    [&](int i, double* R, int* tsc) { build_R_into(ins[i], mode_words(mode), mode == MODE_DD, R, tsc, true); }) {}
 
     // build(i, R, tsc) writes instance i's exact R (and may throw a validation error: the
     // first failing instance in index order is reported, before anything is launched)
@@ -314,12 +315,21 @@ class DeviceRun {
         std::string err;
         if (staged_acquire(device, mode, n, count, range, &sp_, err) != 0)
             throw HostError(TOR_E_DEVICE, "device/cuda", err);
+        const auto t_acq = std::chrono::steady_clock::now();
         std::vector<int> tsc(count, 0);
-        // about two blocks per host thread: few copy calls, still overlapping
+        // about two build blocks per host thread; their host->device copies go out in a few
+        // large groups (a copy costs ~45 us before its first byte: 32 copies of 0.5 MB ran at
+        // 14 GB/s, 4 copies of 4 MB at the link's ~48 GB/s), each enqueued by the worker that
+        // completes the group's last block -- so copying still overlaps building
         const int kBlock = std::max(64, (count + 2 * HostPool::get().size() - 1) / (2 * HostPool::get().size()));
         const int nblocks = (count + kBlock - 1) / kBlock;
-        std::vector<int> bst(nblocks, 0);
-        std::vector<std::string> berr(nblocks);
+        const int ngroups = std::min(nblocks, 4);
+        std::vector<int> gfirst(ngroups + 1);
+        for (int g = 0; g <= ngroups; ++g) gfirst[g] = static_cast<int>(static_cast<int64_t>(nblocks) * g / ngroups);
+        std::vector<std::atomic<int>> gleft(ngroups);
+        for (int g = 0; g < ngroups; ++g) gleft[g].store(gfirst[g + 1] - gfirst[g]);
+        std::vector<int> gst(ngroups, 0);
+        std::vector<std::string> gerr(ngroups);
         std::vector<std::exception_ptr> bex(nblocks);
         parallel_for(
             nblocks,
@@ -327,13 +337,17 @@ class DeviceRun {
                 const int lo = b * kBlock, hi = std::min(count, lo + kBlock);
                 try {
                     for (int i = lo; i < hi; ++i) build(i, sp_->staging + i * sp_->stride, &tsc[i]);
+                    build_R_fence();  // the builders' streaming stores before the group's copy
                 } catch (...) {
                     bex[b] = std::current_exception();
-                    return;
+                    return;  // the group's copy is never enqueued: the run fails below
                 }
-                bst[b] = staged_upload_part(sp_, lo, hi, berr[b]);
+                const int g = static_cast<int>(std::upper_bound(gfirst.begin(), gfirst.end(), b) - gfirst.begin()) - 1;
+                if (gleft[g].fetch_sub(1) == 1)
+                    gst[g] = staged_upload_part(sp_, gfirst[g] * kBlock, std::min(count, gfirst[g + 1] * kBlock), gerr[g]);
             },
             1);
+        const auto t_built = std::chrono::steady_clock::now();
         for (auto& e : bex)
             if (e) {
                 staged_release(sp_);  // the pinned staging stays valid for copies in flight
@@ -341,16 +355,18 @@ class DeviceRun {
                 std::rethrow_exception(e);
             }
         int st = 0;
-        for (int b = 0; b < nblocks && st == 0; ++b)
-            if (bst[b]) {
-                st = bst[b];
-                err = berr[b];
+        for (int g = 0; g < ngroups && st == 0; ++g)
+            if (gst[g]) {
+                st = gst[g];
+                err = gerr[g];
             }
         if (st == 0) st = staged_launch(sp_, *std::max_element(tsc.begin(), tsc.end()), err);
         if (st != 0) fail_and_release(err);
         launched_ = true;
         if (std::getenv("TOR_DEBUG_TIMING"))
-            std::fprintf(stderr, "[tor] run: prepare+launch %.2f ms\n",
+            std::fprintf(stderr, "[tor] run: acquire %.2f ms, build+copies enqueued %.2f ms, prepare+launch %.2f ms\n",
+                         std::chrono::duration<double, std::milli>(t_acq - t0).count(),
+                         std::chrono::duration<double, std::milli>(t_built - t0).count(),
                          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     }
     DeviceRun(const DeviceRun&) = delete;
@@ -750,22 +766,36 @@ int tor_torontonian_batch(const tor_input* ins, int count, tor_precision prec, i
             validate_raw(&ins[i], 40);
             if (ins[i].n != ins[0].n) throw HostError(TOR_E_INVALID, "torontonian/range", "batch instances must share N");
         };
-        // validation first (the first bad instance in index order, before any device work)
-        parallel_for(count, [&](int i) {
-            shape_check(i);
-            if (prec == TOR_PREC_AUTO) {
+        // validation (the first bad instance in index order) before any device compute: AUTO in
+        // a pass of its own (it also selects the widths); explicit widths inside the blocks that
+        // build R (DeviceRun reports the first failing block's first failing instance and
+        // launches nothing) -- unless there is no usable device, whose error must not hide a
+        // validation error
+        if (prec == TOR_PREC_AUTO) {
+            parallel_for(count, [&](int i) {
+                shape_check(i);
                 as[i] = make_input(ins[i].n, ins[i].a00_upper, ins[i].a01_upper);
                 precision_of(i);
+            });
+        } else {
+            shape_check(0);
+            try {
+                device_check(device);
+            } catch (const HostError&) {
+                parallel_for(count, shape_check);
+                throw;
             }
-        });
+        }
         const auto t1 = std::chrono::steady_clock::now();
         EngineStats st;
         std::vector<int> modes(count, mode);
         std::vector<EngineOut> res(count);
         if (prec != TOR_PREC_AUTO) {
-            // the exact R straight from the caller's arrays (no copies)
+            // the exact R straight from the caller's arrays (no copies), validated block by block
             DeviceRun dr(device, mode, ins[0].n, count, WorkRange{}, [&](int i, double* R, int* tsc) {
-                build_R_raw(ins[i].n, ins[i].a00_upper, ins[i].a01_upper, mode_words(mode), mode == MODE_DD, R, tsc);
+                shape_check(i);
+                build_R_raw(ins[i].n, ins[i].a00_upper, ins[i].a01_upper, mode_words(mode), mode == MODE_DD, R, tsc,
+                            true);
             });
             if (prec != TOR_PREC_FP64)
                 parallel_for(count, [&](int i) {

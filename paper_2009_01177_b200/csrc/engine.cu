@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -2016,7 +2017,7 @@ class PlanImpl final : public Plan {
     int upload_part(const double* R, int lo, int hi, std::string& err) override {
         const size_t words = static_cast<size_t>(tri_sz(2 * n_)) * Arith<T>::K;
         CK(cudaSetDevice(device_));
-        if (lo == 0) CK(cudaEventRecord(ev_[4], st_));
+        if (!up_started_.exchange(true)) CK(cudaEventRecord(ev_[4], st_));  // (debug timing) first copy
         CK(cudaMemcpyAsync(static_cast<double*>(rin_.p) + words * lo, R + words * lo, sizeof(double) * words * (hi - lo),
                            cudaMemcpyHostToDevice, st_));
         return 0;
@@ -2036,6 +2037,7 @@ class PlanImpl final : public Plan {
             CK(cudaGetLastError());
         }
         h2d_bytes_ = sizeof(T) * rt * ninst_;
+        up_started_.store(false);
         return 0;
     }
 
@@ -2372,6 +2374,7 @@ class PlanImpl final : public Plan {
     size_t smem_ = 0, scr_stride_ = 1, work_stride_ = 0, h2d_bytes_ = 0;
     cudaStream_t st_ = nullptr;
     cudaEvent_t ev_[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    std::atomic<bool> up_started_{false};
     DevBuf pool_, tpool_, jobs_, parts_, errw_, ctr_, scr_, work_, res_, rin_;
     double* res_host_ = nullptr;  // pinned: ninst x 5 result words + the breakdown word
     uint64_t launches_ = 0;       // kernels in the launched graph

@@ -6,8 +6,13 @@
 // -ffp-contract=off.
 #include "host.hpp"
 
+#if defined(__x86_64__)
+#include <emmintrin.h>
+#endif
+
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "../../include/tor_capi.h"
 #include "arith.cuh"
@@ -228,63 +233,109 @@ std::vector<double> build_R(const Input& a, int words, bool grid, int* tscale_lo
     return R;
 }
 
-void build_R_into(const Input& a, int words, bool grid, double* R, int* tscale_log2) {
+void build_R_into(const Input& a, int words, bool grid, double* R, int* tscale_log2, bool stream) {
     // std::complex<double> arrays are layout-compatible with interleaved (re, im) doubles
     build_R_raw(a.n, reinterpret_cast<const double*>(a.a00.data()), reinterpret_cast<const double*>(a.a01.data()),
-                words, grid, R, tscale_log2);
+                words, grid, R, tscale_log2, stream);
 }
 
-void build_R_raw(int n, const double* __restrict__ a00, const double* __restrict__ a01, int words, bool grid,
-                 double* __restrict__ R, int* tscale_log2) {
+namespace {
+// Plain or non-temporal 8-byte store.  Pinned staging written with ordinary stores by many
+// host threads stays dirty in their caches, and the GPU's DMA reads of it then run at ~5 GB/s
+// instead of the link's ~50 GB/s (measured on the B200 boxes, tools/probes/h2d_probe.cu);
+// streaming stores put the data in memory.  Callers fence (build_R_fence) before the copy.
+template <bool kStream> inline void put_word(double* p, double v) {
+#if defined(__x86_64__)
+    if constexpr (kStream) {
+        long long bits;
+        std::memcpy(&bits, &v, sizeof(bits));
+        _mm_stream_si64(reinterpret_cast<long long*>(p), bits);
+        return;
+    }
+#endif
+    *p = v;
+}
+template <bool kStream>
+void build_R_impl(int n, const double* __restrict__ a00, const double* __restrict__ a01, int words, bool grid,
+                  double* __restrict__ R, int* tscale_log2);
+}  // namespace
+
+void build_R_fence() {
+#if defined(__x86_64__)
+    _mm_sfence();
+#endif
+}
+
+void build_R_raw(int n, const double* a00, const double* a01, int words, bool grid, double* R, int* tscale_log2,
+                 bool stream) {
+    if (stream) build_R_impl<true>(n, a00, a01, words, grid, R, tscale_log2);
+    else build_R_impl<false>(n, a00, a01, words, grid, R, tscale_log2);
+}
+
+namespace {
+template <bool kStream>
+void build_R_impl(int n, const double* __restrict__ a00, const double* __restrict__ a01, int words, bool grid,
+                  double* __restrict__ R, int* tscale_log2) {
     const int d = 2 * n;
     // entry (r, s), r <= s, of pair rows r = 2i + ri, s = 2j + sj: x + y with
     //   (x_i, x_j): Re P + Re Q   (x_i, p_j): Im Q - Im P   (p_i, x_j): Im P + Im Q   (p_i, p_j): Re P - Re Q
-    // P = I - A00 (diagonal 1 - Re a_ii), Q = -A01, from the upper triangles (i <= j)
-    auto parts = [&](int r, int s, double& x, double& y) {
-        const int i = r >> 1, j = s >> 1;
-        const size_t t = static_cast<size_t>(i) * n - (static_cast<size_t>(i) * (i + 1)) / 2 + j;
-        const double pre = i == j ? 1.0 - a00[2 * t] : -a00[2 * t];
-        const double pim = i == j ? 0.0 : -a00[2 * t + 1];
-        const double qre = -a01[2 * t], qim = -a01[2 * t + 1];
-        switch ((r & 1) * 2 + (s & 1)) {
-            case 0: x = pre; y = qre; break;
-            case 1: x = qim; y = -pim; break;
-            case 2: x = pim; y = qim; break;
-            default: x = pre; y = -qre; break;
-        }
-    };
+    // P = I - A00 (diagonal 1 - Re a_ii), Q = -A01, from the upper triangles (i <= j).
     // grid (fixed-exponent) DD states need max_k R_kk < 3.75 (arith.cuh); larger inputs are
     // scaled by an exact power of two, undone per term on the device (Acc::sc)
     int sc = 0;
     if (grid) {
         double dmax = 0.0;
-        for (int r = 0; r < d; ++r) {
-            double x, y;
-            parts(r, r, x, y);
-            dmax = std::max(dmax, std::fabs(x + y));
+        for (int i = 0; i < n; ++i) {
+            const size_t t = static_cast<size_t>(i) * n - (static_cast<size_t>(i) * (i + 1)) / 2 + i;
+            const double pre = 1.0 - a00[2 * t], qre = -a01[2 * t];
+            dmax = std::max(dmax, std::max(std::fabs(pre + qre), std::fabs(pre + -qre)));
         }
         while (std::ldexp(dmax, -sc) >= 3.75) ++sc;
     }
     if (tscale_log2) *tscale_log2 = sc;
     const double f = std::ldexp(1.0, -sc);  // exact power of two
-    double* e = R;
-    for (int r = 0; r < d; ++r)
-        for (int s = r; s < d; ++s, e += words) {
-            double x, y;
-            parts(r, s, x, y);
-            if (grid) {
-                const dd g = dd_to_grid(x * f, y * f);
-                e[0] = g.hi;
-                e[1] = g.lo;
-            } else {
-                double hi, lo;
-                two_sum(x, y, hi, lo);
-                e[0] = hi;
-                if (words >= 2) e[1] = lo;
-                for (int w = 2; w < words; ++w) e[w] = 0.0;
-            }
+    auto put = [&](double* e, double x, double y) {
+        if (grid) {
+            const dd g = dd_to_grid(x * f, y * f);
+            put_word<kStream>(e, g.hi);
+            put_word<kStream>(e + 1, g.lo);
+        } else {
+            double hi, lo;
+            two_sum(x, y, hi, lo);
+            put_word<kStream>(e, hi);
+            if (words >= 2) put_word<kStream>(e + 1, lo);
+            for (int w = 2; w < words; ++w) put_word<kStream>(e + w, 0.0);
         }
+    };
+    // mode pair (i, j) fills two consecutive entries of pair rows 2i and 2i+1 (three entries for
+    // i == j): both rows are written front to back
+    size_t t = 0;  // packed index of (i, j) in the n x n upper triangles
+    for (int i = 0; i < n; ++i) {
+        const size_t r0 = 2 * static_cast<size_t>(i);
+        double* row0 = R + static_cast<size_t>(words) * (r0 * d - (r0 * (r0 + 1)) / 2 + r0);
+        double* row1 = row0 + static_cast<size_t>(words) * (d - r0);
+        {
+            const double pre = 1.0 - a00[2 * t], pim = 0.0;
+            const double qre = -a01[2 * t], qim = -a01[2 * t + 1];
+            put(row0, pre, qre);
+            put(row0 + words, qim, -pim);
+            put(row1, pre, -qre);
+            row0 += 2 * words;
+            row1 += words;
+            ++t;
+        }
+        for (int j = i + 1; j < n; ++j, ++t, row0 += 2 * words, row1 += 2 * words) {
+            const double pre = -a00[2 * t], pim = -a00[2 * t + 1];
+            const double qre = -a01[2 * t], qim = -a01[2 * t + 1];
+            put(row0, pre, qre);
+            put(row0 + words, qim, -pim);
+            put(row1, pim, qim);
+            put(row1 + words, pre, -qre);
+        }
+    }
 }
+
+}  // namespace
 
 unsigned __int128 total_op_count(int n) {  // flops.cpp:15-31 (Eq. 8)
     unsigned __int128 total = 0, binom = 1;

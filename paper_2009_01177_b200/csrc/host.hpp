@@ -54,9 +54,14 @@ PrecCfg force_width(const Input& a, int width_bits);
 // triangle of the 2n x 2n matrix in pair order (x_0, p_0, x_1, p_1, ...).
 std::vector<double> build_R(const Input& a, int words, bool grid = false, int* tscale_log2 = nullptr);
 // the same into R (tri(2n) * words doubles)
-void build_R_into(const Input& a, int words, bool grid, double* R, int* tscale_log2);
+void build_R_into(const Input& a, int words, bool grid, double* R, int* tscale_log2, bool stream = false);
 // the same from interleaved (re, im) upper triangles (tor_input layout), no Input copy
-void build_R_raw(int n, const double* a00, const double* a01, int words, bool grid, double* R, int* tscale_log2);
+void build_R_raw(int n, const double* a00, const double* a01, int words, bool grid, double* R, int* tscale_log2,
+                 bool stream = false);
+// stream = true writes R with non-temporal stores (pinned staging the GPU reads next: DMA reads
+// of lines still dirty in the host caches are ~10x slower); build_R_fence() orders them before
+// the copy is enqueued
+void build_R_fence();
 
 // Closed-form reference op counters (linalg.hpp:44-57, flops.cpp:9-31).
 void op_counts(int n, uint64_t& mults, uint64_t& adds, uint64_t& recips, uint64_t& rsqrts);
