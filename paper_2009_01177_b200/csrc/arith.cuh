@@ -739,6 +739,59 @@ template <>
 TOR_HD Piv<qd> pivot2<qd>(const qd& s00, const qd& s01, const qd& s11, const qd& t) {
     return qd_pivot_ool(s00, s01, s11, t);
 }
+#if defined(__CUDA_ARCH__)
+// The same pivot for lanes that share it (the warp-cooperative fan-out levels and DFS steps
+// compute one pivot in >= 2 lanes): the lane with role 0 runs the reciprocal square root of
+// s00 and the products with it (u1, s00 rho1), its partner lane ^ xm (role 1, same inputs)
+// that of the determinant and t rhod, then they exchange -- one rsqrt and three products per
+// lane instead of two and four (QD: ~780 instead of ~1090 FP64 instructions per pivot; the
+// same bodies on the same operands, so every value is bit-identical to qd_pivot_ool).
+__device__ __noinline__ Piv<qd> qd_pivot_split_ool(qd s00, qd s01, qd s11, qd t, bool role, int xm) {
+    Piv<qd> p;
+    const qd a = qd_renorm5_bf(s00.x[0], s00.x[1], s00.x[2], s00.x[3], 0.0);
+    p.bad0 = nonpositive(a.x[0]);
+    const qd det = qd_rank2_body<true>(qd{{0.0, 0.0, 0.0, 0.0}}, qd_neg(a), s11, s01, s01);
+    p.bad1 = nonpositive(det.x[0]);
+    qd x, f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        x.x[i] = role ? det.x[i] : a.x[i];
+        f.x[i] = role ? t.x[i] : s01.x[i];
+    }
+    const qd y = qd_rsqrt_body<true>(x);     // rho1 | rhod
+    const qd m1 = qd_mul_body<true>(f, y);   // u1 = s01 rho1 | tn = t rhod
+    const qd m2 = qd_mul_body<true>(a, y);   // s00 rho1 | (unused)
+    qd ar, rd;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double yo = __shfl_xor_sync(0xffffffffu, y.x[i], xm);
+        const double m1o = __shfl_xor_sync(0xffffffffu, m1.x[i], xm);
+        const double m2o = __shfl_xor_sync(0xffffffffu, m2.x[i], xm);
+        p.r1.x[i] = role ? yo : y.x[i];
+        rd.x[i] = role ? y.x[i] : yo;
+        p.u1.x[i] = role ? m1o : m1.x[i];
+        p.tn.x[i] = role ? m1.x[i] : m1o;
+        ar.x[i] = role ? m2o : m2.x[i];
+    }
+    p.r2 = qd_mul_body<true>(ar, rd);
+    return p;
+}
+#endif
+// Pivot shared by the lanes l and l ^ xm (all 32 lanes call it): the split form for QD, the
+// plain pivot otherwise
+template <class T>
+TOR_HD Piv<T> pivot2_shared(const T& s00, const T& s01, const T& s11, const T& t, int lane, int xm) {
+    (void)lane;
+    (void)xm;
+    return pivot2<T>(s00, s01, s11, t);
+}
+#if defined(__CUDA_ARCH__) && !defined(TOR_QD_NO_SPLIT)
+template <>
+__device__ __forceinline__ Piv<qd> pivot2_shared<qd>(const qd& s00, const qd& s01, const qd& s11, const qd& t,
+                                                       int lane, int xm) {
+    return qd_pivot_split_ool(s00, s01, s11, t, (lane & xm) != 0, xm);
+}
+#endif
 // QD pivot-row vector pair in one out-of-line body (one call instead of three)
 struct QdPair {
     qd u, w;

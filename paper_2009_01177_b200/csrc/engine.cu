@@ -97,6 +97,7 @@ template <> struct Cfg<double> {
     static constexpr bool TMEM = false;
     static constexpr bool WS = false;
     static constexpr int WS_MODE = 0;
+    static constexpr bool TSHARE = false;
 };
 template <> struct Cfg<dd> {
     static constexpr int L = 4;
@@ -110,6 +111,7 @@ template <> struct Cfg<dd> {
     static constexpr int WPB = 12;
     static constexpr int MINB = 1;
     static constexpr bool TMEM = true;
+    static constexpr bool TSHARE = false;
 };
 template <> struct Cfg<qd> {
 #ifndef TOR_QD_L
@@ -119,7 +121,17 @@ template <> struct Cfg<qd> {
 #define TOR_QD_MINB 1
 #endif
     static constexpr int L = TOR_QD_L;
-    static constexpr int WPB = 1;
+    // Time-shared areas (TSHARE): a QD warp area is ~50 KB, so only four fit on an SM.  Two warps
+    // (w, w + 4: same SM sub-partition, same TMEM lane quadrant) take turns on one area: a warp
+    // runs the DFS step and the fan-out of its leaf in the area, copies the 32 lane-node states
+    // into its own TMEM columns (21 entries x 8 words per lane), hands the area to its partner
+    // and runs the lane subtrees from TMEM -- 8 warps per SM instead of 4, same per-job
+    // arithmetic and order (bit-identical results).
+#ifndef TOR_QD_TSHARE
+#define TOR_QD_TSHARE 1
+#endif
+    static constexpr bool TSHARE = TOR_QD_TSHARE != 0;
+    static constexpr int WPB = TSHARE ? 8 : 1;
     static constexpr int MINB = TOR_QD_MINB;
     static constexpr bool TMEM = false;
     static constexpr bool WS = false;
@@ -329,7 +341,7 @@ __device__ void dfs_elim(const T* P, int q, T* slot, bool write_slot, T* root, c
     };
     load_batch(0);
     // ---- pivots (all lanes, warp-uniform) and pivot-row vectors
-    const Piv<T> pv = pivot2<T>(p00, p01, p11, t_in);
+    const Piv<T> pv = pivot2_shared<T>(p00, p01, p11, t_in, lane, 1);
     if (lane == 0) {
         if (pv.bad0 || pv.bad1) report_breakdown(err, mask, 2 * nsel + (pv.bad0 ? 0 : 1));
         *t_out = pv.tn;
@@ -605,9 +617,9 @@ template <class T> struct SubReg<T, 1> {
 // Lane subtree rooted at an L-mode view in shared memory: emits the node's own
 // term and all 2^L - 1 extensions.  Branch 0 includes the first view mode (its
 // elimination reads shared memory), branch 1 excludes it (loads the trailing block).
-template <class T, int L, class AC, class E>
-__device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t, bool neg, uint64_t mask, int nsel,
-                                          AC& acc, E* err) {
+template <class T, int L, class AC, class E, class View>
+__device__ __forceinline__ void lane_tree_v(const View& V, const T& t, bool neg, uint64_t mask, int nsel, AC& acc,
+                                            E* err) {
     using A = Arith<T>;
     constexpr int M = 2 * L;
     acc.add(t, neg, nsel);
@@ -616,27 +628,26 @@ __device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t,
         St<T, L - 1> Sn;
         T tn;
         if (br == 0) {
-            const Piv<T> pv = pivot2<T>(S[tri_ix(d, sr, sr)], S[tri_ix(d, sr, sr + 1)], S[tri_ix(d, sr + 1, sr + 1)], t);
+            const Piv<T> pv = pivot2<T>(V(0, 0), V(0, 1), V(1, 1), t);
             const T r1 = pv.r1, u1 = pv.u1, r2 = pv.r2;
             if (pv.bad0 || pv.bad1) report_breakdown(err, mask | bit, 2 * nsel + (pv.bad0 ? 0 : 1));
             tn = pv.tn;
             T u[M], w[M];
 #pragma unroll
             for (int j = 2; j < M; ++j) {
-                A::vec(S[tri_ix(d, sr, sr + j)], S[tri_ix(d, sr + 1, sr + j)], r1, u1, r2, u[j], w[j]);
+                A::vec(V(0, j), V(1, j), r1, u1, r2, u[j], w[j]);
             }
 #pragma unroll
             for (int i = 2; i < M; ++i)
 #pragma unroll
                 for (int j = i; j < M; ++j)
-                    Sn.e[cix<M - 2>(i - 2, j - 2)] =
-                        A::rank2(S[tri_ix(d, sr + i, sr + j)], u[i], u[j], w[i], w[j]);
+                    Sn.e[cix<M - 2>(i - 2, j - 2)] = A::rank2(V(i, j), u[i], u[j], w[i], w[j]);
             acc.add(tn, !neg, nsel + 1);
         } else {
 #pragma unroll
             for (int i = 2; i < M; ++i)
 #pragma unroll
-                for (int j = i; j < M; ++j) Sn.e[cix<M - 2>(i - 2, j - 2)] = S[tri_ix(d, sr + i, sr + j)];
+                for (int j = i; j < M; ++j) Sn.e[cix<M - 2>(i - 2, j - 2)] = V(i, j);
             tn = t;
         }
         SubReg<T, L - 1>::run(Sn, tn, br == 0 ? !neg : neg, br == 0 ? (mask | bit) : mask, nsel + (br == 0), acc,
@@ -644,6 +655,12 @@ __device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t,
     };
 #pragma unroll 1
     for (int br = 0; br < 2; ++br) branch(br);
+}
+template <class T> struct SmemView;
+template <class T, int L, class AC, class E>
+__device__ __forceinline__ void lane_tree(const T* S, int d, int sr, const T& t, bool neg, uint64_t mask, int nsel,
+                                          AC& acc, E* err) {
+    lane_tree_v<T, L, AC, E>(SmemView<T>{S, d, sr}, t, neg, mask, nsel, acc, err);
 }
 
 // ------------------------------------------------------------------ TMEM ----
@@ -695,6 +712,30 @@ template <> __device__ __forceinline__ dd from_u32<dd>(const uint32_t* r) { retu
 template <> __device__ __forceinline__ double from_u32<double>(const uint32_t* r) {
     return __hiloint2double(static_cast<int>(r[1]), static_cast<int>(r[0]));
 }
+__device__ __forceinline__ void to_u32(const qd& v, uint32_t* r) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        r[2 * i] = static_cast<uint32_t>(__double2loint(v.x[i]));
+        r[2 * i + 1] = static_cast<uint32_t>(__double2hiint(v.x[i]));
+    }
+}
+template <> __device__ __forceinline__ qd from_u32<qd>(const uint32_t* r) {
+    qd v;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v.x[i] = __hiloint2double(static_cast<int>(r[2 * i + 1]), static_cast<int>(r[2 * i]));
+    return v;
+}
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr)
+                 : "memory");
+}
+__device__ __forceinline__ void tm_st8(uint32_t taddr, const uint32_t* r) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
 __device__ __forceinline__ void tm_ld2(uint32_t taddr, uint32_t& a, uint32_t& b) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n" : "=r"(a), "=r"(b) : "r"(taddr) : "memory");
 }
@@ -703,13 +744,32 @@ __device__ __forceinline__ void tm_st2(uint32_t taddr, uint32_t a, uint32_t b) {
 }
 // one state entry (U words)
 template <int U> __device__ __forceinline__ void tm_ld_e(uint32_t taddr, uint32_t* r) {
-    if constexpr (U == 4) tm_ld4(taddr, r[0], r[1], r[2], r[3]);
+    if constexpr (U == 8) tm_ld8(taddr, r);
+    else if constexpr (U == 4) tm_ld4(taddr, r[0], r[1], r[2], r[3]);
     else tm_ld2(taddr, r[0], r[1]);
 }
 template <int U> __device__ __forceinline__ void tm_st_e(uint32_t taddr, const uint32_t* r) {
-    if constexpr (U == 4) tm_st4(taddr, r[0], r[1], r[2], r[3]);
+    if constexpr (U == 8) tm_st8(taddr, r);
+    else if constexpr (U == 4) tm_st4(taddr, r[0], r[1], r[2], r[3]);
     else tm_st2(taddr, r[0], r[1]);
 }
+// Lane-state accessors of lane_tree: entry (i, j) of the lane's D-row view from shared memory,
+// or entry (i, j) of the lane's own TMEM row (natural layout, entry k at columns U k), loaded
+// where it is used
+template <class T> struct SmemView {
+    const T* S;
+    int d, sr;
+    __device__ __forceinline__ T operator()(int i, int j) const { return S[tri_ix(d, sr + i, sr + j)]; }
+};
+template <class T, int D> struct TmemView {
+    uint32_t row;
+    __device__ __forceinline__ T operator()(int i, int j) const {
+        uint32_t r[TmU<T>::U];
+        tm_ld_e<TmU<T>::U>(row + static_cast<uint32_t>(TmU<T>::U * cix<D>(i, j)), r);
+        tm_wait_ld();
+        return from_u32<T>(r);
+    }
+};
 
 // (row, col) of flat index k in a packed D-row upper triangle (compile-time)
 __host__ __device__ constexpr int tri_row(int D, int k) {
@@ -1059,7 +1119,8 @@ template <class T> struct WarpSmem {
     static constexpr int kUwEntries = uw_need();
     static constexpr int kDfsT = kUwOff + kUwEntries;  // DFS slot t values (<= 32)
     // (warp-specialised: the DFS t values are producer-private, see kProdEntries)
-    static constexpr int kEntries = kDfsT + (Cfg<T>::WS_MODE == 2 ? 0 : 32);
+    // (time-shared areas: the DFS t values of both warps)
+    static constexpr int kEntries = kDfsT + (Cfg<T>::WS_MODE == 2 ? 0 : (Cfg<T>::TSHARE ? 64 : 32));
     // WS mode 2 producer-private: pivot-row vectors of the DFS and levels 1..3, DFS t
     // values of its two job contexts
     __host__ __device__ static constexpr int prod_uw() {
@@ -1317,7 +1378,8 @@ template <class T, int E_LVL> struct FanLevel {
 #pragma unroll
             for (int u = 0; u < UBQ; ++u) wq[u] = tabs[WarpSmem<T>::item_off(E_LVL) + lane + 32 * u];
         }
-        const Piv<T> pv = pivot2<T>(P[0], P[1], P[m], tvals[nr.tix]);
+        // (lanes l and l ^ E share parent x = l & (E - 1))
+        const Piv<T> pv = pivot2_shared<T>(P[0], P[1], P[m], tvals[nr.tix], lane, E);
         if (g == 0) {
             const uint64_t nm = leaf_mask | (static_cast<uint64_t>((x << 1) | 1) << (Q0 - E_LVL));
             if (pv.bad0 || pv.bad1) report_breakdown(err, nm, 2 * (leaf_sel + __popc(x)) + (pv.bad0 ? 0 : 1));
@@ -1502,8 +1564,15 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         }
     }
     __shared__ uint32_t tmem_base;
+    // time-shared areas: whose turn it is (0 / 1 = warp w < 4 / w >= 4) and who has finished
+    __shared__ volatile int ts_turn[4], ts_done[8];
+    if constexpr (Cfg<T>::TSHARE) {
+        if (threadIdx.x < 4) ts_turn[threadIdx.x] = 0;
+        if (threadIdx.x < 8) ts_done[threadIdx.x] = 0;
+    }
+    constexpr bool kUseTmem = Cfg<T>::TMEM || Cfg<T>::TSHARE;
     uint32_t tm_row = 0;
-    if constexpr (Cfg<T>::TMEM) {
+    if constexpr (kUseTmem) {
         // warp w uses TMEM lanes 32(w%4).. (its lane quadrant) and columns 256(w/4)..
         static_assert(Cfg<T>::WPB == 4 || Cfg<T>::WPB == 8 || Cfg<T>::WPB == 12, "TMEM lane handoff: 4, 8, 12 warps");
         constexpr uint32_t kCols = Cfg<T>::WPB >= 8 ? 512 : 256;
@@ -1536,10 +1605,10 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
     const int pw = Cfg<T>::WS ? (wib & 3) : wib;
     const int ppb = Cfg<T>::WS ? 4 : WPB;  // producers per block
     auto area = [&](int a) { return reinterpret_cast<T*>(smem_raw + SM::kTabBytes + a * SM::kWarpBytes); };
-    T* sm = area(Cfg<T>::WS_MODE == 2 ? pw : (Cfg<T>::WS ? 2 * pw : pw));
+    T* sm = area(Cfg<T>::WS_MODE == 2 ? pw : (Cfg<T>::WS ? 2 * pw : (Cfg<T>::TSHARE ? (wib & 3) : pw)));
     T* tvals = sm + SM::kTOff;
     T* uwv = Cfg<T>::WS_MODE == 2 ? area(8) + pw * SM::kProdEntries : sm + SM::kUwOff;
-    T* dfs_t = Cfg<T>::WS_MODE == 2 ? uwv + SM::kProdUw : sm + SM::kDfsT;
+    T* dfs_t = Cfg<T>::WS_MODE == 2 ? uwv + SM::kProdUw : sm + SM::kDfsT + (Cfg<T>::TSHARE ? 32 * (wib >> 2) : 0);
     T* slots = scratch + static_cast<size_t>(blockIdx.x * ppb + pw) * scratch_stride;
 
     // DFS step + root + fan-out of one leaf of job J into the fan area fsm (buffers +
@@ -1750,6 +1819,14 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
             AccT acc;
             acc.sc = tsc;
             for (uint64_t leaf = 0; leaf < (1ull << D); ++leaf) {
+                if constexpr (Cfg<T>::TSHARE) {
+                    // wait for the area: my turn, or the partner warp has no more leaves.  Every
+                    // lane polls (one broadcast load per trip, a warp-uniform exit): a single polling
+                    // lane left the warp split in two groups that each ran the whole leaf
+                    while (ts_turn[wib & 3] != (wib >> 2) && !ts_done[wib ^ 4]) __nanosleep(64);
+                    __syncwarp();
+                    __threadfence_block();
+                }
                 produce_leaf(J, leaf, tm_row, sm, dfs_t, slots);
                 // lanes: node (FAN, c); TMEM rows hold the nodes of the level-5 lane map
                 const uint64_t leaf_mask = J.mask | (leaf << Q0);
@@ -1760,14 +1837,36 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                 const uint64_t lmask = leaf_mask | (static_cast<uint64_t>(c) << L);
                 const int lsel = leaf_sel + __popc(c);
                 const bool nodeneg = ((nmodes - lsel) & 1) != 0;  // term sign (-1)^(n - |Z|)
-                lane_tree<T, L, AccT>(sm + nr.off, 2 * L, 0, vt, nodeneg, lmask, lsel, acc, err);
+                if constexpr (Cfg<T>::TSHARE) {
+                    // the lane's node state (a contiguous packed 2L-row triangle) -> its TMEM row,
+                    // then the area goes to the partner warp
+                    constexpr int U = TmU<T>::U;
+#pragma unroll
+                    for (int k = 0; k < tri_sz(2 * L); ++k) {
+                        uint32_t r[U];
+                        to_u32(sm[nr.off + k], r);
+                        tm_st_e<U>(tm_row + static_cast<uint32_t>(U * k), r);
+                    }
+                    tm_wait_st();
+                    __syncwarp();
+                    __threadfence_block();
+                    ts_turn[wib & 3] = (wib >> 2) ^ 1;  // (every lane stores the same value: no divergence)
+                    lane_tree_v<T, L, AccT>(TmemView<T, 2 * L>{tm_row}, vt, nodeneg, lmask, lsel, acc, err);
+                } else {
+                    lane_tree<T, L, AccT>(sm + nr.off, 2 * L, 0, vt, nodeneg, lmask, lsel, acc, err);
+                }
                 acc.flush();
                 __syncwarp();
             }
             write_partial(acc, job);
         }
+        if constexpr (Cfg<T>::TSHARE) {
+            __syncwarp();
+            __threadfence_block();
+            ts_done[wib] = 1;
+        }
     }
-    if constexpr (Cfg<T>::TMEM) {
+    if constexpr (kUseTmem) {
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         __syncthreads();
         if ((threadIdx.x >> 5) == 0)
@@ -2123,7 +2222,7 @@ class PlanImpl final : public Plan {
             using SM = WarpSmem<T>;
             constexpr int WPB = Cfg<T>::WPB;
             smem_ = Cfg<T>::WS_MODE == 2 ? SM::kTabBytes + SM::kWarpBytes * 8 + sizeof(T) * SM::kProdEntries * 4
-                                         : SM::kTabBytes + SM::kWarpBytes * WPB;
+                                         : SM::kTabBytes + SM::kWarpBytes * (Cfg<T>::TSHARE ? WPB / 2 : WPB);
             for (auto* kfn : {subtree_kernel<T, false>, subtree_kernel<T, true>}) {
                 CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
                 CK(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
