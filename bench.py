@@ -206,11 +206,11 @@ def ref_sample(m, precision: str, seconds: float):
         # torontonian_partial over partition(n, rank, nproc) slices: each rank's share keeps
         # the popcount mix of the full sum; calibrate the sample to ~`seconds`
         width = {"128": "128", "dd": "128", "256": "256", "qd": "256"}.get(precision, "128")
-        nproc = 1 << 30
+        nproc = 1 << max(5, min(30, n - 8))  # >= 256 subset-terms per partition rank
         done, secs = ref.partial_sample(m, width, nproc, 0, threads, threads)
         rate = done / max(secs, 1e-9)
         target = max(threads, int(rate * seconds))
-        nranks = threads * max(1, round(target / max(done, 1)))
+        nranks = min(threads * max(1, round(target / max(done, 1))), nproc - threads)
         done, secs = ref.partial_sample(m, width, nproc, threads, nranks, threads)
         return dict(value=done / secs, cores=threads, kind="reference",
                     sample=f"torfp torontonian_partial<{'2' if width == '128' else '4'}> (fixed-{width}) over "

@@ -18,3 +18,9 @@ timeout 300 python tools/prof_one.py 4 128 > gpurun_out/prof_plain.log 2>&1 && \
 timeout 1500 ncu --set full --metrics sm__sass_thread_inst_executed_op_dfma_pred_on.sum,sm__sass_thread_inst_executed_op_dadd_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --import-source on -k regex:subtree -c 1 -o gpurun_out/prof_round python tools/prof_one.py 4 128 > gpurun_out/ncu_full.log 2>&1
 echo "ncu exit $?" >> gpurun_out/ncu_full.log
 tail -2 gpurun_out/pytest_gpu.log; tail -1 gpurun_out/smoke.log
+# QD (n = 28 sub-instance of config 4) and fp64 (config-3 batch) kernels: one ncu --set full capture each
+bash tools/ncu_full.sh r02_qd_n28 4 256 28 > gpurun_out/ncu_qd.log 2>&1
+bash tools/ncu_cfg3.sh r02_cfg3_fp64 fp64 > gpurun_out/ncu_cfg3.log 2>&1
+for w in cfg1-n16-fp64 cfg2-n20-dd; do
+  timeout 900 python bench.py --workload $w --steps 20 --warmup 5 --cpu-sample-seconds 5 > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err
+done
