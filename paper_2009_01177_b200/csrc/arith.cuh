@@ -785,7 +785,7 @@ TOR_HD Piv<T> pivot2_shared(const T& s00, const T& s01, const T& s11, const T& t
     (void)xm;
     return pivot2<T>(s00, s01, s11, t);
 }
-#if defined(__CUDA_ARCH__) && !defined(TOR_QD_NO_SPLIT)
+#if defined(__CUDA_ARCH__)
 template <>
 __device__ __forceinline__ Piv<qd> pivot2_shared<qd>(const qd& s00, const qd& s01, const qd& s11, const qd& t,
                                                        int lane, int xm) {
