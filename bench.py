@@ -212,13 +212,13 @@ def ref_sample(m, precision: str, seconds: float):
         target = max(threads, int(rate * seconds))
         nranks = min(threads * max(1, round(target / max(done, 1))), nproc - threads)
         done, secs = ref.partial_sample(m, width, nproc, threads, nranks, threads)
-        return dict(value=done / secs, cores=threads, kind="reference",
+        return dict(value=done / secs, unit=UNIT, cores=threads, kind="reference",
                     sample=f"torfp torontonian_partial<{'2' if width == '128' else '4'}> (fixed-{width}) over "
                            f"{nranks} of {nproc} partition ranks of n={n}: {done} subset-terms in {secs:.2f} s "
                            f"on {threads} threads")
     from oracle import port
     done, secs = port.partial_sample(m, 128 if precision in ("128", "dd") else 256, seconds, threads)
-    return dict(value=done / secs, cores=threads, kind="port",
+    return dict(value=done / secs, unit=UNIT, cores=threads, kind="port",
                 sample=f"oracle/tor_oracle.c fixed-point restatement: {done} subset-terms in {secs:.2f} s")
 
 
@@ -234,7 +234,7 @@ def ref_batch_sample(ms, precision: str, seconds: float):
     if not ref.available():
         from oracle import port
         done, secs = port.partial_sample(ms[0], 128, seconds, threads)
-        return dict(value=done / secs, cores=threads, kind="port",
+        return dict(value=done / secs, unit=UNIT, cores=threads, kind="port",
                     sample=f"oracle/tor_oracle.c fixed-point restatement: {done} subset-terms in {secs:.2f} s")
     done, t0, k = 0, time.perf_counter(), 0
     if precision == "fp64":
@@ -249,7 +249,7 @@ def ref_batch_sample(ms, precision: str, seconds: float):
             k += 1
         what = f"torfp torontonian(Bits128, workers={threads}) on {k} of the {len(ms)} config-3 items"
     secs = time.perf_counter() - t0
-    return dict(value=k * (1 << n) / secs, cores=threads, kind="reference",
+    return dict(value=k * (1 << n) / secs, unit=UNIT, cores=threads, kind="reference",
                 sample=f"{what}: {k * (1 << n)} subset-terms in {secs:.2f} s")
 
 

@@ -15,6 +15,13 @@ torontonian_partial<W>, torontonian.cpp:72-103) over prefix classes of the top k
   k = 6,  classes 0 and 0x2A (2^24 subsets each), fixed-128: shard-width classes, which the
          default n = 30 schedule (c = 18) runs as 4096 jobs each with 3 DFS levels.
 
+And the headline instance itself (config 4, all 32 click modes):
+
+  k = 6,  class 0x15 (2^26 subsets), fixed-128: one of the 64 top-level classes of the measured
+         n = 32 double-double run -- the default schedule (c = 18, jobs of 14 modes, five
+         producer DFS levels), i.e. exactly what bench.py times and what each rank of a
+         multi-GPU run computes (~30 min on 8 cores, as 256 sub-classes of k = 14).
+
 Writes tests/golden/reference_deep.json (~20 min on 8 cores: the k = 6 classes are evaluated as their 64 sub-classes of k = 12 so the harness threads over them).
 """
 from __future__ import annotations
@@ -67,11 +74,12 @@ def main():
         gold = json.load(open(OUT))
     C = gold["cases"]
     todo = [("n30_k12_fff", 12, 0xFFF, (128, 256), 0), ("n30_k6_00", 6, 0x00, (128,), 6),
-            ("n30_k6_2a", 6, 0x2A, (128,), 6)]
+            ("n30_k6_2a", 6, 0x2A, (128,), 6), ("n32_k6_15", 6, 0x15, (128,), 8)]
     for name, k, cls, widths, split in todo:
         if name in C:
             continue
-        C[name] = slice_case(m, k, cls, widths, split)
+        inst = W.load_config_instance(4) if name.startswith("n32") else m
+        C[name] = slice_case(inst, k, cls, widths, split)
         with open(OUT, "w") as f:
             json.dump(gold, f, indent=1, sort_keys=True)
     print("wrote", OUT)

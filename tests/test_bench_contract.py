@@ -40,6 +40,17 @@ def test_committed_bench_line():
     assert ref["e2e"]["h2d_bytes_per_step"] == 0 and ref["cpu_baseline"]["value"] == ref["value"]
 
 
+def test_committed_round2_bench_lines():
+    d = json.load(open(os.path.join(ROOT, "profiles", "r02_bench.json")))
+    _check_line(d, cpu=True)
+    assert d["config"]["workload"] == "cfg4-n32-dd" and d["n_gpus"] == 1 and d["steps"] == 20 and d["warmup"] == 5
+    assert d["cpu_baseline"]["unit"] == d["unit"] and d["clocks"]["reasons"] == []
+    ref = json.load(open(os.path.join(ROOT, "profiles", "r02_bench_reference.json")))
+    assert ref["impl"] == "reference" and ref["metric"] == d["metric"] and ref["config"]["workload"] == "cfg4-n32-dd"
+    for w in ("cfg4-n32-qd", "cfg5-n40-dd", "cfg3-batch-fp64", "cfg3-batch-dd"):
+        _check_line(json.load(open(os.path.join(ROOT, "profiles", f"r02_bench_{w}.json"))), cpu=True)
+
+
 @pytest.mark.gpu
 def test_bench_runs_and_prints_one_line():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1", "--warmup", "3",
@@ -65,3 +76,4 @@ def test_reference_arm_runs_on_host():
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "subset-terms/s"
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["kind"] in ("reference", "port")
+    assert d["cpu_baseline"]["unit"] == d["unit"]

@@ -112,6 +112,32 @@ def test_n30_shard_width_class_vs_reference(cls_name, cls):
     assert ok, f"QD slice vs fixed-128: err = {rel:.3g} sum|t|"
 
 
+def test_n32_headline_class_vs_reference():
+    """The headline instance (config 4, n = 32, double-double), one of its 64 top-level prefix
+    classes (k = 6, class 0x15, 2^26 subsets) through the default schedule -- c = 18, jobs of
+    14 modes, five producer DFS levels: the pipeline bench.py times and the share of one rank
+    of a multi-GPU run -- against the reference's fixed-128 class sum."""
+    case = _deep().get("n32_k6_15")
+    if case is None:
+        pytest.skip("n32_k6_15 golden missing")
+    m = W.load_config_instance(4)
+    g = case["widths"]["128"]
+    want = fixed_value(g["raw"], g["frac_bits"])
+    [c] = T.torontonian_classes(m, "128", 6, 0x15, 0x16)
+    ok, rel = within(words_value(c["words"]), want, c["sum_abs"], "dd")
+    assert ok, f"class partial: err = {rel:.3g} sum|t|"
+    assert c["sum_abs"] == pytest.approx(g["sum_abs"], rel=1e-12)
+    assert c["term_count"] == 1 << 26
+    # the same class inside the whole run's per-class partials (what bench.py's ranks all-gather)
+    parts = T.torontonian_classes(m, "128", 6, 0x14, 0x18)
+    assert parts[1]["words"] == c["words"]
+    # the quad-double pipeline (time-shared areas, jobs of 14 modes) on the same class: the
+    # fixed-128 golden bounds the check
+    [q] = T.torontonian_classes(m, "256", 6, 0x15, 0x16)
+    ok, rel = within(words_value(q["words"]), want, q["sum_abs"], "dd")
+    assert ok, f"QD class partial vs fixed-128: err = {rel:.3g} sum|t|"
+
+
 # ----------------------------------------------------------- class partials / devices --
 @pytest.mark.parametrize("prec", ["128", "256", "fp64"])
 def test_class_partials_fold_bit_identical(prec):
