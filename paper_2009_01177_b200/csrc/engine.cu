@@ -1564,9 +1564,6 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
     __shared__ uint32_t tmem_base;
     // time-shared areas: whose turn it is (0 / 1 = warp w < 4 / w >= 4) and who has finished
     __shared__ volatile int ts_turn[4], ts_done[8];
-#ifndef TOR_QD_LOCKSTEP
-#define TOR_QD_LOCKSTEP 1
-#endif
     __shared__ unsigned long long ts_ls[2];
     if (threadIdx.x < 2) ts_ls[threadIdx.x] = 0ull;
     if constexpr (Cfg<T>::TSHARE) {
@@ -1679,10 +1676,8 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
         constexpr int CF = Cfg<T>::WS ? cons_first<T>() : FAN + 1;
         if constexpr (CF > 1) FanLevel<T, 1>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
         if constexpr (CF > 2) FanLevel<T, 2>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
-        if constexpr (Cfg<T>::TSHARE && TOR_QD_LOCKSTEP >= 3) ts_sync(4ull * (++ts_k));
         if constexpr (CF > 3) FanLevel<T, 3>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
         if constexpr (CF > 4) FanLevel<T, 4>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
-        if constexpr (Cfg<T>::TSHARE && TOR_QD_LOCKSTEP >= 3) ts_sync(4ull * (++ts_k));
         if constexpr (CF > 5) FanLevel<T, 5>::run(fsm, ftv, uwv, tabs, leaf_mask, leaf_sel, perr, tm_slot);
     };
     using AccT = Acc<T, kScaled>;
@@ -1838,13 +1833,13 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                     while (ts_turn[wib & 3] != (wib >> 2) && !ts_done[wib ^ 4]) __nanosleep(64);
                     __syncwarp();
                     __threadfence_block();
-                    // The four holders of a phase start their fan-out together: the warps that run
-                    // the same code at the same time share its instruction fetches (n = 28: 72.4 ->
-                    // 71.0 ms; a desynchronised pool of areas ran at half the speed).  Arrival
-                    // counter per group; a finished warp credits all later rounds.
+                    // The four holders of a phase start their fan-out together: warps that run the
+                    // same code at the same time share its instruction fetches (n = 32: 1285 -> 1176
+                    // ms, n = 28: 72.9 -> 71.0; a desynchronised pool of areas ran at half the speed;
+                    // further meetings per leaf gain nothing).  Arrival counter per group; a finished
+                    // warp credits all later rounds.
                     ++ts_k;
                     ts_sync(4ull * ts_k);
-
                 }
                 produce_leaf(J, leaf, tm_row, sm, dfs_t, slots);
                 // lanes: node (FAN, c); TMEM rows hold the nodes of the level-5 lane map
@@ -1870,10 +1865,6 @@ __global__ void __launch_bounds__(32 * Cfg<T>::WPB, Cfg<T>::MINB)
                     __syncwarp();
                     __threadfence_block();
                     ts_turn[wib & 3] = (wib >> 2) ^ 1;  // (every lane stores the same value: no divergence)
-#if TOR_QD_LOCKSTEP >= 2
-                    ++ts_k;
-                    ts_sync(4ull * ts_k);  // and their lane subtrees
-#endif
                     lane_tree_v<T, L, AccT>(TmemView<T, 2 * L>{tm_row}, vt, nodeneg, lmask, lsel, acc, err);
                 } else {
                     lane_tree<T, L, AccT>(sm + nr.off, 2 * L, 0, vt, nodeneg, lmask, lsel, acc, err);
